@@ -1,0 +1,39 @@
+# Build everything in-tree (the .so files travel to the GPU box with gpurun).
+#   make            -> libbspmm.so (sm_100a), liboracle.so, libsynth.so
+#   make lib|oracle|synth
+NVCC      ?= /usr/local/cuda/bin/nvcc
+CC        := /usr/bin/gcc
+CXX       := /usr/bin/g++
+PKG       := paper_1903_11409_b200
+CSRC      := $(PKG)/csrc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+# no fast-math: FTZ off, IEEE div/sqrt, FMA contraction only where written
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+             -ftz=false -prec-div=true -prec-sqrt=true -Iinclude -Xptxas -v
+LIB       := $(PKG)/libbspmm.so
+CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu
+HOST_SRCS := $(CSRC)/partition.cpp $(CSRC)/plan.cpp
+HDRS      := include/bspmm.h $(CSRC)/internal.h $(CSRC)/ptx.cuh
+
+all: lib oracle synth
+
+lib: $(LIB)
+
+$(LIB): $(CU_SRCS) $(HOST_SRCS) $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) $(HOST_SRCS) 2> build/ptxas.log || (cat build/ptxas.log; false)
+	@grep -E "registers|spill|smem" build/ptxas.log | sed 's/^ptxas info *: //' > build/ptxas_summary.txt || true
+
+oracle: oracle/liboracle.so
+oracle/liboracle.so: oracle/oracle.c
+	$(CC) -O2 -std=c11 -fPIC -shared -fopenmp -ffp-contract=off -fno-fast-math -o $@ $< -lm
+
+synth: synth/libsynth.so
+synth/libsynth.so: synth/synth.c
+	$(CC) -O2 -std=c11 -fPIC -shared -fopenmp -o $@ $<
+
+clean:
+	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so
+	rm -rf build
+
+.PHONY: all lib oracle synth clean
