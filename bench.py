@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""bench.py — Batched SpMM (arXiv 1903.11409) on B200: GFLOP/s (2*nnz*k,
+PAPER.md:341) and effective HBM GB/s for BASELINE.json config 5 (batch 65536
+molecule-like graphs, k=256), sharded by nnz*k over N GPUs.
+
+A step = one pass of the whole hot path over the batch: the device batch-offset
+builder (row a-1) + the batched CSR SpMM kernel (rows a-3..a-6); the partition
+(row a-7) is computed once per job on the host.  Inputs (5.4 GB at N=1) are far
+larger than the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "Batched SpMM GFLOP/s & effective HBM GB/s (% of B200 peak) at 1/2/4/8 GPUs"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def alg_bytes(n_rows: int, nnz: int, k: int, batch: int) -> int:
+    """Algorithmic HBM bytes of one SpMM launch: every node row
+    costs 8k + 4 + 8d bytes (B row read once, C row written once, one row pointer,
+    d (col, val) pairs) plus 8 B of row offset per matrix."""
+    return 8 * k * n_rows + 4 * (n_rows + 1) + 8 * nnz + 8 * (batch + 1)
+
+
+def offsets_bytes(batch: int) -> int:
+    return 4 * batch + 8 * (batch + 1)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """NVML sampler of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock"}
+
+    def __init__(self, index: int, period: float = 0.002):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.dev = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.dev, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+        self.period = period
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.dev, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(self.dev))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml-unavailable"], "samples": 0}
+        names = [v for b, v in self.REASONS.items() if self.reasons & b and b != 0x1]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def cpu_baseline(b, budget_s: float = 12.0):
+    """The oracle (oracle/, fp64 loops, OpenMP across matrices) as it stands, on a
+    bounded prefix of this rank's graphs, on the host cores."""
+    import oracle
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    ncal = min(b.batch, 512)
+    def run(nb):
+        g1 = int(b.row_off[nb])
+        z1 = int(b.row_ptr[g1])
+        t0 = time.perf_counter()
+        oracle.spmm(b.k, b.row_off[:nb + 1], None, b.row_ptr[:g1 + 1], b.col[:z1], b.vals[:z1], b.B[:g1])
+        return time.perf_counter() - t0, 2.0 * z1 * b.k
+    dt, _ = run(ncal)
+    nb = int(min(b.batch, max(ncal, ncal * budget_s / max(dt, 1e-6))))
+    dt, fl = run(nb)
+    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {nb} of {b.batch} graphs of the rank-0 shard (config 5), fp64 oracle.spmm, "
+                      f"{dt:.2f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    cid = args.config
+    c = synth.CONFIGS[cid]
+    cores = len(os.sched_getaffinity(0))
+    # bounded sample per step: a fixed prefix of the batch, ~0.25 s of oracle work
+    b = synth.config(cid, i0=0, i1=min(c["batch"], 2048))
+    nb = b.batch
+    def step():
+        oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+    t0 = time.perf_counter()
+    step()
+    one = time.perf_counter() - t0
+    if one > 0:
+        nb = max(16, min(b.batch, int(b.batch * 0.25 / one)))
+    g1 = int(b.row_off[nb]); z1 = int(b.row_ptr[g1])
+    ro, rp, col, vals, B = b.row_off[:nb + 1], b.row_ptr[:g1 + 1], b.col[:z1], b.vals[:z1], b.B[:g1]
+    def step():
+        oracle.spmm(b.k, ro, None, rp, col, vals, B)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    flops = 2.0 * z1 * b.k
+    val = flops / dt / 1e9
+    sample = f"first {nb} graphs of config {cid} per step (fp64 oracle.spmm, OpenMP over matrices)"
+    out = {"metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": synth.CONFIG_NAMES[cid], "global_batch": c["batch"], "k": c["k"],
+                      "parallelism": "cpu-oracle"},
+           "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def load_traffic(cid: int):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            e = d.get(f"c{cid}")
+            if e and e.get("dram_bytes_per_launch"):
+                return float(e["dram_bytes_per_launch"]), e.get("source", p)
+        except Exception:
+            pass
+    return None, None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="bspmm", choices=["bspmm", "reference"])
+    ap.add_argument("--config", type=int, default=5, help="BASELINE.json config id (bench line: 5)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kt", type=int, default=0)
+    ap.add_argument("--warps", type=int, default=0)
+    ap.add_argument("--ctas", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_1903_11409_b200 as bs
+    from paper_1903_11409_b200 import dist as bdist
+
+    rank, world, local = bdist.env_world()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    bdist.init("nccl", dev)
+    assert world == args.gpus or world == 1, "--gpus must match WORLD_SIZE"
+
+    cid = args.config
+    c = synth.CONFIGS[cid]
+    seed = synth.BASE_SEED + cid
+    # a-7: every rank computes the same split from the per-graph nnz counts
+    n_all, z_all = synth.counts(c["kind"], c["params"], seed, 0, c["batch"])
+    nnz_off_all = np.zeros(c["batch"] + 1, np.int64)
+    np.cumsum(z_all, out=nnz_off_all[1:])
+    i0, i1 = bdist.shard_of(nnz_off_all, c["k"], rank, world)
+    b = synth.config(cid, i0=i0, i1=i1)
+    k = b.k
+    h = bs.Handle(dev)
+    h.set_hints(int(b.sizes.max()) if b.batch else 0, int(b.nnz.max()) if b.batch else 0)
+    if args.kt or args.warps or args.ctas:
+        h.set_tuning(args.kt, args.warps, args.ctas)
+
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    sizes, row_ptr, col, vals, B = T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)
+    C = torch.empty((b.n_rows, k), dtype=torch.float32, device=dev)
+    ro = torch.empty(b.batch + 1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        h.build_offsets(sizes, out=ro)                   # a-1
+        if ev is not None:
+            ev[0].record(stream)
+        h.csr(ro, None, row_ptr, col, vals, B, C)         # a-3..a-6
+        if ev is not None:
+            ev[1].record(stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+    plan = h.last_plan()
+    K = args.steps
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = h.launch_count()
+    bdist.barrier(dev)
+    torch.cuda.synchronize(dev)
+    with Clocks(dev.index) as clk:
+        t0.record(stream)
+        for s in range(K):
+            step(kev[s])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    bdist.barrier(dev)
+    launches = h.launch_count() - launches0
+    ms_rank = t0.elapsed_time(t1) / K
+    spmm_ms_rank = float(np.mean([a.elapsed_time(e) for a, e in kev]))
+    ms = bdist.max_over_ranks(ms_rank, dev)
+    spmm_ms = bdist.max_over_ranks(spmm_ms_rank, dev)
+    NNZ_total = int(nnz_off_all[-1])
+    N_total = int(n_all.sum())
+    flops = 2.0 * NNZ_total * k
+    bytes_step = alg_bytes(N_total, NNZ_total, k, c["batch"]) + offsets_bytes(c["batch"])
+    value = flops / (ms / 1e3) / 1e9
+    hbm_gbs = bytes_step / (ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    # roofline of the dominant kernel on this rank (the SpMM), per launch
+    spmm_bytes = alg_bytes(b.n_rows, b.n_nnz, k, b.batch)
+    achieved = spmm_bytes / (spmm_ms_rank / 1e3) / 1e9
+    traffic, tsrc = load_traffic(cid) if world == 1 else (None, None)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "spmm_csr_kernel", "alg_bytes_per_launch": spmm_bytes,
+            "launch_ms": spmm_ms_rank, "peak_source": peak_src, "traffic_source": tsrc,
+            "share_of_step": spmm_ms_rank / ms_rank}
+
+    # e2e through the public API on HOST buffers (pinned): H2D inputs + D2H C inside the region
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        hs, hrp, hc, hv, hB = pin(b.sizes), pin(b.row_ptr), pin(b.col), pin(b.vals), pin(b.B)
+        hC = torch.empty((b.n_rows, k), dtype=torch.float32).pin_memory()
+        del C, B
+        torch.cuda.empty_cache()
+        h.csr_host(hs, hrp, hc, hv, hB, hC)              # warm-up (allocates the device mirror)
+        bdist.barrier(dev)
+        t = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            h.csr_host(hs, hrp, hc, hv, hB, hC)
+        e2e_s = (time.perf_counter() - t) / args.e2e_steps
+        e2e_s = bdist.max_over_ranks(e2e_s, dev)
+        h2d = bdist.sum_over_ranks(hs.numel() * 4 + hrp.numel() * 4 + hc.numel() * 4 + hv.numel() * 4 +
+                                   hB.numel() * 4, dev)
+        d2h = bdist.sum_over_ranks(hC.numel() * 4, dev)
+        e2e = {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+               "path": "bspmm_csr_host (pinned host buffers, chunked H2D/compute/D2H overlap)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(b)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-mol graphs, U[-1,1) values)",
+            "config": {"workload": synth.CONFIG_NAMES[cid], "global_batch": c["batch"], "k": k,
+                       "rows": N_total, "nnz": NNZ_total, "parallelism": f"batch-sharded x{world} (nnz*k split)",
+                       "l2": "inputs larger than L2 (no flush needed)", "plan": plan},
+            "hbm_gbs": hbm_gbs, "hbm_frac_of_measured": hbm_gbs / peak,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,234 @@
+/*
+ * bspmm.h — C ABI of the B200-native Batched SpMM library (libbspmm.so).
+ *
+ * The operation (§IV, "Batched Algorithm for SpMM", lines 240-264,
+ * and the GCN use of it, Fig. algo:graph_conv_batched, lines 304-321):
+ * for every matrix i of a mini-batch, in ONE launch,
+ *
+ *     C_i = A_i * B_i          ("SpMM computes C = AB")
+ *
+ * with A_i an n_i x n_i sparse adjacency matrix (square; graph
+ * convention a_uu = 1, a_vu = 1 for an edge u->v) stored as CSR
+ * (rpt / colids / values, Fig. algo:code_swa_spmm_csr :196-207)
+ * or as a TF SparseTensor (interleaved (row, col) index pairs + values,
+ * PAPER.md:74, Fig. algo:code_swa_spmm_st :175-185, entries unsorted :141),
+ * and B_i / C_i dense n_i x k fp32 row-major (PAPER.md:101 C[rid][j]); k is
+ * uniform across the batch.
+ *
+ * Batch layout (the "reshape to (m_X * batchsize) x n_X"):
+ * the dense rows of all matrices are concatenated.  Matrix i owns the global
+ * rows [row_off[i], row_off[i] + n_i) of B and C.  row_off replaces the
+ * paper's host-built pointer arrays; it is int64.
+ *
+ * Conventions (every entry point):
+ *  - All functions return bspmm_status_t; nothing is thrown across the ABI.
+ *  - Pointers marked "dev" are device pointers on the handle's device, owned
+ *    by the caller (typically torch tensors); "host" pointers are host memory.
+ *    The library never frees caller memory.  The handle owns only its
+ *    workspace (grown on demand, freed by bspmm_destroy) and BORROWS the
+ *    stream given to bspmm_create / bspmm_set_stream.
+ *  - Calls on device pointers are asynchronous on the handle's stream: they
+ *    enqueue kernels and return.  Inputs must stay alive and unmodified until
+ *    the stream reaches that point.  Device faults surface from a later call,
+ *    bspmm_sync or bspmm_destroy (BSPMM_ERROR_CUDA).
+ *  - Host-side checks: NULL where required, batch < 0, k < 1, ld < k.
+ *    With BSPMM_VALIDATE the library also checks every index/offset on the
+ *    device and SYNCHRONISES at the end of the call to report
+ *    BSPMM_ERROR_INDEX.  Without it, out-of-range indices are undefined
+ *    behaviour (as in cuSPARSE).
+ *  - Degenerate inputs are legal: batch = 0 is a no-op; n_i = 0 writes
+ *    nothing; rows with no entries are written as +0.0 by the same kernel
+ *    (the paper's "set matrix C to O", PAPER.md:95/:177/:198, without a
+ *    separate initialisation launch).  C is OVERWRITTEN
+ *    (no alpha/beta).  Rows between row_off[i] + n_i and row_off[i+1]
+ *    (padding) are never touched.  Duplicate (row, col) entries are summed.
+ *  - Fast path: k % 4 == 0, ldb % 4 == 0, ldc % 4 == 0 and 16-byte aligned
+ *    B and C (float4 lanes, TMA bulk staging).  Anything else runs the scalar
+ *    path; that is not an error.
+ *  - A handle is not thread-safe; distinct handles are independent.
+ *  - Multi-GPU: no ABI change.  One handle per rank/device, called on the
+ *    rank's contiguous sub-batch (bspmm_partition), offsets rebased to 0.
+ */
+#ifndef BSPMM_H_
+#define BSPMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define BSPMM_API __attribute__((visibility("default")))
+#else
+#define BSPMM_API
+#endif
+
+typedef struct bspmm_handle_s* bspmm_handle_t;
+
+typedef enum {
+  BSPMM_SUCCESS = 0,
+  BSPMM_ERROR_INVALID_VALUE = 1, /* NULL where required, batch<0, k<1, ld<k, bad flags   */
+  BSPMM_ERROR_OUT_OF_MEMORY = 2, /* workspace growth failed                              */
+  BSPMM_ERROR_CUDA = 3,          /* CUDA API / launch / async error; see last_error_string */
+  BSPMM_ERROR_INDEX = 4,         /* BSPMM_VALIDATE found an index or offset out of range  */
+  BSPMM_ERROR_NOT_SUPPORTED = 5  /* device is not sm_100 (B200), or no device             */
+} bspmm_status_t;
+
+#define BSPMM_VALIDATE 0x1u /* device pass checking every index; synchronising; off by default */
+
+/* Launch plan ("decides whether the cache blocking is
+ * applied and how many threads are assigned"), re-derived for sm_100a: a unit
+ * of work is (matrix i, k-tile t); persistent CTAs walk the units. */
+typedef struct {
+  int32_t kt;             /* k-tile width in columns (column cache blocking) */
+  int32_t tiles;          /* p = ceil(k / kt) column blocks per matrix    */
+  int32_t lanes;          /* lanes per row: the sub-warp, see bspmm_subwarp  */
+  int32_t vec;            /* 1: float4 lanes + TMA bulk staging; 0: scalar lanes + cp.async     */
+  int32_t chunks;         /* float4 (vec) or float (scalar) column chunks per lane              */
+  int32_t stages;         /* shared-memory ring depth per CTA                                   */
+  int32_t stage_b_bytes;  /* B-tile capacity per stage (rows * kt * 4 must fit to be staged)    */
+  int32_t stage_s_bytes;  /* sparse-structure capacity per stage (rpt + (col,val) pairs)        */
+  int32_t smem_bytes;     /* dynamic shared memory per CTA                                      */
+  int32_t threads;        /* CTA size: 1 producer warp + consumer warps                         */
+  int32_t grid;           /* persistent CTAs launched                                           */
+  int32_t max_rows;       /* planning assumption for max n_i (hint or default)                  */
+  int64_t units;          /* batch * tiles                                                      */
+} bspmm_plan_t;
+
+/* ---- lifetime -------------------------------------------------------- */
+
+/* Creates a handle on `device` (cudaSetDevice is NOT left changed).  stream is
+ * a cudaStream_t (NULL = legacy default stream), borrowed.  flags: 0 or
+ * BSPMM_VALIDATE.  Errors: INVALID_VALUE (out NULL, bad flags),
+ * NOT_SUPPORTED (no device / not compute capability 10.0), CUDA. */
+BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* stream, unsigned flags);
+
+/* Synchronises the handle's stream, frees the workspace.  NULL is a no-op. */
+BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h);
+
+/* Re-targets the borrowed stream (e.g. torch's current stream per call). */
+BSPMM_API bspmm_status_t bspmm_set_stream(bspmm_handle_t h, void* stream);
+
+/* Planner hints (host scalars, optional; 0 = unknown).  max_rows: max n_i
+ * in upcoming batches; max_nnz: max entries of one A_i.  Matrices larger than
+ * the plan's stage capacity still run correctly, reading B from global memory
+ * directly (the paper's "case 3"). */
+BSPMM_API bspmm_status_t bspmm_set_hints(bspmm_handle_t h, int32_t max_rows, int64_t max_nnz);
+
+/* Tuning override for experiments: kt (multiple of 4 on the vec path, 0 =
+ * auto), consumer warps per CTA (0 = auto), CTAs per SM (0 = auto). */
+BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t consumer_warps,
+                                          int32_t ctas_per_sm);
+
+/* Waits for all work enqueued by this handle; surfaces asynchronous errors. */
+BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h);
+
+/* ---- the hot path ---------------------------------------------------- */
+
+/* Batched CSR SpMM (SWA SpMM for CSR, Fig.
+ * algo:code_swa_spmm_csr; batched per PAPER.md:259-264):
+ *   for i in [0, batch), r in [0, n_i), c in [0, k):
+ *     C[(row_off[i]+r)*ldc + c] = sum_{e = row_ptr[g]}^{row_ptr[g+1]-1}
+ *                                  vals[e] * B[(row_off[i]+col_idx[e])*ldb + c],
+ *     g = row_off[i] + r, accumulated in fp32 FMA in storage order from +0.0.
+ *  row_off  [batch+1] dev int64, or NULL: then `sizes` is required and the
+ *           library builds packed offsets itself (bspmm_build_offsets).
+ *  sizes    [batch]   dev int32 n_i, or NULL: n_i = row_off[i+1] - row_off[i].
+ *  row_ptr  [row_off[batch]+1] dev int32: block-diagonal CSR row pointer
+ *           holding ABSOLUTE positions into col_idx / vals.
+ *  col_idx  [nnz] dev int32 LOCAL column ids, 0 <= c < n_i (square A_i).
+ *  vals     [nnz] dev fp32.
+ *  B        [row_off[batch] x ldb] dev fp32 row-major, ldb >= k.
+ *  C        same shape with ldc >= k; must not alias B.
+ * Errors: INVALID_VALUE, CUDA, INDEX (VALIDATE only). */
+BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                   const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
+                                   const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc);
+
+/* Batched COO / SparseTensor SpMM (Fig.
+ * algo:code_swa_spmm_st).  The entries of A_i are [nnz_off[i], nnz_off[i+1])
+ * of idx / vals, in ANY order.  They are first converted on the device to
+ * canonical CSR (stable by (row, col): duplicates keep their input order) and
+ * then multiplied by the CSR kernel, so the result is deterministic (the
+ * paper's atomic accumulation, is not).
+ *  nnz_off     [batch+1] dev int64.
+ *  idx         [nnz][2] dev int32: (row, col) LOCAL pairs, interleaved
+ *              exactly as TF SparseTensor ids (rid = ids[2e],
+ *              cid = ids[2e+1]).
+ *  total_rows  host: row_off[batch] (sizes the CSR row pointer).
+ *  total_nnz   host: nnz_off[batch].
+ *  csr_*_out   dev, nullable as a group: when non-NULL the built CSR is
+ *              written there ([total_rows+1], [total_nnz], [total_nnz]),
+ *              otherwise into handle workspace.
+ * row_off may be NULL (then built from sizes); nnz_off is required. */
+BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                   const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
+                                   const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc,
+                                   int64_t total_rows, int64_t total_nnz, int32_t* csr_row_ptr_out,
+                                   int32_t* csr_col_out, float* csr_val_out);
+
+/* COO -> CSR alone (hot-path row a-2; exported for the bit-exact tests).
+ * Output order per matrix: by (row, col, original position); row_ptr holds
+ * absolute positions (nnz_off[i] + local); padding rows between matrices get
+ * empty ranges; row_ptr[row_off[batch]] = nnz_off[batch].  vals are moved
+ * bitwise.  row_off must be given (dev int64). */
+BSPMM_API bspmm_status_t bspmm_coo2csr(bspmm_handle_t h, int32_t batch, const int64_t* row_off,
+                                       const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
+                                       const float* vals, int64_t total_rows, int64_t total_nnz,
+                                       int32_t* row_ptr_out, int32_t* col_out, float* val_out);
+
+/* Batch-offset builder (hot-path row a-1): offsets_out[0] = 0,
+ * offsets_out[i+1] = offsets_out[i] + sizes[i], int64, on the device
+ * (replaces the host pointer arrays + H2D copy of PAPER.md:281/:343).
+ * sizes [batch] dev int32, offsets_out [batch+1] dev int64. */
+BSPMM_API bspmm_status_t bspmm_build_offsets(bspmm_handle_t h, int32_t batch, const int32_t* sizes,
+                                             int64_t* offsets_out);
+
+/* End-to-end call on HOST buffers (packed layout, ldb = ldc = k): copies the
+ * inputs host->device (pinned memory recommended), builds offsets, runs the
+ * CSR kernel and copies C back, pipelined in row chunks across copy and
+ * compute streams; returns when C_host is complete (synchronous).
+ *  sizes_host [batch], row_ptr_host [total_rows+1] (absolute),
+ *  col_host / vals_host [total_nnz], B_host / C_host [total_rows x k]. */
+BSPMM_API bspmm_status_t bspmm_csr_host(bspmm_handle_t h, int32_t batch, int32_t k, const int32_t* sizes_host,
+                                        const int32_t* row_ptr_host, const int32_t* col_host,
+                                        const float* vals_host, const float* B_host, float* C_host,
+                                        int64_t total_rows, int64_t total_nnz);
+
+/* ---- host-only helpers (no device needed) ----------------------------- */
+
+/* Multi-GPU partition (hot-path row a-7): contiguous graph ranges balanced
+ * by cost c_i = nnz_i * k.  With P_j = sum_{i<j} c_i and T = P_batch:
+ * split[0] = 0, split[parts] = batch, and for 0 < r < parts split[r] is the
+ * smallest j in [0, batch] with P_j * parts >= r * T (if T == 0,
+ * floor(r * batch / parts)).  Rank r owns graphs [split[r], split[r+1]).
+ * nnz_off [batch+1] HOST int64; split_out [parts+1] HOST int32. */
+BSPMM_API bspmm_status_t bspmm_partition(int32_t batch, const int64_t* nnz_off, int32_t k, int32_t parts,
+                                         int32_t* split_out);
+
+/* The paper's subWarp rule: 32 if n_B > 16, else the
+ * smallest power of two >= n_B.  Returns 0 for n_B < 1. */
+BSPMM_API int32_t bspmm_subwarp(int32_t n_B);
+
+/* The launch plan bspmm_csr would use for (k, batch, aligned) on a device
+ * with `num_sms` SMs and `smem_per_cta` bytes of opt-in shared memory
+ * (max_rows / max_nnz: hints, 0 = unknown; kt_override / warps / ctas_per_sm:
+ * tuning, 0 = auto).  Pure host function. */
+BSPMM_API bspmm_status_t bspmm_plan(int32_t k, int32_t batch, int32_t aligned, int32_t max_rows, int64_t max_nnz,
+                                    int32_t num_sms, int32_t smem_per_cta, int32_t kt_override,
+                                    int32_t consumer_warps, int32_t ctas_per_sm, bspmm_plan_t* out);
+
+/* The plan used by the most recent bspmm_csr / bspmm_coo on this handle. */
+BSPMM_API bspmm_status_t bspmm_last_plan(bspmm_handle_t h, bspmm_plan_t* out);
+
+/* Kernel launches issued by this handle since creation (for bench claims). */
+BSPMM_API int64_t bspmm_launch_count(bspmm_handle_t h);
+
+BSPMM_API const char* bspmm_status_string(bspmm_status_t s);
+BSPMM_API const char* bspmm_last_error_string(bspmm_handle_t h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSPMM_H_ */

@@ -1,0 +1,239 @@
+"""B200-native Batched SpMM (arXiv 1903.11409), Python binding.
+
+Argument marshalling only: every step of the hot path runs in libbspmm.so
+(include/bspmm.h).  torch supplies device memory and streams.  Importing this
+package fails loudly when the CUDA extension is missing; there is no CPU
+fallback.
+
+    import paper_1903_11409_b200 as bs
+    h = bs.Handle()                       # cuda:current, torch's current stream
+    C = h.csr(row_off, None, row_ptr, col, vals, B)     # C_i = A_i B_i, one launch
+    C = h.coo(None, sizes, nnz_off, idx, vals, B, total_rows=N)
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BspmmError, Plan, lib
+
+__all__ = ["Handle", "BspmmError", "Plan", "partition", "subwarp", "plan", "default_handle", "header_symbols",
+           "LIB_PATH"]
+
+LIB_PATH = _lib.LIB_PATH
+header_symbols = _lib.header_symbols
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(t, name, dtype, device, ndim=None):
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.device != device:
+        raise ValueError(f"{name} must be on {device}, got {t.device}")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must have {ndim} dims")
+
+
+class Handle:
+    """One library handle per device (not thread-safe).  Calls enqueue on torch's
+    current stream of the handle's device and return without synchronising."""
+
+    def __init__(self, device=None, validate: bool = False):
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self._h = ctypes.c_void_p()
+        st = lib.bspmm_create(ctypes.byref(self._h), self.device.index, None, _lib.VALIDATE if validate else 0)
+        if st != _lib.SUCCESS:
+            raise BspmmError(st, "bspmm_create")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.bspmm_destroy(h)
+            self._h = None
+
+    # ---- plumbing ----------------------------------------------------------
+    def _stream(self):
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        lib.bspmm_set_stream(self._h, ctypes.c_void_p(s))
+
+    def _raise(self, st, where):
+        if st != _lib.SUCCESS:
+            raise BspmmError(st, where, lib.bspmm_last_error_string(self._h).decode())
+
+    def set_hints(self, max_rows: int = 0, max_nnz: int = 0):
+        self._raise(lib.bspmm_set_hints(self._h, int(max_rows), int(max_nnz)), "bspmm_set_hints")
+
+    def set_tuning(self, kt: int = 0, consumer_warps: int = 0, ctas_per_sm: int = 0):
+        self._raise(lib.bspmm_set_tuning(self._h, int(kt), int(consumer_warps), int(ctas_per_sm)),
+                    "bspmm_set_tuning")
+
+    def sync(self):
+        self._raise(lib.bspmm_sync(self._h), "bspmm_sync")
+
+    def last_plan(self) -> dict:
+        p = Plan()
+        self._raise(lib.bspmm_last_plan(self._h, ctypes.byref(p)), "bspmm_last_plan")
+        return p.as_dict()
+
+    def launch_count(self) -> int:
+        return int(lib.bspmm_launch_count(self._h))
+
+    # ---- hot path ------------------------------------------------------------
+    def build_offsets(self, sizes: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Row a-1: int64 exclusive scan of int32 sizes, [batch+1], on the device."""
+        _check(sizes, "sizes", torch.int32, self.device, 1)
+        batch = sizes.shape[0]
+        if out is None:
+            out = torch.empty(batch + 1, dtype=torch.int64, device=self.device)
+        _check(out, "out", torch.int64, self.device, 1)
+        assert out.shape[0] == batch + 1 and sizes.is_contiguous() and out.is_contiguous()
+        self._stream()
+        self._raise(lib.bspmm_build_offsets(self._h, batch, _ptr(sizes), _ptr(out)), "bspmm_build_offsets")
+        return out
+
+    def csr(self, row_off: Optional[torch.Tensor], sizes: Optional[torch.Tensor], row_ptr: torch.Tensor,
+            col: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None,
+            k: Optional[int] = None, batch: Optional[int] = None) -> torch.Tensor:
+        """Batched CSR SpMM: C_i = A_i B_i for all i in one launch (bspmm_csr).
+        B, C: 2-D fp32 [rows, ld] with unit column stride; k defaults to B.shape[1]."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("row_ptr", row_ptr, torch.int32), ("col", col, torch.int32),
+                            ("vals", vals, torch.float32), ("B", B, torch.float32), ("C", C, torch.float32)):
+            _check(t, name, dt, dev)
+        if batch is None:
+            batch = (row_off.shape[0] - 1) if row_off is not None else sizes.shape[0]
+        if k is None:
+            k = B.shape[1]
+        if C is None:
+            C = torch.empty((B.shape[0], k), dtype=torch.float32, device=dev)
+        assert B.stride(1) == 1 and C.stride(1) == 1, "B and C need unit column stride"
+        self._stream()
+        st = lib.bspmm_csr(self._h, batch, k, _ptr(row_off), _ptr(sizes), _ptr(row_ptr), _ptr(col), _ptr(vals),
+                           _ptr(B), B.stride(0), _ptr(C), C.stride(0))
+        self._raise(st, "bspmm_csr")
+        return C
+
+    def coo(self, row_off: Optional[torch.Tensor], sizes: Optional[torch.Tensor], nnz_off: torch.Tensor,
+            idx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None,
+            k: Optional[int] = None, total_rows: Optional[int] = None, csr_out=None) -> torch.Tensor:
+        """Batched COO/SparseTensor SpMM (bspmm_coo): device COO->CSR, then the CSR kernel.
+        idx: int32 [nnz, 2] (row, col) local pairs.  csr_out: optional (row_ptr, col, vals) tensors."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("nnz_off", nnz_off, torch.int64), ("idx", idx, torch.int32),
+                            ("vals", vals, torch.float32), ("B", B, torch.float32), ("C", C, torch.float32)):
+            _check(t, name, dt, dev)
+        batch = nnz_off.shape[0] - 1
+        if k is None:
+            k = B.shape[1]
+        if total_rows is None:
+            total_rows = B.shape[0]
+        if C is None:
+            C = torch.empty((B.shape[0], k), dtype=torch.float32, device=dev)
+        rp_o, col_o, val_o = csr_out if csr_out is not None else (None, None, None)
+        self._stream()
+        st = lib.bspmm_coo(self._h, batch, k, _ptr(row_off), _ptr(sizes), _ptr(nnz_off), _ptr(idx), _ptr(vals),
+                           _ptr(B), B.stride(0), _ptr(C), C.stride(0), int(total_rows), int(idx.shape[0]),
+                           _ptr(rp_o), _ptr(col_o), _ptr(val_o))
+        self._raise(st, "bspmm_coo")
+        return C
+
+    def coo2csr(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], nnz_off: torch.Tensor,
+                idx: torch.Tensor, vals: torch.Tensor, total_rows: int):
+        """Row a-2 alone: canonical CSR (row_ptr, col, vals) built on the device."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("nnz_off", nnz_off, torch.int64), ("idx", idx, torch.int32),
+                            ("vals", vals, torch.float32)):
+            _check(t, name, dt, dev)
+        nnz = idx.shape[0]
+        rp = torch.empty(total_rows + 1, dtype=torch.int32, device=dev)
+        col = torch.empty(nnz, dtype=torch.int32, device=dev)
+        v = torch.empty(nnz, dtype=torch.float32, device=dev)
+        self._stream()
+        st = lib.bspmm_coo2csr(self._h, nnz_off.shape[0] - 1, _ptr(row_off), _ptr(sizes), _ptr(nnz_off), _ptr(idx),
+                               _ptr(vals), int(total_rows), int(nnz), _ptr(rp), _ptr(col), _ptr(v))
+        self._raise(st, "bspmm_coo2csr")
+        return rp, col, v
+
+    def csr_host(self, sizes: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, vals: np.ndarray, B: np.ndarray,
+                 C: Optional[np.ndarray] = None) -> np.ndarray:
+        """End-to-end on host buffers (bspmm_csr_host): H2D, offsets, SpMM, D2H, pipelined; synchronous.
+        Arrays may be numpy arrays or CPU torch tensors (pinned for full copy overlap)."""
+        def arr(x, dt):
+            if isinstance(x, torch.Tensor):
+                assert x.device.type == "cpu" and x.is_contiguous()
+                assert x.dtype == {np.int32: torch.int32, np.float32: torch.float32}[dt]
+                return x, ctypes.c_void_p(x.data_ptr())
+            x = np.ascontiguousarray(x, dtype=dt)
+            return x, _np_ptr(x)
+        sizes, p_s = arr(sizes, np.int32)
+        row_ptr, p_rp = arr(row_ptr, np.int32)
+        col, p_c = arr(col, np.int32)
+        vals, p_v = arr(vals, np.float32)
+        B, p_B = arr(B, np.float32)
+        N, k = B.shape
+        if C is None:
+            C = np.empty((N, k), dtype=np.float32)
+        C, p_C = arr(C, np.float32)
+        self._stream()
+        st = lib.bspmm_csr_host(self._h, int(sizes.shape[0]), int(k), p_s, p_rp, p_c, p_v, p_B, p_C, int(N),
+                                int(col.shape[0]))
+        self._raise(st, "bspmm_csr_host")
+        return C
+
+
+_default = {}
+
+
+def default_handle(device=None) -> Handle:
+    idx = torch.cuda.current_device() if device is None else torch.device(device).index
+    if idx not in _default:
+        _default[idx] = Handle(idx)
+    return _default[idx]
+
+
+# ---- host-only helpers (no GPU needed) -------------------------------------------
+
+def partition(nnz_off, k: int, parts: int) -> np.ndarray:
+    """Row a-7: contiguous nnz*k-balanced split of graphs over `parts` ranks."""
+    no = np.ascontiguousarray(nnz_off, dtype=np.int64)
+    out = np.zeros(parts + 1, dtype=np.int32)
+    st = lib.bspmm_partition(no.shape[0] - 1, _np_ptr(no), int(k), int(parts), _np_ptr(out))
+    if st != _lib.SUCCESS:
+        raise BspmmError(st, "bspmm_partition")
+    return out
+
+
+def subwarp(n_B: int) -> int:
+    """The paper's subWarp rule."""
+    return int(lib.bspmm_subwarp(int(n_B)))
+
+
+def plan(k: int, batch: int, aligned: bool = True, max_rows: int = 0, max_nnz: int = 0, num_sms: int = 148,
+         smem_per_cta: int = 232448, kt: int = 0, consumer_warps: int = 0, ctas_per_sm: int = 0) -> dict:
+    """The launch plan bspmm_csr would use (pure host)."""
+    p = Plan()
+    st = lib.bspmm_plan(int(k), int(batch), int(bool(aligned)), int(max_rows), int(max_nnz), int(num_sms),
+                        int(smem_per_cta), int(kt), int(consumer_warps), int(ctas_per_sm), ctypes.byref(p))
+    if st != _lib.SUCCESS:
+        raise BspmmError(st, "bspmm_plan")
+    return p.as_dict()

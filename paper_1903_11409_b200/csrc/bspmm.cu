@@ -1,0 +1,445 @@
+// bspmm.cu — the C ABI (include/bspmm.h): handle, validation, workspace,
+// planning and launches; plus the end-to-end host-buffer path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.h"
+
+using namespace bspmm;
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+bspmm_status_t fail_cuda(bspmm_handle_t h, cudaError_t e, const char* where) {
+  if (h) h->err = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? BSPMM_ERROR_OUT_OF_MEMORY : BSPMM_ERROR_CUDA;
+}
+bspmm_status_t fail(bspmm_handle_t h, bspmm_status_t s, const char* msg) {
+  if (h) h->err = msg;
+  return s;
+}
+
+#define CK(h, expr)                                        \
+  do {                                                     \
+    cudaError_t e_ = (expr);                               \
+    if (e_ != cudaSuccess) return fail_cuda(h, e_, #expr); \
+  } while (0)
+
+inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// grow a device buffer (synchronises the handle's streams before freeing)
+bspmm_status_t grow(bspmm_handle_t h, void** buf, size_t* cap, size_t need) {
+  if (need <= *cap) return BSPMM_SUCCESS;
+  if (*buf) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (h->s_h2d) CK(h, cudaStreamSynchronize(h->s_h2d));
+    if (h->s_d2h) CK(h, cudaStreamSynchronize(h->s_d2h));
+    CK(h, cudaFree(*buf));
+    *buf = nullptr;
+    *cap = 0;
+  }
+  size_t sz = al256(std::max(need, *cap + *cap / 2));
+  CK(h, cudaMalloc(buf, sz));
+  *cap = sz;
+  return BSPMM_SUCCESS;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bspmm_status_t check_validate_flag(bspmm_handle_t h) {
+  int host = 0;
+  CK(h, cudaMemcpyAsync(&host, h->dev_flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (host) {
+    h->err = "BSPMM_VALIDATE: index/offset out of range (flag " + std::to_string(host) + ")";
+    return BSPMM_ERROR_INDEX;
+  }
+  return BSPMM_SUCCESS;
+}
+
+bspmm_status_t plan_for(bspmm_handle_t h, int32_t batch, int32_t k, bool aligned, bspmm_plan_t* plan) {
+  bspmm_status_t st = make_plan(k, batch, aligned, h->hint_rows, h->hint_nnz, h->num_sms, h->smem_optin,
+                                h->tune_kt, h->tune_warps, h->tune_ctas, plan);
+  if (st != BSPMM_SUCCESS) return fail(h, st, "planner rejected the arguments");
+  h->last_plan = *plan;
+  return BSPMM_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+BSPMM_API const char* bspmm_status_string(bspmm_status_t s) {
+  switch (s) {
+    case BSPMM_SUCCESS: return "BSPMM_SUCCESS";
+    case BSPMM_ERROR_INVALID_VALUE: return "BSPMM_ERROR_INVALID_VALUE";
+    case BSPMM_ERROR_OUT_OF_MEMORY: return "BSPMM_ERROR_OUT_OF_MEMORY";
+    case BSPMM_ERROR_CUDA: return "BSPMM_ERROR_CUDA";
+    case BSPMM_ERROR_INDEX: return "BSPMM_ERROR_INDEX";
+    case BSPMM_ERROR_NOT_SUPPORTED: return "BSPMM_ERROR_NOT_SUPPORTED";
+  }
+  return "BSPMM_UNKNOWN_STATUS";
+}
+
+BSPMM_API const char* bspmm_last_error_string(bspmm_handle_t h) { return h ? h->err.c_str() : "null handle"; }
+
+BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* stream, unsigned flags) {
+  if (!out) return BSPMM_ERROR_INVALID_VALUE;
+  *out = nullptr;
+  if (flags & ~BSPMM_VALIDATE) return BSPMM_ERROR_INVALID_VALUE;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return BSPMM_ERROR_NOT_SUPPORTED;
+  }
+  if (device < 0 || device >= n) return BSPMM_ERROR_INVALID_VALUE;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return BSPMM_ERROR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return BSPMM_ERROR_NOT_SUPPORTED;  // built for sm_100a only
+  bspmm_handle_t h = new (std::nothrow) bspmm_handle_s();
+  if (!h) return BSPMM_ERROR_OUT_OF_MEMORY;
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(stream);
+  h->flags = flags;
+  h->num_sms = prop.multiProcessorCount;
+  h->smem_optin = (int)prop.sharedMemPerBlockOptin;
+  DeviceGuard g(device);
+  if (cudaMalloc(&h->dev_flag, sizeof(int)) != cudaSuccess) {
+    delete h;
+    return BSPMM_ERROR_OUT_OF_MEMORY;
+  }
+  cudaMemset(h->dev_flag, 0, sizeof(int));
+  *out = h;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
+  if (!h) return BSPMM_SUCCESS;
+  bspmm_status_t st = BSPMM_SUCCESS;
+  {
+    DeviceGuard g(h->device);
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) st = BSPMM_ERROR_CUDA;
+    if (h->s_h2d) cudaStreamSynchronize(h->s_h2d), cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamSynchronize(h->s_d2h), cudaStreamDestroy(h->s_d2h);
+    for (auto& e : h->ev)
+      if (e) cudaEventDestroy(e);
+    if (h->ws) cudaFree(h->ws);
+    if (h->hbuf) cudaFree(h->hbuf);
+    if (h->dev_flag) cudaFree(h->dev_flag);
+  }
+  delete h;
+  return st;
+}
+
+BSPMM_API bspmm_status_t bspmm_set_stream(bspmm_handle_t h, void* stream) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  h->stream = static_cast<cudaStream_t>(stream);
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_set_hints(bspmm_handle_t h, int32_t max_rows, int64_t max_nnz) {
+  if (!h || max_rows < 0 || max_nnz < 0) return BSPMM_ERROR_INVALID_VALUE;
+  h->hint_rows = max_rows;
+  h->hint_nnz = max_nnz;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t warps, int32_t ctas_per_sm) {
+  if (!h || kt < 0 || warps < 0 || warps > 16 || ctas_per_sm < 0 || ctas_per_sm > 4) return BSPMM_ERROR_INVALID_VALUE;
+  h->tune_kt = kt;
+  h->tune_warps = warps;
+  h->tune_ctas = ctas_per_sm;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  DeviceGuard g(h->device);
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (h->s_h2d) CK(h, cudaStreamSynchronize(h->s_h2d));
+  if (h->s_d2h) CK(h, cudaStreamSynchronize(h->s_d2h));
+  CK(h, cudaGetLastError());
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_last_plan(bspmm_handle_t h, bspmm_plan_t* out) {
+  if (!h || !out) return BSPMM_ERROR_INVALID_VALUE;
+  *out = h->last_plan;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API int64_t bspmm_launch_count(bspmm_handle_t h) { return h ? h->launches : -1; }
+
+BSPMM_API bspmm_status_t bspmm_build_offsets(bspmm_handle_t h, int32_t batch, const int32_t* sizes,
+                                             int64_t* offsets_out) {
+  if (!h || batch < 0 || !offsets_out || (batch > 0 && !sizes)) return BSPMM_ERROR_INVALID_VALUE;
+  DeviceGuard g(h->device);
+  if ((h->flags & BSPMM_VALIDATE) && batch > 0) {
+    CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
+    CK(h, launch_validate_sizes(batch, sizes, h->dev_flag, h->stream));
+    h->launches++;
+    bspmm_status_t st = check_validate_flag(h);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  CK(h, launch_offsets(batch, sizes, offsets_out, h->stream));
+  h->launches++;
+  return BSPMM_SUCCESS;
+}
+
+static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                               const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
+                               const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc,
+                               bool validate) {
+  if (validate) {
+    CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
+    CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr, col_idx, h->dev_flag, h->stream));
+    h->launches++;
+    bspmm_status_t st = check_validate_flag(h);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  const bool aligned = (k % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C);
+  bspmm_plan_t plan;
+  bspmm_status_t st = plan_for(h, batch, k, aligned, &plan);
+  if (st != BSPMM_SUCCESS) return st;
+  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc};
+  CK(h, launch_spmm_csr(a, plan, h->stream));
+  if (plan.units > 0) h->launches++;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                   const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
+                                   const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || k < 1 || ldb < k || ldc < k) return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1 or ld<k");
+  if (batch == 0) return BSPMM_SUCCESS;
+  if ((!row_off && !sizes) || !row_ptr || !col_idx || !vals || !B || !C)
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  if (B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
+  DeviceGuard g(h->device);
+  if (!row_off) {
+    bspmm_status_t st = grow(h, &h->ws, &h->ws_bytes, al256((size_t)(batch + 1) * 8));
+    if (st != BSPMM_SUCCESS) return st;
+    int64_t* ro = static_cast<int64_t*>(h->ws);
+    st = bspmm_build_offsets(h, batch, sizes, ro);
+    if (st != BSPMM_SUCCESS) return st;
+    return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc,
+                    (h->flags & BSPMM_VALIDATE) != 0);
+  }
+  return csr_impl(h, batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc,
+                  (h->flags & BSPMM_VALIDATE) != 0);
+}
+
+// workspace layout for the COO path: [row_off][row_ptr][col][val][keys x2][pay x2]
+struct CooWs {
+  int64_t* row_off;
+  int32_t* row_ptr;
+  int32_t* col;
+  float* val;
+  uint64_t* keys;
+  uint32_t* pay;
+};
+
+static bspmm_status_t coo_workspace(bspmm_handle_t h, int32_t batch, int64_t N, int64_t NNZ, bool need_ro,
+                                    bool need_csr, CooWs* w) {
+  size_t off = 0;
+  const size_t o_ro = off;
+  off += need_ro ? al256((size_t)(batch + 1) * 8) : 0;
+  const size_t o_rp = off;
+  off += need_csr ? al256((size_t)(N + 1) * 4) : 0;
+  const size_t o_col = off;
+  off += need_csr ? al256((size_t)NNZ * 4) : 0;
+  const size_t o_val = off;
+  off += need_csr ? al256((size_t)NNZ * 4) : 0;
+  const size_t o_keys = off;
+  off += al256((size_t)2 * NNZ * 8);
+  const size_t o_pay = off;
+  off += al256((size_t)2 * NNZ * 4);
+  bspmm_status_t st = grow(h, &h->ws, &h->ws_bytes, std::max<size_t>(off, 256));
+  if (st != BSPMM_SUCCESS) return st;
+  char* b = static_cast<char*>(h->ws);
+  w->row_off = need_ro ? reinterpret_cast<int64_t*>(b + o_ro) : nullptr;
+  w->row_ptr = need_csr ? reinterpret_cast<int32_t*>(b + o_rp) : nullptr;
+  w->col = need_csr ? reinterpret_cast<int32_t*>(b + o_col) : nullptr;
+  w->val = need_csr ? reinterpret_cast<float*>(b + o_val) : nullptr;
+  w->keys = reinterpret_cast<uint64_t*>(b + o_keys);
+  w->pay = reinterpret_cast<uint32_t*>(b + o_pay);
+  return BSPMM_SUCCESS;
+}
+
+static bspmm_status_t coo2csr_impl(bspmm_handle_t h, int32_t batch, const int64_t* row_off, const int32_t* sizes,
+                                   const int64_t* nnz_off, const int32_t* idx, const float* vals, int64_t NNZ,
+                                   int32_t* rp, int32_t* col, float* val, const CooWs& w) {
+  if (h->flags & BSPMM_VALIDATE) {
+    CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
+    CK(h, launch_validate_coo(batch, row_off, sizes, nnz_off, idx, h->dev_flag, h->stream));
+    h->launches++;
+    bspmm_status_t st = check_validate_flag(h);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  const int32_t cap = coo_smem_cap(h->hint_nnz, h->smem_optin);
+  CK(h, launch_coo2csr(batch, row_off, sizes, nnz_off, idx, vals, rp, col, val, w.keys, w.pay, NNZ, cap,
+                       h->stream));
+  h->launches++;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_coo2csr(bspmm_handle_t h, int32_t batch, const int64_t* row_off,
+                                       const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
+                                       const float* vals, int64_t total_rows, int64_t total_nnz,
+                                       int32_t* row_ptr_out, int32_t* col_out, float* val_out) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || total_rows < 0 || total_nnz < 0 || total_nnz > INT32_MAX)
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "bad batch / totals");
+  if (batch == 0) return BSPMM_SUCCESS;
+  if (!row_off || !nnz_off || !row_ptr_out || (total_nnz > 0 && (!idx || !vals || !col_out || !val_out)))
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  DeviceGuard g(h->device);
+  CooWs w;
+  bspmm_status_t st = coo_workspace(h, batch, total_rows, total_nnz, false, false, &w);
+  if (st != BSPMM_SUCCESS) return st;
+  return coo2csr_impl(h, batch, row_off, sizes, nnz_off, idx, vals, total_nnz, row_ptr_out, col_out, val_out, w);
+}
+
+BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                   const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
+                                   const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc,
+                                   int64_t total_rows, int64_t total_nnz, int32_t* csr_row_ptr_out,
+                                   int32_t* csr_col_out, float* csr_val_out) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || k < 1 || ldb < k || ldc < k || total_rows < 0 || total_nnz < 0 || total_nnz > INT32_MAX)
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1, ld<k or bad totals");
+  if (batch == 0) return BSPMM_SUCCESS;
+  const bool out_given = csr_row_ptr_out != nullptr;
+  if (out_given != (csr_col_out != nullptr) || out_given != (csr_val_out != nullptr))
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "csr_*_out must be all NULL or all non-NULL");
+  if ((!row_off && !sizes) || !nnz_off || !B || !C || (total_nnz > 0 && (!idx || !vals)))
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  if (B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
+  DeviceGuard g(h->device);
+  CooWs w;
+  bspmm_status_t st = coo_workspace(h, batch, total_rows, total_nnz, row_off == nullptr, !out_given, &w);
+  if (st != BSPMM_SUCCESS) return st;
+  const int64_t* ro = row_off;
+  if (!ro) {
+    st = bspmm_build_offsets(h, batch, sizes, w.row_off);
+    if (st != BSPMM_SUCCESS) return st;
+    ro = w.row_off;
+  }
+  int32_t* rp = out_given ? csr_row_ptr_out : w.row_ptr;
+  int32_t* col = out_given ? csr_col_out : w.col;
+  float* val = out_given ? csr_val_out : w.val;
+  st = coo2csr_impl(h, batch, ro, sizes, nnz_off, idx, vals, total_nnz, rp, col, val, w);
+  if (st != BSPMM_SUCCESS) return st;
+  // indices were validated on the COO side; the built CSR is consistent by construction
+  return csr_impl(h, batch, k, ro, sizes, rp, col, val, B, ldb, C, ldc, false);
+}
+
+// ---- end-to-end host-buffer path ------------------------------------------
+BSPMM_API bspmm_status_t bspmm_csr_host(bspmm_handle_t h, int32_t batch, int32_t k, const int32_t* sizes_host,
+                                        const int32_t* row_ptr_host, const int32_t* col_host,
+                                        const float* vals_host, const float* B_host, float* C_host,
+                                        int64_t total_rows, int64_t total_nnz) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || k < 1 || total_rows < 0 || total_nnz < 0 || total_nnz > INT32_MAX)
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1 or bad totals");
+  if (batch == 0) return BSPMM_SUCCESS;
+  if (!sizes_host || !row_ptr_host || !B_host || !C_host || (total_nnz > 0 && (!col_host || !vals_host)))
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  DeviceGuard g(h->device);
+  const int64_t N = total_rows, NNZ = total_nnz;
+  // device mirror: [sizes][row_off][row_ptr][col][val][B][C]
+  size_t off = 0;
+  const size_t o_sz = off; off += al256((size_t)batch * 4);
+  const size_t o_ro = off; off += al256((size_t)(batch + 1) * 8);
+  const size_t o_rp = off; off += al256((size_t)(N + 1) * 4);
+  const size_t o_col = off; off += al256((size_t)NNZ * 4);
+  const size_t o_val = off; off += al256((size_t)NNZ * 4);
+  const size_t o_B = off; off += al256((size_t)N * k * 4);
+  const size_t o_C = off; off += al256((size_t)N * k * 4);
+  bspmm_status_t st = grow(h, &h->hbuf, &h->hbuf_bytes, off);
+  if (st != BSPMM_SUCCESS) return st;
+  char* base = static_cast<char*>(h->hbuf);
+  int32_t* d_sz = reinterpret_cast<int32_t*>(base + o_sz);
+  int64_t* d_ro = reinterpret_cast<int64_t*>(base + o_ro);
+  int32_t* d_rp = reinterpret_cast<int32_t*>(base + o_rp);
+  int32_t* d_col = reinterpret_cast<int32_t*>(base + o_col);
+  float* d_val = reinterpret_cast<float*>(base + o_val);
+  float* d_B = reinterpret_cast<float*>(base + o_B);
+  float* d_C = reinterpret_cast<float*>(base + o_C);
+  if (!h->s_h2d) CK(h, cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+  if (!h->s_d2h) CK(h, cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+  for (auto& e : h->ev)
+    if (!e) CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+  // chunk plan: contiguous graph ranges of ~equal rows (host arithmetic for scheduling only)
+  const int64_t bytesBC = N * (int64_t)k * 4;
+  const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(24, (bytesBC + (96 << 20) - 1) / (96 << 20)));
+  int32_t gi[25];
+  int64_t gr[25];
+  gi[0] = 0;
+  gr[0] = 0;
+  {
+    int32_t i = 0;
+    int64_t r = 0;
+    for (int c = 1; c < nch; ++c) {
+      const int64_t target = N * c / nch;
+      while (i < batch && r + sizes_host[i] <= target) r += sizes_host[i++];
+      gi[c] = i;
+      gr[c] = r;
+    }
+    gi[nch] = batch;
+    gr[nch] = N;
+  }
+  const bool validate = (h->flags & BSPMM_VALIDATE) != 0;
+  cudaEvent_t ev_sizes = h->ev[0];
+  CK(h, cudaMemcpyAsync(d_sz, sizes_host, (size_t)batch * 4, cudaMemcpyHostToDevice, h->s_h2d));
+  CK(h, cudaEventRecord(ev_sizes, h->s_h2d));
+  CK(h, cudaStreamWaitEvent(h->stream, ev_sizes, 0));
+  st = bspmm_build_offsets(h, batch, d_sz, d_ro);
+  if (st != BSPMM_SUCCESS) return st;
+  for (int c = 0; c < nch; ++c) {
+    const int32_t i0 = gi[c], i1 = gi[c + 1];
+    const int64_t r0 = gr[c], r1 = gr[c + 1];
+    if (i1 == i0) continue;
+    const int64_t z0 = row_ptr_host[r0], z1 = row_ptr_host[r1];
+    cudaEvent_t ev_in = h->ev[1 + 2 * c], ev_out = h->ev[2 + 2 * c];
+    CK(h, cudaMemcpyAsync(d_rp + r0, row_ptr_host + r0, (size_t)(r1 - r0 + 1) * 4, cudaMemcpyHostToDevice,
+                          h->s_h2d));
+    if (z1 > z0) {
+      CK(h, cudaMemcpyAsync(d_col + z0, col_host + z0, (size_t)(z1 - z0) * 4, cudaMemcpyHostToDevice, h->s_h2d));
+      CK(h, cudaMemcpyAsync(d_val + z0, vals_host + z0, (size_t)(z1 - z0) * 4, cudaMemcpyHostToDevice, h->s_h2d));
+    }
+    CK(h, cudaMemcpyAsync(d_B + r0 * k, B_host + r0 * k, (size_t)(r1 - r0) * k * 4, cudaMemcpyHostToDevice,
+                          h->s_h2d));
+    CK(h, cudaEventRecord(ev_in, h->s_h2d));
+    CK(h, cudaStreamWaitEvent(h->stream, ev_in, 0));
+    st = csr_impl(h, i1 - i0, k, d_ro + i0, nullptr, d_rp, d_col, d_val, d_B, k, d_C, k, validate);
+    if (st != BSPMM_SUCCESS) return st;
+    CK(h, cudaEventRecord(ev_out, h->stream));
+    CK(h, cudaStreamWaitEvent(h->s_d2h, ev_out, 0));
+    CK(h, cudaMemcpyAsync(C_host + r0 * k, d_C + r0 * k, (size_t)(r1 - r0) * k * 4, cudaMemcpyDeviceToHost,
+                          h->s_d2h));
+  }
+  CK(h, cudaStreamSynchronize(h->s_d2h));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return BSPMM_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// internal.h — private declarations shared by the libbspmm.so sources.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "bspmm.h"
+
+#if defined(__CUDACC__)
+#define BSPMM_HD __host__ __device__
+#else
+#define BSPMM_HD
+#endif
+
+namespace bspmm {
+
+constexpr int kMaxStages = 8;
+constexpr int kHdrBytes = 32;       // per-stage unit header
+constexpr int kDefaultRows = 64;    // planning assumption when no max_rows hint
+constexpr int kDefaultWarps = 8;    // consumer warps per CTA
+constexpr int kMaxVecKt = 512;      // 4 float4 chunks x 32 lanes
+constexpr int kMaxScalarKt = 128;   // 4 float chunks x 32 lanes
+constexpr int kCooSmemCap = 2048;   // default COO entries sorted in shared memory
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int32_t pow2_ceil(int32_t x) {
+  int32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+BSPMM_HD inline int32_t align_up(int32_t x, int32_t a) { return (x + a - 1) / a * a; }
+
+// smem carve-up shared by planner and kernel: [hdr S*32][full S*8][empty S*8] pad 128, then stages
+BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stages * (kHdrBytes + 16), 128); }
+
+// planner (plan.cpp)
+bspmm_status_t make_plan(int32_t k, int32_t batch, bool aligned, int32_t max_rows, int64_t max_nnz,
+                         int32_t num_sms, int32_t smem_per_cta, int32_t kt_override, int32_t warps,
+                         int32_t ctas_per_sm, bspmm_plan_t* out);
+
+struct CsrArgs {
+  int32_t batch, k;
+  const int64_t* row_off;
+  const int32_t* sizes;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const float* vals;
+  const float* B;
+  int64_t ldb;
+  float* C;
+  int64_t ldc;
+};
+
+// kernels (.cu)
+cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s);
+cudaError_t launch_offsets(int32_t batch, const int32_t* sizes, int64_t* out, cudaStream_t s);
+cudaError_t launch_coo2csr(int32_t batch, const int64_t* row_off, const int32_t* sizes,
+                           const int64_t* nnz_off, const int32_t* idx, const float* vals, int32_t* row_ptr,
+                           int32_t* col_out, float* val_out, uint64_t* ws_keys, uint32_t* ws_pay,
+                           int64_t ws_stride, int32_t smem_cap, cudaStream_t s);
+int32_t coo_smem_cap(int64_t max_nnz_hint, int32_t smem_optin);
+cudaError_t launch_validate_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes,
+                                const int32_t* row_ptr, const int32_t* col, int* flag, cudaStream_t s);
+cudaError_t launch_validate_coo(int32_t batch, const int64_t* row_off, const int32_t* sizes,
+                                const int64_t* nnz_off, const int32_t* idx, int* flag, cudaStream_t s);
+cudaError_t launch_validate_sizes(int32_t batch, const int32_t* sizes, int* flag, cudaStream_t s);
+
+}  // namespace bspmm
+
+struct bspmm_handle_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  unsigned flags = 0;
+  int num_sms = 148;
+  int smem_optin = 232448;
+  int32_t hint_rows = 0;
+  int64_t hint_nnz = 0;
+  int32_t tune_kt = 0, tune_warps = 0, tune_ctas = 0;
+  bspmm_plan_t last_plan{};
+  int64_t launches = 0;
+  std::string err;
+  // device workspace (grown on demand)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  int* dev_flag = nullptr;
+  // e2e host-path buffers and streams
+  void* hbuf = nullptr;
+  size_t hbuf_bytes = 0;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev[64] = {};
+};

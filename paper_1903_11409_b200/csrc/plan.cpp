@@ -1,0 +1,103 @@
+// plan.cpp — the launch planner (hot-path row a-3).
+//
+// PAPER.md:240-264 decides, from the matrix sizes, whether column cache
+// blocking is applied (p column blocks, :257, :263) and how many threads each
+// SpMM gets (subWarp * m_A for CSR, :259).  Re-derived for sm_100a:
+//  * a unit is (matrix i, k-tile t); tiles = p = ceil(k / kt);
+//  * kt starts at the whole row (capped at 512 columns on the float4 path,
+//    128 on the scalar path) and is halved while the batch yields fewer than
+//    2 units per SM (the paper's "batch 50 fails to fill the SMs", :377) or a
+//    two-stage shared-memory ring of n_max x kt tiles does not fit;
+//  * lanes per row = the paper's subWarp rule (:150-155) applied to the
+//    tile's float4 columns (vec) or columns (scalar);
+//  * persistent grid = min(units, SMs x CTAs/SM); each CTA walks units
+//    blockIdx.x, +grid, ... through an S-stage TMA ring.
+#include <algorithm>
+
+#include "internal.h"
+
+extern "C" BSPMM_API int32_t bspmm_subwarp(int32_t n_B) {
+  if (n_B < 1) return 0;
+  if (n_B > 16) return 32;
+  return bspmm::pow2_ceil(n_B);
+}
+
+namespace bspmm {
+
+static int32_t lanes_for(int32_t kt, bool vec) {
+  return bspmm_subwarp(vec ? (kt + 3) / 4 : kt);
+}
+
+bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, int64_t max_nnz,
+                         int32_t num_sms, int32_t smem_per_cta, int32_t kt_override, int32_t warps,
+                         int32_t ctas_per_sm, bspmm_plan_t* out) {
+  if (!out || k < 1 || batch < 0 || num_sms < 1 || smem_per_cta < 1024) return BSPMM_ERROR_INVALID_VALUE;
+  bspmm_plan_t p{};
+  const int32_t R = max_rows > 0 ? max_rows : kDefaultRows;
+  const int64_t Z = max_nnz > 0 ? max_nnz : 8LL * R;
+  const int32_t ctas = ctas_per_sm > 0 ? ctas_per_sm : 1;
+  const int32_t W = warps > 0 ? std::min(warps, 16) : kDefaultWarps;
+  // per-CTA shared-memory budget (B200: 228 KB per SM, 227 KB opt-in per CTA; 1 KB reserved per CTA)
+  const int32_t budget = std::min(smem_per_cta, (233472 / ctas) - 1024);
+  const int32_t kmax = vec ? kMaxVecKt : kMaxScalarKt;
+  const int32_t quantum = vec ? 4 : 1;
+
+  int32_t kt;
+  if (kt_override > 0) {
+    kt = std::min(kt_override, kmax);
+    if (vec) kt = align_up(kt, 4);
+    kt = std::min(kt, align_up(k, quantum));
+  } else {
+    kt = std::min(align_up(k, quantum), kmax);
+    const int64_t target_units = 2LL * num_sms;
+    while ((int64_t)batch * ceil_div(k, kt) < target_units && kt > 32) kt = align_up(kt / 2, quantum);
+  }
+  // structure capacity: (col, val) pairs + row pointer
+  int64_t s_bytes64 = align_up(8 * (int32_t)std::min<int64_t>(Z, 1 << 20), 16) + align_up(4 * (R + 1), 16);
+  auto stages_for = [&](int32_t kt_) {
+    int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 16);
+    int64_t per = b + s_bytes64;
+    int64_t s = 0;
+    while (s < kMaxStages && ring_prefix_bytes((int32_t)(s + 1)) + (s + 1) * per <= budget) ++s;
+    return (int32_t)s;
+  };
+  if (kt_override <= 0)
+    while (stages_for(kt) < 2 && kt > quantum * 8) kt = align_up(kt / 2, quantum);
+
+  int32_t stages = stages_for(kt);
+  int32_t b_bytes = align_up(std::max<int32_t>(16, R * kt * 4), 16);
+  int32_t s_bytes = (int32_t)s_bytes64;
+  if (stages < 1) {
+    // even one stage does not fit: shrink capacities; bigger matrices go direct
+    s_bytes = std::min<int32_t>(s_bytes, budget / 4) / 16 * 16;
+    b_bytes = (budget - ring_prefix_bytes(1) - s_bytes) / 16 * 16;
+    stages = 1;
+  }
+  p.kt = kt;
+  p.tiles = (int32_t)ceil_div(k, kt);
+  p.vec = vec ? 1 : 0;
+  p.lanes = lanes_for(kt, vec);
+  const int32_t cols = vec ? (kt + 3) / 4 : kt;
+  const int32_t ch = (int32_t)ceil_div(cols, p.lanes);
+  p.chunks = ch <= 1 ? 1 : (ch <= 2 ? 2 : 4);
+  p.stages = stages;
+  p.stage_b_bytes = b_bytes;
+  p.stage_s_bytes = s_bytes;
+  p.smem_bytes = ring_prefix_bytes(stages) + stages * (b_bytes + s_bytes);
+  p.threads = 32 * (1 + W);
+  p.units = (int64_t)batch * p.tiles;
+  p.grid = (int32_t)std::min<int64_t>(p.units, (int64_t)num_sms * ctas);
+  p.max_rows = R;
+  *out = p;
+  return BSPMM_SUCCESS;
+}
+
+}  // namespace bspmm
+
+extern "C" BSPMM_API bspmm_status_t bspmm_plan(int32_t k, int32_t batch, int32_t aligned, int32_t max_rows,
+                                               int64_t max_nnz, int32_t num_sms, int32_t smem_per_cta,
+                                               int32_t kt_override, int32_t consumer_warps,
+                                               int32_t ctas_per_sm, bspmm_plan_t* out) {
+  return bspmm::make_plan(k, batch, aligned != 0, max_rows, max_nnz, num_sms, smem_per_cta, kt_override,
+                          consumer_warps, ctas_per_sm, out);
+}

@@ -1,0 +1,300 @@
+// spmm_csr.cu — the batched CSR SpMM kernel for sm_100a (hot-path rows a-4,
+// a-5, a-6).
+//
+// What it computes (PAPER.md Fig. algo:code_swa_spmm_csr, lines 196-207,
+// batched as in §IV-C): for every matrix i, row r < n_i and
+// column c < k
+//     C[g][c] = sum_{e in row g} vals[e] * B[row_off[i] + col[e]][c],
+// g = row_off[i] + r, accumulated as fp32 FMA in CSR storage order from +0.
+//
+// How (B200-first; the paper's P100 design is prior art):
+//  * persistent CTAs walk units u = (matrix i, k-tile t) with stride grid;
+//  * warp 0 is the PRODUCER: it prefetches unit metadata 32 units at a time
+//    (one lane per unit), then per unit waits for a free ring stage and
+//    stages B_i[:, tile] into shared memory with TMA bulk copies
+//    (cp.async.bulk, one copy when the tile is the whole contiguous B_i,
+//    else one per row) and the unit's CSR structure (row pointers, (col, val)
+//    pairs) with cp.async, all completing on the stage's "full" mbarrier;
+//  * warps 1..W are CONSUMERS: a sub-warp of `lanes` lanes owns one row at a
+//    time (SWA; row ownership means no atomics, :170), each
+//    lane owns float4 column chunks (the paper's lane-strided columns
+//    j = lane, lane + subWarp, ..., :204, widened to 128-bit), reads B from
+//    shared memory, accumulates in registers and writes the C row with
+//    128-bit streaming stores.  Empty rows store +0 (no init launch,
+//    PAPER.md:220-222).  Then the warp arrives on the stage's "empty" barrier;
+//  * a unit whose tile or structure exceeds the stage capacity is computed
+//    straight from global memory (the paper's no-shared-memory case 3,
+//    PAPER.md:249-252), decided per unit on the device.
+#include <cstdint>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace bspmm {
+
+struct SpmmParams {
+  int64_t units;
+  int32_t tiles, kt, k;
+  int32_t stages, stage_b, stage_s, lanes;
+  const int64_t* __restrict__ row_off;
+  const int32_t* __restrict__ sizes;
+  const int32_t* __restrict__ row_ptr;
+  const int32_t* __restrict__ col;
+  const float* __restrict__ vals;
+  const float* __restrict__ B;
+  int64_t ldb;
+  float* __restrict__ C;
+  int64_t ldc;
+};
+
+struct __align__(16) UnitHdr {
+  int64_t g0;      // first global row of the matrix
+  int32_t n;       // rows (n_i)
+  int32_t nz0;     // absolute position of the matrix's first entry
+  int32_t nnz;     // entries of the matrix
+  int32_t c0;      // first column of the tile
+  int32_t kw;      // tile width (ragged last tile)
+  int32_t staged;  // 1: tile + structure are in the stage
+};
+static_assert(sizeof(UnitHdr) == kHdrBytes, "header size");
+
+template <bool VEC>
+__device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem) {
+  UnitHdr* hdr = reinterpret_cast<UnitHdr*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
+  uint64_t* empty = full + p.stages;
+  unsigned char* ring = smem + ring_prefix_bytes(p.stages);
+  const int32_t stage_bytes = p.stage_b + p.stage_s;
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = policy_evict_first();
+
+  int64_t m_g0 = 0;
+  int32_t m_n = 0, m_nz0 = 0, m_nnz = 0, m_c0 = 0, m_kw = 0;
+  int j = 0;
+  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+    if ((j & 31) == 0) {  // metadata for the next 32 units, one lane each
+      const int64_t uu = u + (int64_t)lane * gridDim.x;
+      if (uu < p.units) {
+        const int64_t i = uu / p.tiles;
+        const int32_t t = (int32_t)(uu - i * p.tiles);
+        m_g0 = p.row_off[i];
+        m_n = p.sizes ? p.sizes[i] : (int32_t)(p.row_off[i + 1] - m_g0);
+        m_nz0 = p.row_ptr[m_g0];
+        m_nnz = p.row_ptr[m_g0 + m_n] - m_nz0;
+        m_c0 = t * p.kt;
+        m_kw = min(p.kt, p.k - m_c0);
+      }
+    }
+    const int src = j & 31;
+    const int64_t g0 = __shfl_sync(0xffffffffu, m_g0, src);
+    const int32_t n = __shfl_sync(0xffffffffu, m_n, src);
+    const int32_t nz0 = __shfl_sync(0xffffffffu, m_nz0, src);
+    const int32_t nnz = __shfl_sync(0xffffffffu, m_nnz, src);
+    const int32_t c0 = __shfl_sync(0xffffffffu, m_c0, src);
+    const int32_t kw = __shfl_sync(0xffffffffu, m_kw, src);
+
+    const int s = j % p.stages;
+    const uint32_t phase = (uint32_t)(j / p.stages) & 1u;
+    mbar_wait(&empty[s], phase ^ 1u);
+    unsigned char* st = ring + (size_t)s * stage_bytes;
+    const bool staged = (int64_t)n * kw * 4 <= p.stage_b && 8LL * nnz + 4LL * (n + 1) <= p.stage_s;
+    const uint32_t tx = (VEC && staged) ? (uint32_t)n * (uint32_t)kw * 4u : 0u;
+    if (lane == 0) {
+      UnitHdr h;
+      h.g0 = g0; h.n = n; h.nz0 = nz0; h.nnz = nnz; h.c0 = c0; h.kw = kw; h.staged = staged ? 1 : 0;
+      hdr[s] = h;
+      mbar_arrive_expect_tx(&full[s], tx);  // release: header visible to consumers
+    }
+    if (staged) {
+      const float* bsrc = p.B + g0 * p.ldb + c0;
+      if (VEC) {
+        if (kw == p.ldb) {  // whole contiguous B_i: one bulk copy
+          if (lane == 0 && tx) bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
+        } else {
+          for (int r = lane; r < n; r += 32)
+            bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
+        }
+      } else {
+        float* dst = reinterpret_cast<float*>(st);
+        const int32_t total = n * kw;
+        for (int32_t q = lane; q < total; q += 32) {
+          const int32_t r = q / kw, c = q - r * kw;
+          cp_async4(dst + q, bsrc + (int64_t)r * p.ldb + c);
+        }
+      }
+      int32_t* pairs = reinterpret_cast<int32_t*>(st + p.stage_b);
+      for (int32_t e = lane; e < nnz; e += 32) {
+        cp_async4(pairs + 2 * e, p.col + nz0 + e);
+        cp_async4(pairs + 2 * e + 1, p.vals + nz0 + e);
+      }
+      int32_t* rp = pairs + 2 * nnz;
+      for (int32_t r = lane; r <= n; r += 32) cp_async4(rp + r, p.row_ptr + g0 + r);
+    }
+    cp_async_arrive_noinc(&full[s]);  // 32 arrivals, each after its lane's copies land
+  }
+}
+
+// one sub-warp row loop; VEC: float4 chunks, else scalar chunks
+template <int CH, bool VEC, bool STAGED>
+__device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
+                                     int step, int li) {
+  const int L = p.lanes;
+  const int32_t cols = VEC ? (h.kw >> 2) : h.kw;  // chunks of 4 (VEC) or 1 column
+  const int32_t* rp;
+  const int2* pr = nullptr;
+  const float* Bbase;
+  int64_t bstride;  // floats between consecutive B rows
+  if (STAGED) {
+    pr = reinterpret_cast<const int2*>(st + p.stage_b);
+    rp = reinterpret_cast<const int32_t*>(st + p.stage_b) + 2 * h.nnz;
+    Bbase = reinterpret_cast<const float*>(st);
+    bstride = h.kw;
+  } else {
+    rp = p.row_ptr + h.g0;
+    Bbase = p.B + h.g0 * p.ldb + h.c0;
+    bstride = p.ldb;
+  }
+  for (int r = first; r < h.n; r += step) {
+    const int32_t e0 = rp[r] - h.nz0, e1 = rp[r + 1] - h.nz0;
+    float4 acc[CH];
+#pragma unroll
+    for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+    for (int32_t e = e0; e < e1; ++e) {
+      int32_t cidx;
+      float a;
+      if (STAGED) {
+        const int2 cv = pr[e];
+        cidx = cv.x;
+        a = __int_as_float(cv.y);
+      } else {
+        cidx = __ldg(p.col + h.nz0 + e);
+        a = __ldg(p.vals + h.nz0 + e);
+      }
+      const float* brow = Bbase + (int64_t)cidx * bstride;
+#pragma unroll
+      for (int v = 0; v < CH; ++v) {
+        const int c = li + v * L;
+        if (c < cols) {
+          if (VEC) {
+            float4 b;
+            if (STAGED) b = reinterpret_cast<const float4*>(brow)[c];
+            else b = ldg_nc_f4(brow + 4 * c);
+            acc[v].x = fmaf(a, b.x, acc[v].x);
+            acc[v].y = fmaf(a, b.y, acc[v].y);
+            acc[v].z = fmaf(a, b.z, acc[v].z);
+            acc[v].w = fmaf(a, b.w, acc[v].w);
+          } else {
+            const float b = STAGED ? brow[c] : __ldg(brow + c);
+            acc[v].x = fmaf(a, b, acc[v].x);
+          }
+        }
+      }
+    }
+    float* crow = p.C + (h.g0 + r) * p.ldc + h.c0;
+#pragma unroll
+    for (int v = 0; v < CH; ++v) {
+      const int c = li + v * L;
+      if (c < cols) {
+        if (VEC) stg_cs_f4(crow + 4 * c, acc[v]);
+        else stg_cs_f1(crow + c, acc[v].x);
+      }
+    }
+  }
+}
+
+template <int CH, bool VEC>
+__device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem) {
+  const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
+  uint64_t* empty = full + p.stages;
+  const unsigned char* ring = smem + ring_prefix_bytes(p.stages);
+  const int32_t stage_bytes = p.stage_b + p.stage_s;
+  const int lane = threadIdx.x & 31;
+  const int cw = (threadIdx.x >> 5) - 1;
+  const int W = (blockDim.x >> 5) - 1;
+  const int L = p.lanes;
+  const int rpw = 32 / L;
+  const int sub = lane / L, li = lane % L;
+  const int first = cw * rpw + sub, step = W * rpw;
+  int j = 0;
+  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+    const int s = j % p.stages;
+    mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
+    const UnitHdr h = hdr[s];
+    const unsigned char* st = ring + (size_t)s * stage_bytes;
+    if (h.staged) rows<CH, VEC, true>(p, h, st, first, step, li);
+    else rows<CH, VEC, false>(p, h, st, first, step, li);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+template <int CH, bool VEC>
+__global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
+  uint64_t* empty = full + p.stages;
+  if (threadIdx.x == 0) {
+    const uint32_t W = (blockDim.x >> 5) - 1;
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1 + 32);  // producer lane-0 expect_tx + 32 cp.async arrivals
+      mbar_init(&empty[s], W);      // one arrival per consumer warp
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0) produce<VEC>(p, smem);
+  else consume<CH, VEC>(p, smem);
+}
+
+template <int CH, bool VEC>
+static cudaError_t launch_t(const SpmmParams& sp, const bspmm_plan_t& plan, cudaStream_t s) {
+  auto kern = spmm_csr_kernel<CH, VEC>;
+  static thread_local int configured_bytes[64] = {};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (plan.smem_bytes > 48 * 1024 && configured_bytes[dev & 63] < plan.smem_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);
+    if (e != cudaSuccess) return e;
+    configured_bytes[dev & 63] = plan.smem_bytes;
+  }
+  kern<<<plan.grid, plan.threads, plan.smem_bytes, s>>>(sp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s) {
+  if (plan.units == 0 || plan.grid == 0) return cudaSuccess;
+  SpmmParams sp;
+  sp.units = plan.units;
+  sp.tiles = plan.tiles;
+  sp.kt = plan.kt;
+  sp.k = a.k;
+  sp.stages = plan.stages;
+  sp.stage_b = plan.stage_b_bytes;
+  sp.stage_s = plan.stage_s_bytes;
+  sp.lanes = plan.lanes;
+  sp.row_off = a.row_off;
+  sp.sizes = a.sizes;
+  sp.row_ptr = a.row_ptr;
+  sp.col = a.col;
+  sp.vals = a.vals;
+  sp.B = a.B;
+  sp.ldb = a.ldb;
+  sp.C = a.C;
+  sp.ldc = a.ldc;
+  if (plan.vec) {
+    switch (plan.chunks) {
+      case 1: return launch_t<1, true>(sp, plan, s);
+      case 2: return launch_t<2, true>(sp, plan, s);
+      default: return launch_t<4, true>(sp, plan, s);
+    }
+  }
+  switch (plan.chunks) {
+    case 1: return launch_t<1, false>(sp, plan, s);
+    case 2: return launch_t<2, false>(sp, plan, s);
+    default: return launch_t<4, false>(sp, plan, s);
+  }
+}
+
+}  // namespace bspmm

@@ -1,0 +1,124 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol
+include/bspmm.h declares, rejects bad arguments, and its host-only functions
+(partition, subWarp rule, planner) agree with the oracle / the paper.
+No compute call touches a GPU here."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1903_11409_b200 as bs
+from paper_1903_11409_b200 import _lib
+
+
+def test_exports_every_header_symbol():
+    syms = bs.header_symbols()
+    assert len(syms) >= 18, syms
+    raw = ctypes.CDLL(bs.LIB_PATH)
+    missing = [s for s in syms if not hasattr(raw, s)]
+    assert not missing, missing
+    # nothing else leaks: internal symbols are hidden
+    assert not hasattr(raw, "_ZN5bspmm9make_planEiibilii iiiP12bspmm_plan_t".replace(" ", ""))
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", bs.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def test_status_strings_and_null_handle():
+    lib = _lib.lib
+    assert lib.bspmm_status_string(0) == b"BSPMM_SUCCESS"
+    assert lib.bspmm_status_string(4) == b"BSPMM_ERROR_INDEX"
+    assert lib.bspmm_destroy(None) == 0
+    assert lib.bspmm_csr(None, 1, 1, None, None, None, None, None, None, 1, None, 1) == _lib.INVALID_VALUE
+    assert lib.bspmm_sync(None) == _lib.INVALID_VALUE
+    assert lib.bspmm_launch_count(None) == -1
+
+
+def test_create_without_gpu_is_not_supported_or_ok():
+    h = ctypes.c_void_p()
+    assert _lib.lib.bspmm_create(None, 0, None, 0) == _lib.INVALID_VALUE
+    assert _lib.lib.bspmm_create(ctypes.byref(h), 0, None, 0x80) == _lib.INVALID_VALUE
+    st = _lib.lib.bspmm_create(ctypes.byref(h), 0, None, 0)
+    import torch
+    if not torch.cuda.is_available():
+        assert st == _lib.NOT_SUPPORTED and not h.value
+    else:
+        assert st == _lib.SUCCESS
+        _lib.lib.bspmm_destroy(h)
+
+
+def test_subwarp_rule_golden(golden):
+    for n_b, want in golden["subwarp"]["cases"]:
+        assert bs.subwarp(n_b) == want, (n_b, golden["subwarp"]["cite"])
+    assert bs.subwarp(0) == 0
+    # invariants: power of two, monotone, 32 above 16
+    prev = 0
+    for n in range(1, 300):
+        s = bs.subwarp(n)
+        assert s & (s - 1) == 0 and s >= prev and s >= min(n, 32) and (n <= 16 or s == 32)
+        prev = s
+
+
+def test_partition_matches_oracle_bit_exact(golden):
+    for ex in golden["partition"]:
+        nnz_off = np.concatenate([[0], np.cumsum(ex["nnz"])]).astype(np.int64)
+        assert list(bs.partition(nnz_off, ex["k"], ex["parts"])) == ex["split"], ex["cite"]
+    rng = np.random.default_rng(11)
+    for _ in range(2000):
+        batch = int(rng.integers(0, 60))
+        nnz_off = np.concatenate([[0], np.cumsum(rng.integers(0, 40, size=batch))]).astype(np.int64)
+        k, G = int(rng.integers(1, 1025)), int(rng.integers(1, 9))
+        assert np.array_equal(bs.partition(nnz_off, k, G), oracle.partition(nnz_off, k, G))
+
+
+def test_partition_c5_shape():
+    import synth
+    n, z = synth.counts(synth.MOL, (20, 60, 0, 0), synth.BASE_SEED + 5, 0, 65536)
+    nnz_off = np.concatenate([[0], np.cumsum(z)]).astype(np.int64)
+    for G in (1, 2, 4, 8):
+        s = bs.partition(nnz_off, 256, G)
+        assert np.array_equal(s, oracle.partition(nnz_off, 256, G))
+        cost = [int(nnz_off[s[r + 1]] - nnz_off[s[r]]) for r in range(G)]
+        assert max(cost) - min(cost) <= 2 * int(z.max())         # within a graph or two
+
+
+def test_partition_rejects_bad_args():
+    with pytest.raises(bs.BspmmError):
+        bs.partition(np.array([0, 5, 3], dtype=np.int64), 4, 2)      # non-monotone
+    with pytest.raises(bs.BspmmError):
+        bs.partition(np.array([0, 5], dtype=np.int64), 4, 0)
+
+
+@pytest.mark.parametrize("k", [1, 3, 4, 5, 16, 17, 33, 64, 128, 256, 512, 1000, 1024, 4096])
+@pytest.mark.parametrize("batch", [1, 4, 100, 200, 65536])
+def test_plan_invariants(k, batch):
+    for aligned in (True, False):
+        if aligned and k % 4:
+            continue
+        for rows in (0, 8, 60, 300, 5000):
+            p = bs.plan(k, batch, aligned=aligned, max_rows=rows)
+            assert p["tiles"] == -(-k // p["kt"])                            # tiles cover [0, k)
+            assert p["kt"] * (p["tiles"] - 1) < k <= p["kt"] * p["tiles"]    # disjoint, no empty tile
+            cols = -(-p["kt"] // 4) if p["vec"] else p["kt"]
+            assert p["lanes"] == bs.subwarp(cols)
+            assert p["lanes"] * p["chunks"] >= cols
+            assert p["smem_bytes"] <= 232448 and p["stages"] >= 1
+            assert p["units"] == batch * p["tiles"]
+            assert 1 <= p["grid"] <= min(p["units"], 148 * 4)
+            if aligned:
+                assert p["kt"] % 4 == 0
+            if rows and rows * p["kt"] * 4 <= 100000:
+                assert p["stage_b_bytes"] >= rows * p["kt"] * 4                 # fits -> staged
+
+
+def test_plan_paper_shapes():
+    # C4 (PAPER.md:366 shape): 100 matrices cannot fill 148 SMs whole -> column blocking (p > 1)
+    p = bs.plan(512, 100, max_rows=50)
+    assert p["tiles"] > 1 and p["units"] >= 2 * 148
+    # C5: whole rows, one unit per matrix
+    p = bs.plan(256, 65536, max_rows=60)
+    assert p["tiles"] == 1 and p["stages"] >= 2

@@ -1,0 +1,335 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bars:
+* integer / index work (offsets, COO->CSR, partition, shards): bit-exact;
+* fp32 C: |C - C_ref| <= 1e-5 * sum|a||b| per element against the fp64 oracle
+  (north_star), AND bitwise equal to the fp32 storage-order FMA oracle O3'
+  (the kernel keeps CSR storage order), AND exact on integer-valued inputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1903_11409_b200 as bs
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def h():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    assert torch.cuda.get_device_capability(0) == (10, 0)
+    return bs.Handle(0)
+
+
+def T(a, dt=None):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.to(DEV) if dt is None else t.to(DEV, dt)
+
+
+def run_csr(h, b, sizes=False, ld=None, hints=True, C_init=None):
+    if hints:
+        h.set_hints(int(b.sizes.max()) if b.batch else 0, int(b.nnz.max()) if b.batch else 0)
+    else:
+        h.set_hints(0, 0)
+    k = b.k
+    ldb = k if ld is None else ld
+    Bp = np.zeros((b.n_rows, ldb), dtype=np.float32)
+    Bp[:, :k] = b.B
+    Bd = T(Bp)
+    Cd = torch.full((b.n_rows, ldb), float("nan"), device=DEV) if C_init is None else T(C_init)
+    h.csr(T(b.row_off), T(b.sizes) if sizes else None, T(b.row_ptr), T(b.col), T(b.vals), Bd, Cd, k=k,
+          batch=b.batch)
+    torch.cuda.synchronize()
+    return Cd.cpu().numpy()[:, :k]
+
+
+def assert_parity(b, C, what=""):
+    C32 = oracle.spmm_f32(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+    Cref, bound = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+    ok, worst = oracle.check_bound(C, Cref, bound)
+    assert ok, f"{what}: bound violated, worst |d|/bound = {worst}"
+    diff = np.nonzero(C.view(np.uint32) != C32.view(np.uint32))
+    assert diff[0].size == 0, f"{what}: {diff[0].size} elements differ bitwise from O3', first {diff[0][:5]}"
+
+
+# ------------------------------------------------------------ a-1 offsets
+
+@pytest.mark.parametrize("batch", [0, 1, 5, 1023, 1024, 1025, 4095, 4096, 4097, 65536, 100003])
+def test_offsets_bit_exact(h, batch):
+    rng = np.random.default_rng(batch)
+    sizes = rng.integers(0, 300, size=batch).astype(np.int32)
+    sizes[::7] = 0
+    out = h.build_offsets(T(sizes))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.offsets(sizes))
+
+
+def test_offsets_int64_no_wrap(h):
+    sizes = np.full(5000, (1 << 31) - 1, dtype=np.int32)
+    out = h.build_offsets(T(sizes)).cpu().numpy()
+    assert np.array_equal(out, oracle.offsets(sizes)) and out[-1] > (1 << 40)
+
+
+# ------------------------------------------------------------ a-3..a-6 CSR SpMM
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+@pytest.mark.parametrize("int_valued", [False, True])
+def test_configs_csr(h, cid, int_valued):
+    b = synth.config(cid, int_valued=int_valued)
+    C = run_csr(h, b)
+    assert_parity(b, C, f"config {cid}")
+    if int_valued:
+        Cref, _ = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+        assert np.array_equal(C, Cref)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 16, 17, 33, 64, 100, 128, 256, 300, 512, 1000, 1024])
+def test_k_sweep_adversarial(h, k):
+    rng = np.random.default_rng(1000 + k)
+    for trial in range(4):
+        b = synth.random_batch(rng, int(rng.integers(1, 40)), k, nmax=70, dmax=6, duplicates=trial % 2 == 1)
+        assert_parity(b, run_csr(h, b), f"k={k} trial={trial}")
+        assert_parity(b, run_csr(h, b, sizes=True, hints=False), f"k={k} trial={trial} no hints")
+
+
+@pytest.mark.parametrize("k,ld", [(16, 20), (64, 68), (5, 7), (128, 129), (256, 260)])
+def test_leading_dimension(h, k, ld):
+    rng = np.random.default_rng(k * ld)
+    b = synth.random_batch(rng, 30, k, nmax=40, dmax=5)
+    C = run_csr(h, b, ld=ld)
+    assert_parity(b, C, f"k={k} ld={ld}")
+
+
+def test_padded_layout_untouched(h):
+    """row_off with gaps + sizes: only matrix rows are written (padding stays NaN)."""
+    rng = np.random.default_rng(42)
+    b = synth.random_batch(rng, 20, 64, nmax=30, allow_empty_graphs=False)
+    gap = 5
+    ro = np.array([int(b.row_off[i]) + gap * i for i in range(b.batch + 1)], dtype=np.int64)
+    Np = int(ro[-1])
+    rp = np.zeros(Np + 1, dtype=np.int32)
+    Bp = np.zeros((Np, 64), dtype=np.float32)
+    for i in range(b.batch):
+        n = int(b.sizes[i])
+        rp[ro[i]:ro[i] + n + 1] = b.row_ptr[b.row_off[i]:b.row_off[i] + n + 1]
+        rp[ro[i] + n:ro[i + 1]] = b.row_ptr[b.row_off[i + 1]]
+        Bp[ro[i]:ro[i] + n] = b.B[b.row_off[i]:b.row_off[i + 1]]
+    rp[Np] = b.row_ptr[-1]
+    Cd = torch.full((Np, 64), float("nan"), device=DEV)
+    h.set_hints(0, 0)
+    h.csr(T(ro), T(b.sizes), T(rp), T(b.col), T(b.vals), T(Bp), Cd)
+    C = Cd.cpu().numpy()
+    Cref = oracle.spmm_f32(64, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+    for i in range(b.batch):
+        n = int(b.sizes[i])
+        assert np.array_equal(C[ro[i]:ro[i] + n], Cref[b.row_off[i]:b.row_off[i + 1]])
+        assert np.all(np.isnan(C[ro[i] + n:ro[i + 1]]))
+
+
+def test_large_matrices_direct_path(h):
+    """Matrices beyond the stage capacity (paper case 3) run from global memory."""
+    for k in (256, 7):
+        b = synth.generate(synth.MIX, (1500, 3000, 1, 8), 3, k, seed=77)
+        h.set_hints(64, 512)  # deliberately too small: forces the direct path
+        C = run_csr(h, b, hints=False)
+        assert_parity(b, C, f"direct k={k}")
+        # and with hints large enough that some units stage, mixed with direct ones
+        assert_parity(b, run_csr(h, b, hints=True), f"mixed k={k}")
+
+
+def test_empty_batch_and_empty_graphs(h):
+    b = synth.random_batch(np.random.default_rng(3), 6, 32, nmax=0)   # every graph has n_i = 0
+    assert b.n_rows == 0
+    run_csr(h, b)
+    h.csr(T(np.zeros(1, np.int64)), None, T(np.zeros(1, np.int32)), T(np.zeros(0, np.int32)),
+          T(np.zeros(0, np.float32)), torch.zeros((0, 8), device=DEV), torch.zeros((0, 8), device=DEV), batch=0)
+    torch.cuda.synchronize()
+
+
+def test_tuning_space_bitwise(h):
+    """Every (kt, warps, CTAs/SM) choice computes the same bits (storage-order FMA)."""
+    b = synth.config(4)
+    ref = run_csr(h, b)
+    for kt in (32, 64, 128, 256, 512):
+        for warps in (1, 4, 8, 16):
+            for ctas in (1, 2):
+                h.set_tuning(kt, warps, ctas)
+                C = run_csr(h, b)
+                assert np.array_equal(C.view(np.uint32), ref.view(np.uint32)), (kt, warps, ctas)
+    h.set_tuning(0, 0, 0)
+
+
+def test_deterministic_repeat(h):
+    b = synth.config(3)
+    a = run_csr(h, b)
+    c = run_csr(h, b)
+    assert np.array_equal(a.view(np.uint32), c.view(np.uint32))
+
+
+# ------------------------------------------------------------ a-2 COO -> CSR
+
+def test_coo2csr_bit_exact_configs(h):
+    for cid in (1, 3):
+        b = synth.config(cid, coo=True)
+        rp, col, v = h.coo2csr(T(b.row_off), None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), b.n_rows)
+        torch.cuda.synchronize()
+        orp, ocol, ov = oracle.coo2csr(b.row_off, None, b.nnz_off, b.coo_idx, b.coo_vals)
+        assert np.array_equal(rp.cpu().numpy(), orp)
+        assert np.array_equal(col.cpu().numpy(), ocol)
+        assert np.array_equal(v.cpu().numpy().view(np.uint32), ov.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_coo2csr_adversarial(h, seed):
+    rng = np.random.default_rng(500 + seed)
+    b = synth.random_batch(rng, int(rng.integers(1, 50)), 4, nmax=40, dmax=8, duplicates=True)
+    rp, col, v = h.coo2csr(T(b.row_off), T(b.sizes), T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), b.n_rows)
+    orp, ocol, ov = oracle.coo2csr(b.row_off, b.sizes, b.nnz_off, b.coo_idx, b.coo_vals)
+    assert np.array_equal(rp.cpu().numpy(), orp)
+    assert np.array_equal(col.cpu().numpy(), ocol)
+    assert np.array_equal(v.cpu().numpy().view(np.uint32), ov.view(np.uint32))
+
+
+def test_coo2csr_global_fallback(h):
+    """A matrix with more entries than the shared-memory sort capacity (global merge path)."""
+    rng = np.random.default_rng(9)
+    n, m = 3000, 20000
+    idx = np.stack([rng.integers(0, n, m), rng.integers(0, n, m)], 1).astype(np.int32)
+    idx[1000:1100] = idx[0]                                  # duplicates across the range
+    vals = rng.standard_normal(m).astype(np.float32)
+    ro = np.array([0, 7, 7 + n, 7 + n + 5], dtype=np.int64)
+    sizes = np.array([7, n, 5], dtype=np.int32)
+    small = np.array([[1, 2], [0, 0], [6, 6]], dtype=np.int32)
+    allidx = np.concatenate([small, idx, np.array([[4, 4]], np.int32)])
+    allv = np.concatenate([np.ones(3, np.float32), vals, np.ones(1, np.float32)])
+    no = np.array([0, 3, 3 + m, 4 + m], dtype=np.int64)
+    h.set_hints(0, 0)
+    rp, col, v = h.coo2csr(T(ro), T(sizes), T(no), T(allidx), T(allv), int(ro[-1]))
+    orp, ocol, ov = oracle.coo2csr(ro, sizes, no, allidx, allv)
+    assert np.array_equal(rp.cpu().numpy(), orp)
+    assert np.array_equal(col.cpu().numpy(), ocol)
+    assert np.array_equal(v.cpu().numpy().view(np.uint32), ov.view(np.uint32))
+
+
+@pytest.mark.parametrize("cid", [1, 3])
+def test_coo_spmm(h, cid):
+    b = synth.config(cid, coo=True)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    rp = torch.empty(b.n_rows + 1, dtype=torch.int32, device=DEV)
+    col = torch.empty(b.n_nnz, dtype=torch.int32, device=DEV)
+    v = torch.empty(b.n_nnz, dtype=torch.float32, device=DEV)
+    C = h.coo(None, T(b.sizes), T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B), csr_out=(rp, col, v))
+    C2 = h.coo(T(b.row_off), None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B))
+    torch.cuda.synchronize()
+    orp, ocol, ov = oracle.coo2csr(b.row_off, None, b.nnz_off, b.coo_idx, b.coo_vals)
+    assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(col.cpu().numpy(), ocol)
+    C32 = oracle.spmm_f32(b.k, b.row_off, None, orp, ocol, ov, b.B)
+    Cref, bound = oracle.spmm(b.k, b.row_off, None, orp, ocol, ov, b.B)
+    for Cg in (C.cpu().numpy(), C2.cpu().numpy()):
+        assert oracle.check_bound(Cg, Cref, bound)[0]
+        assert np.array_equal(Cg.view(np.uint32), C32.view(np.uint32))
+
+
+# ------------------------------------------------------------ a-7 shards (one-GPU emulation)
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_shard_emulation_bitwise(h, G):
+    b = synth.config(2)
+    full = run_csr(h, b)
+    split = bs.partition(b.nnz_off, b.k, G)
+    assert np.array_equal(split, oracle.partition(b.nnz_off, b.k, G))
+    out = np.full_like(full, np.nan)
+    for r in range(G):
+        i0, i1 = int(split[r]), int(split[r + 1])
+        if i1 == i0:
+            continue
+        part = synth.config(2, i0=i0, i1=i1)           # regenerated per rank from per-graph seeds
+        Cr = run_csr(h, part)
+        out[b.row_off[i0]:b.row_off[i1]] = Cr
+    assert np.array_equal(out.view(np.uint32), full.view(np.uint32))
+
+
+# ------------------------------------------------------------ e2e host path
+
+@pytest.mark.parametrize("cid", [2, 4])
+def test_host_path_matches_device_path(h, cid):
+    b = synth.config(cid)
+    dev = run_csr(h, b)
+    C = h.csr_host(b.sizes, b.row_ptr, b.col, b.vals, b.B)
+    assert np.array_equal(C.view(np.uint32), dev.view(np.uint32))
+
+
+def test_host_path_chunked_pinned(h):
+    b = synth.config(5, i0=0, i1=20000)          # ~270 MB of B+C: several pipeline chunks
+    h.set_hints(60, 200)
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    C = torch.empty((b.n_rows, b.k), dtype=torch.float32).pin_memory()
+    h.csr_host(pin(b.sizes), pin(b.row_ptr), pin(b.col), pin(b.vals), pin(b.B), C)
+    rng = np.random.default_rng(1)
+    mat = rng.integers(0, b.batch, 400)
+    rl = np.array([rng.integers(0, b.sizes[i]) for i in mat], np.int32)
+    ref, bound = oracle.spmm_rows(mat, rl, b.k, b.row_off, b.row_ptr, b.col, b.vals, b.B)
+    got = C.numpy()[b.row_off[mat] + rl]
+    assert oracle.check_bound(got, ref, bound)[0]
+
+
+# ------------------------------------------------------------ VALIDATE
+
+def test_validate_flags_bad_index():
+    hv = bs.Handle(0, validate=True)
+    b = synth.config(1)
+    col = b.col.copy()
+    col[3] = 8                                    # == n_i: out of range
+    with pytest.raises(bs.BspmmError, match="INDEX"):
+        hv.csr(T(b.row_off), None, T(b.row_ptr), T(col), T(b.vals), T(b.B))
+    idx = b.coo_idx.copy()
+    idx[0, 0] = -1
+    with pytest.raises(bs.BspmmError, match="INDEX"):
+        hv.coo(T(b.row_off), None, T(b.nnz_off), T(idx), T(b.coo_vals), T(b.B))
+    with pytest.raises(bs.BspmmError, match="INDEX"):
+        hv.build_offsets(T(np.array([3, -1], np.int32)))
+    # valid input passes under VALIDATE and gives the same bits
+    C = hv.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B)).cpu().numpy()
+    assert_parity(b, C, "validate")
+
+
+def test_invalid_arguments_rejected(h):
+    b = synth.config(1)
+    with pytest.raises(bs.BspmmError, match="INVALID"):
+        h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), k=0)
+    Bd = T(b.B)
+    with pytest.raises(bs.BspmmError, match="INVALID"):
+        h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), Bd, C=Bd)
+
+
+# ------------------------------------------------------------ full size (BASELINE.json c5, bench launch config)
+
+def test_c5_full_size_sampled(h):
+    b = synth.config(5)
+    h.set_hints(60, int(b.nnz.max()))
+    Bd, Cd = T(b.B), torch.full((b.n_rows, b.k), float("nan"), device=DEV)
+    sizes = T(b.sizes)
+    ro = h.build_offsets(sizes)                        # the bench step: offsets + SpMM
+    h.csr(ro, None, T(b.row_ptr), T(b.col), T(b.vals), Bd, Cd)
+    torch.cuda.synchronize()
+    assert np.array_equal(ro.cpu().numpy(), b.row_off)
+    C = Cd.cpu().numpy()
+    rng = np.random.default_rng(2024)
+    mats = np.unique(rng.integers(0, b.batch, 600))
+    # whole sampled matrices: bound + bitwise against O3'
+    for i in mats[:150]:
+        g0, g1 = int(b.row_off[i]), int(b.row_off[i + 1])
+        z0, z1 = int(b.row_ptr[g0]), int(b.row_ptr[g1])
+        ro1 = np.array([0, g1 - g0], np.int64)
+        rp1 = b.row_ptr[g0:g1 + 1] - z0
+        ref32 = oracle.spmm_f32(b.k, ro1, None, rp1, b.col[z0:z1], b.vals[z0:z1], b.B[g0:g1])
+        assert np.array_equal(C[g0:g1].view(np.uint32), ref32.view(np.uint32)), i
+    rl = np.array([rng.integers(0, b.sizes[i]) for i in mats], np.int32)
+    ref, bound = oracle.spmm_rows(mats, rl, b.k, b.row_off, b.row_ptr, b.col, b.vals, b.B)
+    assert oracle.check_bound(C[b.row_off[mats] + rl], ref, bound)[0]
+    # property at any size: every row written (no NaN left), empty rows exact zero
+    assert not np.isnan(C).any()
