@@ -138,7 +138,8 @@ BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h);
  *  row_ptr  [row_off[batch]+1] dev int32: block-diagonal CSR row pointer
  *           holding ABSOLUTE positions into col_idx / vals.
  *  col_idx  [nnz] dev int32 LOCAL column ids, 0 <= c < n_i (square A_i).
- *  vals     [nnz] dev fp32.
+ *  vals     [nnz] dev fp32.  col_idx / vals / B / C may be NULL only when they
+ *           have no elements (no entries / no rows).
  *  B        [row_off[batch] x ldb] dev fp32 row-major, ldb >= k.
  *  C        same shape with ldc >= k; must not alias B.
  * Errors: INVALID_VALUE, CUDA, INDEX (VALIDATE only). */

@@ -49,6 +49,17 @@ def _check(t, name, dtype, device, ndim=None):
         raise ValueError(f"{name} must have {ndim} dims")
 
 
+def _ld(t: torch.Tensor, k: int, name: str) -> int:
+    """Leading dimension of a 2-D row-major fp32 matrix (empty matrices: k)."""
+    if t.dim() != 2:
+        raise ValueError(f"{name} must be 2-D")
+    if t.numel() == 0:
+        return max(k, 1)
+    if t.stride(1) != 1 and t.shape[1] > 1:
+        raise ValueError(f"{name} needs unit column stride")
+    return max(int(t.stride(0)), k) if t.shape[0] > 1 else max(int(t.shape[1]), k)
+
+
 class Handle:
     """One library handle per device (not thread-safe).  Calls enqueue on torch's
     current stream of the handle's device and return without synchronising."""
@@ -124,10 +135,10 @@ class Handle:
             k = B.shape[1]
         if C is None:
             C = torch.empty((B.shape[0], k), dtype=torch.float32, device=dev)
-        assert B.stride(1) == 1 and C.stride(1) == 1, "B and C need unit column stride"
+        ldb, ldc = _ld(B, k, "B"), _ld(C, k, "C")
         self._stream()
         st = lib.bspmm_csr(self._h, batch, k, _ptr(row_off), _ptr(sizes), _ptr(row_ptr), _ptr(col), _ptr(vals),
-                           _ptr(B), B.stride(0), _ptr(C), C.stride(0))
+                           _ptr(B), ldb, _ptr(C), ldc)
         self._raise(st, "bspmm_csr")
         return C
 
@@ -149,9 +160,10 @@ class Handle:
         if C is None:
             C = torch.empty((B.shape[0], k), dtype=torch.float32, device=dev)
         rp_o, col_o, val_o = csr_out if csr_out is not None else (None, None, None)
+        ldb, ldc = _ld(B, k, "B"), _ld(C, k, "C")
         self._stream()
         st = lib.bspmm_coo(self._h, batch, k, _ptr(row_off), _ptr(sizes), _ptr(nnz_off), _ptr(idx), _ptr(vals),
-                           _ptr(B), B.stride(0), _ptr(C), C.stride(0), int(total_rows), int(idx.shape[0]),
+                           _ptr(B), ldb, _ptr(C), ldc, int(total_rows), int(idx.shape[0]),
                            _ptr(rp_o), _ptr(col_o), _ptr(val_o))
         self._raise(st, "bspmm_coo")
         return C

@@ -73,6 +73,39 @@ bspmm_status_t check_validate_flag(bspmm_handle_t h) {
   return BSPMM_SUCCESS;
 }
 
+// persistent look-back scan workspace: grown on demand, zeroed once; epochs tag each call
+bspmm_status_t scan_state(bspmm_handle_t h, int32_t batch, ScanState* ss) {
+  const int32_t tiles = std::max<int32_t>(1, scan_tiles(batch));
+  if (tiles > h->scan_cap) {
+    const int32_t cap = std::max<int32_t>(tiles, 64);
+    const size_t bytes = 256 + al256((size_t)cap * 4) + 2 * al256((size_t)cap * 8);
+    if (h->scan_ws) {
+      CK(h, cudaStreamSynchronize(h->stream));
+      CK(h, cudaFree(h->scan_ws));
+      h->scan_ws = nullptr;
+      h->scan_cap = 0;
+    }
+    CK(h, cudaMalloc(&h->scan_ws, bytes));
+    CK(h, cudaMemsetAsync(h->scan_ws, 0, bytes, h->stream));
+    h->scan_cap = cap;
+    h->scan_ticket = 0;
+    h->scan_epoch = 0;
+  }
+  char* b = static_cast<char*>(h->scan_ws);
+  if (++h->scan_epoch >= (1u << 30)) {  // epoch wrap: clear the status words once
+    CK(h, cudaMemsetAsync(b + 256, 0, (size_t)h->scan_cap * 4, h->stream));
+    h->scan_epoch = 1;
+  }
+  ss->ticket = reinterpret_cast<unsigned long long*>(b);
+  ss->flags = reinterpret_cast<uint32_t*>(b + 256);
+  ss->agg = reinterpret_cast<int64_t*>(b + 256 + al256((size_t)h->scan_cap * 4));
+  ss->incl = ss->agg + al256((size_t)h->scan_cap * 8) / 8;
+  ss->ticket_base = h->scan_ticket;
+  ss->epoch = h->scan_epoch;
+  h->scan_ticket += (unsigned long long)tiles;
+  return BSPMM_SUCCESS;
+}
+
 bspmm_status_t plan_for(bspmm_handle_t h, int32_t batch, int32_t k, bool aligned, bspmm_plan_t* plan) {
   bspmm_status_t st = make_plan(k, batch, aligned, h->hint_rows, h->hint_nnz, h->num_sms, h->smem_optin,
                                 h->tune_kt, h->tune_warps, h->tune_ctas, plan);
@@ -142,6 +175,7 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (h->ws) cudaFree(h->ws);
     if (h->hbuf) cudaFree(h->hbuf);
     if (h->dev_flag) cudaFree(h->dev_flag);
+    if (h->scan_ws) cudaFree(h->scan_ws);
   }
   delete h;
   return st;
@@ -197,7 +231,10 @@ BSPMM_API bspmm_status_t bspmm_build_offsets(bspmm_handle_t h, int32_t batch, co
     bspmm_status_t st = check_validate_flag(h);
     if (st != BSPMM_SUCCESS) return st;
   }
-  CK(h, launch_offsets(batch, sizes, offsets_out, h->stream));
+  ScanState ss;
+  bspmm_status_t st = scan_state(h, batch, &ss);
+  if (st != BSPMM_SUCCESS) return st;
+  CK(h, launch_offsets(batch, sizes, offsets_out, ss, h->stream));
   h->launches++;
   return BSPMM_SUCCESS;
 }
@@ -229,8 +266,8 @@ BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, c
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
   if (batch < 0 || k < 1 || ldb < k || ldc < k) return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1 or ld<k");
   if (batch == 0) return BSPMM_SUCCESS;
-  if ((!row_off && !sizes) || !row_ptr || !col_idx || !vals || !B || !C)
-    return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  // col_idx / vals / B / C may be NULL only when they have no elements (caller's promise)
+  if ((!row_off && !sizes) || !row_ptr) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
   if (B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
   DeviceGuard g(h->device);
   if (!row_off) {

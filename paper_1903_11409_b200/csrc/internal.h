@@ -53,7 +53,18 @@ struct CsrArgs {
 
 // kernels (.cu)
 cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s);
-cudaError_t launch_offsets(int32_t batch, const int32_t* sizes, int64_t* out, cudaStream_t s);
+// decoupled look-back scan state (persistent per handle; epoch-tagged, never reset per call)
+struct ScanState {
+  uint32_t* flags;                 // [tiles] (epoch << 2) | {1: aggregate, 2: inclusive}
+  int64_t* agg;                    // [tiles]
+  int64_t* incl;                   // [tiles]
+  unsigned long long* ticket;      // monotone tile ticket counter
+  unsigned long long ticket_base;  // ticket value at this launch's start
+  uint32_t epoch;                  // 1 .. 2^30-1
+};
+int32_t scan_tiles(int32_t batch);
+cudaError_t launch_offsets(int32_t batch, const int32_t* sizes, int64_t* out, const ScanState& st,
+                           cudaStream_t s);
 cudaError_t launch_coo2csr(int32_t batch, const int64_t* row_off, const int32_t* sizes,
                            const int64_t* nnz_off, const int32_t* idx, const float* vals, int32_t* row_ptr,
                            int32_t* col_out, float* val_out, uint64_t* ws_keys, uint32_t* ws_pay,
@@ -83,6 +94,11 @@ struct bspmm_handle_s {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int* dev_flag = nullptr;
+  // offsets scan state: [ticket u64][flags u32 x cap][agg i64 x cap][incl i64 x cap]
+  void* scan_ws = nullptr;
+  int32_t scan_cap = 0;
+  unsigned long long scan_ticket = 0;
+  uint32_t scan_epoch = 0;
   // e2e host-path buffers and streams
   void* hbuf = nullptr;
   size_t hbuf_bytes = 0;

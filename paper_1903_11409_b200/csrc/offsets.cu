@@ -4,68 +4,131 @@
 // The paper builds the list of per-matrix pointers on the host and copies it
 // host->device inside the timed region; at small n_B
 // that copy decides the race against cuBLAS (:359).  Here the offsets are an
-// int64 exclusive scan of the sizes computed on the device: one CTA of 1024
-// threads, loads of 4 tiles in flight, warp-shuffle block scan per tile.
+// int64 exclusive scan of the int32 sizes computed on the device in one
+// launch: a single-pass decoupled look-back scan.  Each CTA takes a tile of
+// 4096 sizes (ticket order, so predecessors are always running), loads it
+// coalesced and transposes through shared memory, block-scans, publishes its
+// aggregate, looks back over its predecessors' aggregates / inclusive prefixes
+// (epoch-tagged status words: no per-call memset) and writes its offsets back
+// coalesced.
 #include <cstdint>
 
 #include "internal.h"
 
 namespace bspmm {
 
-constexpr int kScanThreads = 1024;
-constexpr int kScanTiles = 4;  // tiles of 1024 sizes loaded before scanning
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
 
-__global__ void __launch_bounds__(kScanThreads) offsets_kernel(int32_t batch, const int32_t* __restrict__ sizes,
-                                                               int64_t* __restrict__ out) {
-  __shared__ int64_t warp_tot[32];
-  __shared__ int64_t carry_s;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (t == 0) {
-    carry_s = 0;
-    out[0] = 0;
-  }
-  __syncthreads();
-  for (int64_t base = 0; base < batch; base += (int64_t)kScanThreads * kScanTiles) {
-    int32_t v[kScanTiles];
-#pragma unroll
-    for (int q = 0; q < kScanTiles; ++q) {
-      const int64_t idx = base + (int64_t)q * kScanThreads + t;
-      v[q] = idx < batch ? __ldg(sizes + idx) : 0;
-    }
-#pragma unroll
-    for (int q = 0; q < kScanTiles; ++q) {
-      // inclusive warp scan
-      int64_t x = v[q];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += y;
-      }
-      if (lane == 31) warp_tot[w] = x;
-      __syncthreads();
-      if (w == 0) {
-        int64_t s = warp_tot[lane];
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int64_t y = __shfl_up_sync(0xffffffffu, s, d);
-          if (lane >= d) s += y;
-        }
-        warp_tot[lane] = s;  // inclusive over warps
-      }
-      __syncthreads();
-      const int64_t carry = carry_s;
-      const int64_t incl = carry + (w ? warp_tot[w - 1] : 0) + x;
-      const int64_t idx = base + (int64_t)q * kScanThreads + t;
-      if (idx < batch) out[idx + 1] = incl;
-      __syncthreads();
-      if (t == kScanThreads - 1) carry_s = incl;
-      __syncthreads();
-    }
-  }
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-cudaError_t launch_offsets(int32_t batch, const int32_t* sizes, int64_t* out, cudaStream_t s) {
-  offsets_kernel<<<1, kScanThreads, 0, s>>>(batch, sizes, out);
+__global__ void __launch_bounds__(kScanThreads) offsets_kernel(int32_t batch, const int32_t* __restrict__ sizes,
+                                                               int64_t* __restrict__ out, ScanState st) {
+  // s_in (int32, padded every 32) and s_out (int64, padded every 16) share one buffer:
+  // s_in is fully consumed into registers before the barrier that precedes s_out's writes
+  __shared__ int64_t s_out[kScanTile + kScanTile / 16];
+  int32_t* s_in = reinterpret_cast<int32_t*>(s_out);
+  __shared__ int64_t warp_tot[kScanThreads / 32];
+  __shared__ int64_t s_excl;
+  __shared__ int32_t s_tile;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (t == 0) s_tile = (int32_t)(atomicAdd(st.ticket, 1ULL) - st.ticket_base);
+  __syncthreads();
+  const int32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * kScanTile;
+  // coalesced load, transpose to thread-contiguous through padded smem
+#pragma unroll
+  for (int it = 0; it < kScanItems; ++it) {
+    const int p = it * kScanThreads + t;
+    const int64_t g = base + p;
+    s_in[p + (p >> 5)] = g < batch ? __ldg(sizes + g) : 0;
+  }
+  __syncthreads();
+  int32_t v[kScanItems];
+  int64_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    const int p = t * kScanItems + j;
+    v[j] = s_in[p + (p >> 5)];
+    sum += v[j];
+  }
+  // block exclusive scan of the thread sums
+  int64_t x = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  int64_t wpre = 0, total = 0;
+#pragma unroll
+  for (int q = 0; q < kScanThreads / 32; ++q) {
+    if (q < w) wpre += warp_tot[q];
+    total += warp_tot[q];
+  }
+  const int64_t thread_excl = wpre + x - sum;
+  // decoupled look-back (one thread)
+  if (t == 0) {
+    const uint32_t tag = st.epoch << 2;
+    int64_t excl = 0;
+    if (tile == 0) {
+      st.incl[0] = total;
+      __threadfence();
+      st_volatile_u32(st.flags, tag | 2u);
+    } else {
+      st.agg[tile] = total;
+      __threadfence();
+      st_volatile_u32(st.flags + tile, tag | 1u);
+      for (int32_t p = tile - 1; p >= 0;) {
+        const uint32_t f = ld_volatile_u32(st.flags + p);
+        if ((f & ~3u) != tag || (f & 3u) == 0) continue;  // predecessor not published yet
+        __threadfence();
+        if ((f & 3u) == 2u) {
+          excl += *((volatile int64_t*)(st.incl + p));
+          break;
+        }
+        excl += *((volatile int64_t*)(st.agg + p));
+        --p;
+      }
+      st.incl[tile] = excl + total;
+      __threadfence();
+      st_volatile_u32(st.flags + tile, tag | 2u);
+    }
+    s_excl = excl;
+  }
+  __syncthreads();
+  int64_t run = s_excl + thread_excl;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    run += v[j];
+    const int p = t * kScanItems + j;
+    s_out[p + (p >> 4)] = run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kScanItems; ++it) {
+    const int p = it * kScanThreads + t;
+    const int64_t g = base + p;
+    if (g < batch) out[g + 1] = s_out[p + (p >> 4)];
+  }
+  if (tile == 0 && t == 0) out[0] = 0;
+}
+
+int32_t scan_tiles(int32_t batch) { return (int32_t)ceil_div(batch, kScanTile); }
+
+cudaError_t launch_offsets(int32_t batch, const int32_t* sizes, int64_t* out, const ScanState& st,
+                           cudaStream_t s) {
+  if (batch <= 0) return cudaMemsetAsync(out, 0, sizeof(int64_t), s);
+  offsets_kernel<<<scan_tiles(batch), kScanThreads, 0, s>>>(batch, sizes, out, st);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,138 @@
+#!/usr/bin/env python
+"""Kernel-level timing of the batched SpMM on one GPU, per BASELINE.json config,
+with an optional tuning sweep.  Steady state: R back-to-back launches captured
+in a CUDA graph, cycling over M replicas of (B, C, structure) whose total
+footprint exceeds 2x L2, so every launch reads B from HBM (SURVEY §8(d) T-evt).
+
+  python tools/kbench.py --configs 2,3,4,5 [--sweep] [--reps 200]
+"""
+import argparse
+import itertools
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1903_11409_b200 as bs  # noqa: E402
+import synth  # noqa: E402
+from bench import alg_bytes, peaks  # noqa: E402
+
+L2 = 126 * 2 ** 20
+
+
+def setup(cid, dev):
+    b = synth.config(cid)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    per = alg_bytes(b.n_rows, b.n_nnz, b.k, b.batch)
+    M = max(1, min(64, int(np.ceil(2 * L2 / per))))
+    reps = []
+    for _ in range(M):
+        reps.append(dict(ro=T(b.row_off), rp=T(b.row_ptr), col=T(b.col), vals=T(b.vals), B=T(b.B),
+                         C=torch.empty((b.n_rows, b.k), device=dev), sizes=T(b.sizes)))
+    return b, reps, per
+
+
+def time_calls(h, reps, R, fn, graph=True):
+    M = len(reps)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for i in range(3 * M):
+            fn(h, reps[i % M])
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(R):
+                fn(h, reps[i % M])
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / R
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(R):
+        fn(h, reps[i % M])
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / R
+
+
+def spmm_only(h, r):
+    h.csr(r["ro"], None, r["rp"], r["col"], r["vals"], r["B"], r["C"])
+
+
+def full_step(h, r):
+    h.build_offsets(r["sizes"], out=r["ro"])
+    h.csr(r["ro"], None, r["rp"], r["col"], r["vals"], r["B"], r["C"])
+
+
+def offsets_only(h, r):
+    h.build_offsets(r["sizes"], out=r["ro"])
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="2,3,4,5")
+    ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--kts", default="0,32,64,128,256,512")
+    ap.add_argument("--warps", default="0,4,8,12,16")
+    ap.add_argument("--ctas", default="0,1,2")
+    ap.add_argument("--ncu-mode", action="store_true", help="plain launches only (for ncu)")
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    peak, _ = peaks()
+    h = bs.Handle(0)
+    for cid in [int(c) for c in args.configs.split(",")]:
+        b, reps, per = setup(cid, dev)
+        h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+        R = args.reps if cid != 5 else max(10, args.reps // 20)
+        if args.ncu_mode:
+            for i in range(6):
+                full_step(h, reps[i % len(reps)])
+            torch.cuda.synchronize()
+            print(json.dumps({"config": cid, "ncu_mode": True, "plan": h.last_plan()}), flush=True)
+            del reps
+            torch.cuda.empty_cache()
+            continue
+        combos = [(0, 0, 0)]
+        if args.sweep:
+            combos = list(itertools.product([int(x) for x in args.kts.split(",")],
+                                            [int(x) for x in args.warps.split(",")],
+                                            [int(x) for x in args.ctas.split(",")]))
+        for kt, w, c in combos:
+            if kt and kt > b.k:
+                continue
+            h.set_tuning(kt, w, c)
+            try:
+                ms = time_calls(h, reps, R, spmm_only)
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "error": str(e)}), flush=True)
+                continue
+            plan = h.last_plan()
+            gbs = per / (ms / 1e3) / 1e9
+            print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "us": ms * 1e3, "GBs": gbs,
+                              "frac": gbs / peak, "GFLOPs": 2 * b.n_nnz * b.k / (ms / 1e3) / 1e9,
+                              "replicas": len(reps), "plan": plan}), flush=True)
+        h.set_tuning(0, 0, 0)
+        ms_step = time_calls(h, reps, R, full_step)
+        ms_off = time_calls(h, reps, R, offsets_only)
+        ms_ng = time_calls(h, reps, min(R, 50), spmm_only, graph=False)
+        print(json.dumps({"config": cid, "step_us": ms_step * 1e3, "offsets_us": ms_off * 1e3,
+                          "spmm_us_no_graph": ms_ng * 1e3, "alg_bytes": per}), flush=True)
+        del reps
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
