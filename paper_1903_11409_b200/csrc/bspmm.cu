@@ -88,7 +88,6 @@ bspmm_status_t scan_state(bspmm_handle_t h, int32_t batch, ScanState* ss) {
     CK(h, cudaMalloc(&h->scan_ws, bytes));
     CK(h, cudaMemsetAsync(h->scan_ws, 0, bytes, h->stream));
     h->scan_cap = cap;
-    h->scan_ticket = 0;
     h->scan_epoch = 0;
   }
   char* b = static_cast<char*>(h->scan_ws);
@@ -100,9 +99,7 @@ bspmm_status_t scan_state(bspmm_handle_t h, int32_t batch, ScanState* ss) {
   ss->flags = reinterpret_cast<uint32_t*>(b + 256);
   ss->agg = reinterpret_cast<int64_t*>(b + 256 + al256((size_t)h->scan_cap * 4));
   ss->incl = ss->agg + al256((size_t)h->scan_cap * 8) / 8;
-  ss->ticket_base = h->scan_ticket;
   ss->epoch = h->scan_epoch;
-  h->scan_ticket += (unsigned long long)tiles;
   return BSPMM_SUCCESS;
 }
 
@@ -230,6 +227,10 @@ BSPMM_API bspmm_status_t bspmm_build_offsets(bspmm_handle_t h, int32_t batch, co
     h->launches++;
     bspmm_status_t st = check_validate_flag(h);
     if (st != BSPMM_SUCCESS) return st;
+  }
+  if (batch == 0) {
+    CK(h, cudaMemsetAsync(offsets_out, 0, sizeof(int64_t), h->stream));
+    return BSPMM_SUCCESS;
   }
   ScanState ss;
   bspmm_status_t st = scan_state(h, batch, &ss);

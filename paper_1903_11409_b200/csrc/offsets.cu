@@ -40,7 +40,15 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(int32_t batch, co
   __shared__ int64_t s_excl;
   __shared__ int32_t s_tile;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (t == 0) s_tile = (int32_t)(atomicAdd(st.ticket, 1ULL) - st.ticket_base);
+  // let a PDL-launched dependent (the SpMM) start its prologue now
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (t == 0) {
+    // ticket order guarantees every predecessor tile is already running; the
+    // CTA drawing the last ticket resets the counter for the next launch
+    const unsigned long long tk = atomicAdd(st.ticket, 1ULL);
+    if (tk == (unsigned long long)gridDim.x - 1) atomicExch(st.ticket, 0ULL);
+    s_tile = (int32_t)tk;
+  }
   __syncthreads();
   const int32_t tile = s_tile;
   const int64_t base = (int64_t)tile * kScanTile;
@@ -76,34 +84,50 @@ __global__ void __launch_bounds__(kScanThreads) offsets_kernel(int32_t batch, co
     total += warp_tot[q];
   }
   const int64_t thread_excl = wpre + x - sum;
-  // decoupled look-back (one thread)
-  if (t == 0) {
+  // decoupled look-back, warp-parallel: lane l inspects predecessor tile - 1 - l
+  if (w == 0) {
     const uint32_t tag = st.epoch << 2;
     int64_t excl = 0;
     if (tile == 0) {
-      st.incl[0] = total;
-      __threadfence();
-      st_volatile_u32(st.flags, tag | 2u);
-    } else {
-      st.agg[tile] = total;
-      __threadfence();
-      st_volatile_u32(st.flags + tile, tag | 1u);
-      for (int32_t p = tile - 1; p >= 0;) {
-        const uint32_t f = ld_volatile_u32(st.flags + p);
-        if ((f & ~3u) != tag || (f & 3u) == 0) continue;  // predecessor not published yet
+      if (lane == 0) {
+        st.incl[0] = total;
         __threadfence();
-        if ((f & 3u) == 2u) {
-          excl += *((volatile int64_t*)(st.incl + p));
-          break;
-        }
-        excl += *((volatile int64_t*)(st.agg + p));
-        --p;
+        st_volatile_u32(st.flags, tag | 2u);
       }
-      st.incl[tile] = excl + total;
-      __threadfence();
-      st_volatile_u32(st.flags + tile, tag | 2u);
+    } else {
+      if (lane == 0) {
+        st.agg[tile] = total;
+        __threadfence();
+        st_volatile_u32(st.flags + tile, tag | 1u);
+      }
+      for (int32_t hi = tile - 1; hi >= 0; hi -= 32) {
+        const int32_t p = hi - lane;
+        uint32_t state = 2u;  // tiles before 0 act as an inclusive zero
+        int64_t val = 0;
+        if (p >= 0) {
+          uint32_t f;
+          do {
+            f = ld_volatile_u32(st.flags + p);
+          } while ((f & ~3u) != tag || (f & 3u) == 0u);
+          __threadfence();
+          state = f & 3u;
+          val = state == 2u ? *((volatile int64_t*)(st.incl + p)) : *((volatile int64_t*)(st.agg + p));
+        }
+        const uint32_t incl_mask = __ballot_sync(0xffffffffu, state == 2u);
+        const int stop = incl_mask ? __ffs(incl_mask) - 1 : 31;  // nearest inclusive predecessor
+        int64_t part = lane <= stop ? val : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+        excl += part;
+        if (incl_mask) break;
+      }
+      if (lane == 0) {
+        st.incl[tile] = excl + total;
+        __threadfence();
+        st_volatile_u32(st.flags + tile, tag | 2u);
+      }
     }
-    s_excl = excl;
+    if (lane == 0) s_excl = excl;
   }
   __syncthreads();
   int64_t run = s_excl + thread_excl;

@@ -48,15 +48,24 @@ struct SpmmParams {
 };
 
 struct __align__(16) UnitHdr {
-  int64_t g0;      // first global row of the matrix
-  int32_t n;       // rows (n_i)
-  int32_t nz0;     // absolute position of the matrix's first entry
-  int32_t nnz;     // entries of the matrix
-  int32_t c0;      // first column of the tile
-  int32_t kw;      // tile width (ragged last tile)
-  int32_t staged;  // 1: tile + structure are in the stage
+  int64_t g0;     // first global row of the matrix
+  int32_t n;      // rows (n_i)
+  int32_t nz0;    // absolute position of the matrix's first entry
+  int32_t nnz;    // entries of the matrix
+  int32_t c0;     // first column of the tile
+  int32_t kw;     // tile width (ragged last tile)
+  int32_t flags;  // bit0: B tile staged in smem; bit1: CSR structure staged in smem
 };
 static_assert(sizeof(UnitHdr) == kHdrBytes, "header size");
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
 
 template <bool VEC>
 __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem) {
@@ -69,7 +78,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
   const uint64_t pol = policy_evict_first();
 
   int64_t m_g0 = 0;
-  int32_t m_n = 0, m_nz0 = 0, m_nnz = 0, m_c0 = 0, m_kw = 0;
+  int32_t m_n = 0, m_nz0 = 0, m_nz1 = 0, m_c0 = 0, m_kw = 0;
   int j = 0;
   for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
     if ((j & 31) == 0) {  // metadata for the next 32 units, one lane each
@@ -77,19 +86,17 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
       if (uu < p.units) {
         const int64_t i = uu / p.tiles;
         const int32_t t = (int32_t)(uu - i * p.tiles);
-        m_g0 = p.row_off[i];
+        m_g0 = p.row_off[i];                                                  // round trip 1
         m_n = p.sizes ? p.sizes[i] : (int32_t)(p.row_off[i + 1] - m_g0);
-        m_nz0 = p.row_ptr[m_g0];
-        m_nnz = p.row_ptr[m_g0 + m_n] - m_nz0;
         m_c0 = t * p.kt;
         m_kw = min(p.kt, p.k - m_c0);
+        m_nz0 = p.row_ptr[m_g0];                                              // round trip 2 (in flight)
+        m_nz1 = p.row_ptr[m_g0 + m_n];
       }
     }
     const int src = j & 31;
     const int64_t g0 = __shfl_sync(0xffffffffu, m_g0, src);
     const int32_t n = __shfl_sync(0xffffffffu, m_n, src);
-    const int32_t nz0 = __shfl_sync(0xffffffffu, m_nz0, src);
-    const int32_t nnz = __shfl_sync(0xffffffffu, m_nnz, src);
     const int32_t c0 = __shfl_sync(0xffffffffu, m_c0, src);
     const int32_t kw = __shfl_sync(0xffffffffu, m_kw, src);
 
@@ -97,31 +104,35 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
     const uint32_t phase = (uint32_t)(j / p.stages) & 1u;
     mbar_wait(&empty[s], phase ^ 1u);
     unsigned char* st = ring + (size_t)s * stage_bytes;
-    const bool staged = (int64_t)n * kw * 4 <= p.stage_b && 8LL * nnz + 4LL * (n + 1) <= p.stage_s;
-    const uint32_t tx = (VEC && staged) ? (uint32_t)n * (uint32_t)kw * 4u : 0u;
-    if (lane == 0) {
-      UnitHdr h;
-      h.g0 = g0; h.n = n; h.nz0 = nz0; h.nnz = nnz; h.c0 = c0; h.kw = kw; h.staged = staged ? 1 : 0;
-      hdr[s] = h;
-      mbar_arrive_expect_tx(&full[s], tx);  // release: header visible to consumers
-    }
-    if (staged) {
-      const float* bsrc = p.B + g0 * p.ldb + c0;
-      if (VEC) {
-        if (kw == p.ldb) {  // whole contiguous B_i: one bulk copy
-          if (lane == 0 && tx) bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
-        } else {
-          for (int r = lane; r < n; r += 32)
-            bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
-        }
+    const bool bst = (int64_t)n * kw * 4 <= p.stage_b;
+    const float* bsrc = p.B + g0 * p.ldb + c0;
+    // a-4: the B tile goes out first: it needs round trip 1 only
+    if (VEC && bst && n > 0) {
+      const uint32_t tx = (uint32_t)n * (uint32_t)kw * 4u;
+      if (lane == 0) mbar_expect_tx(&full[s], tx);
+      __syncwarp();
+      if (kw == p.ldb) {  // the whole contiguous B_i: one bulk copy
+        if (lane == 0) bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
       } else {
-        float* dst = reinterpret_cast<float*>(st);
-        const int32_t total = n * kw;
-        for (int32_t q = lane; q < total; q += 32) {
-          const int32_t r = q / kw, c = q - r * kw;
-          cp_async4(dst + q, bsrc + (int64_t)r * p.ldb + c);
-        }
+        for (int r = lane; r < n; r += 32)
+          bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
       }
+    }
+    // now wait for round trip 2 (keeps the copies above ahead of this stall)
+    int32_t nz0r = m_nz0, nz1r = m_nz1;
+    asm volatile("" : "+r"(nz0r), "+r"(nz1r)::"memory");
+    const int32_t nz0 = __shfl_sync(0xffffffffu, nz0r, src);
+    const int32_t nnz = __shfl_sync(0xffffffffu, nz1r, src) - nz0;
+    const bool sst = 8LL * nnz + 4LL * (n + 1) <= p.stage_s;
+    if (!VEC && bst) {
+      float* dst = reinterpret_cast<float*>(st);
+      const int32_t total = n * kw;
+      for (int32_t q = lane; q < total; q += 32) {
+        const int32_t r = q / kw, c = q - r * kw;
+        cp_async4(dst + q, bsrc + (int64_t)r * p.ldb + c);
+      }
+    }
+    if (sst) {
       int32_t* pairs = reinterpret_cast<int32_t*>(st + p.stage_b);
       for (int32_t e = lane; e < nnz; e += 32) {
         cp_async4(pairs + 2 * e, p.col + nz0 + e);
@@ -130,63 +141,103 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
       int32_t* rp = pairs + 2 * nnz;
       for (int32_t r = lane; r <= n; r += 32) cp_async4(rp + r, p.row_ptr + g0 + r);
     }
+    if (lane == 0) {
+      UnitHdr h;
+      h.g0 = g0; h.n = n; h.nz0 = nz0; h.nnz = nnz; h.c0 = c0; h.kw = kw;
+      h.flags = (bst ? 1 : 0) | (sst ? 2 : 0);
+      hdr[s] = h;
+      mbar_arrive(&full[s]);  // release: header visible to consumers
+    }
     cp_async_arrive_noinc(&full[s]);  // 32 arrivals, each after its lane's copies land
   }
 }
 
-// one sub-warp row loop; VEC: float4 chunks, else scalar chunks
-template <int CH, bool VEC, bool STAGED>
+// a-5/a-6 for one unit: a sub-warp of L lanes owns a row; each lane owns CH
+// column chunks (float4 when VEC).  Up to G entries of a row are loaded ahead
+// (independent shared-memory loads), then accumulated strictly in storage
+// order, so the result is bitwise the fp32 storage-order FMA sum (O3').
+template <int CH, bool VEC, bool BST, bool SST>
 __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
                                      int step, int li) {
+  constexpr int G = CH >= 4 ? 2 : 4;
   const int L = p.lanes;
   const int32_t cols = VEC ? (h.kw >> 2) : h.kw;  // chunks of 4 (VEC) or 1 column
   const int32_t* rp;
   const int2* pr = nullptr;
   const float* Bbase;
   int64_t bstride;  // floats between consecutive B rows
-  if (STAGED) {
+  if (SST) {
     pr = reinterpret_cast<const int2*>(st + p.stage_b);
     rp = reinterpret_cast<const int32_t*>(st + p.stage_b) + 2 * h.nnz;
+  } else {
+    rp = p.row_ptr + h.g0;
+  }
+  if (BST) {
     Bbase = reinterpret_cast<const float*>(st);
     bstride = h.kw;
   } else {
-    rp = p.row_ptr + h.g0;
     Bbase = p.B + h.g0 * p.ldb + h.c0;
     bstride = p.ldb;
   }
-  for (int r = first; r < h.n; r += step) {
-    const int32_t e0 = rp[r] - h.nz0, e1 = rp[r + 1] - h.nz0;
+  int r = first;
+  int32_t nx0 = 0, nx1 = 0;
+  if (r < h.n) {
+    nx0 = rp[r];
+    nx1 = rp[r + 1];
+  }
+  for (; r < h.n; r += step) {
+    const int32_t e0 = nx0 - h.nz0, e1 = nx1 - h.nz0;
+    if (r + step < h.n) {  // next row's range, loaded ahead
+      nx0 = rp[r + step];
+      nx1 = rp[r + step + 1];
+    }
     float4 acc[CH];
 #pragma unroll
     for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 2
-    for (int32_t e = e0; e < e1; ++e) {
-      int32_t cidx;
-      float a;
-      if (STAGED) {
-        const int2 cv = pr[e];
-        cidx = cv.x;
-        a = __int_as_float(cv.y);
-      } else {
-        cidx = __ldg(p.col + h.nz0 + e);
-        a = __ldg(p.vals + h.nz0 + e);
-      }
-      const float* brow = Bbase + (int64_t)cidx * bstride;
+    for (int32_t e = e0; e < e1; e += G) {
+      const int32_t cnt = min(G, e1 - e);
+      int32_t cidx[G];
+      float a[G];
 #pragma unroll
-      for (int v = 0; v < CH; ++v) {
-        const int c = li + v * L;
-        if (c < cols) {
-          if (VEC) {
-            float4 b;
-            if (STAGED) b = reinterpret_cast<const float4*>(brow)[c];
-            else b = ldg_nc_f4(brow + 4 * c);
-            acc[v].x = fmaf(a, b.x, acc[v].x);
-            acc[v].y = fmaf(a, b.y, acc[v].y);
-            acc[v].z = fmaf(a, b.z, acc[v].z);
-            acc[v].w = fmaf(a, b.w, acc[v].w);
+      for (int q = 0; q < G; ++q) {
+        cidx[q] = 0;
+        a[q] = 0.f;
+        if (q < cnt) {
+          if (SST) {
+            const int2 cv = pr[e + q];
+            cidx[q] = cv.x;
+            a[q] = __int_as_float(cv.y);
           } else {
-            const float b = STAGED ? brow[c] : __ldg(brow + c);
-            acc[v].x = fmaf(a, b, acc[v].x);
+            cidx[q] = __ldg(p.col + h.nz0 + e + q);
+            a[q] = __ldg(p.vals + h.nz0 + e + q);
+          }
+        }
+      }
+      float4 b[G][CH];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const float* brow = Bbase + (int64_t)cidx[q] * bstride;
+#pragma unroll
+        for (int v = 0; v < CH; ++v) {
+          const int c = li + v * L;
+          b[q][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < cnt && c < cols) {
+            if (VEC) b[q][v] = BST ? reinterpret_cast<const float4*>(brow)[c] : ldg_nc_f4(brow + 4 * c);
+            else b[q][v].x = BST ? brow[c] : __ldg(brow + c);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        if (q < cnt) {
+#pragma unroll
+          for (int v = 0; v < CH; ++v) {
+            acc[v].x = fmaf(a[q], b[q][v].x, acc[v].x);
+            if (VEC) {
+              acc[v].y = fmaf(a[q], b[q][v].y, acc[v].y);
+              acc[v].z = fmaf(a[q], b[q][v].z, acc[v].z);
+              acc[v].w = fmaf(a[q], b[q][v].w, acc[v].w);
+            }
           }
         }
       }
@@ -223,8 +274,12 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
     const UnitHdr h = hdr[s];
     const unsigned char* st = ring + (size_t)s * stage_bytes;
-    if (h.staged) rows<CH, VEC, true>(p, h, st, first, step, li);
-    else rows<CH, VEC, false>(p, h, st, first, step, li);
+    switch (h.flags) {
+      case 3: rows<CH, VEC, true, true>(p, h, st, first, step, li); break;
+      case 1: rows<CH, VEC, true, false>(p, h, st, first, step, li); break;
+      case 2: rows<CH, VEC, false, true>(p, h, st, first, step, li); break;
+      default: rows<CH, VEC, false, false>(p, h, st, first, step, li); break;
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -238,12 +293,16 @@ __global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p) {
   if (threadIdx.x == 0) {
     const uint32_t W = (blockDim.x >> 5) - 1;
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1 + 32);  // producer lane-0 expect_tx + 32 cp.async arrivals
+      mbar_init(&full[s], 1 + 32);  // producer lane-0 arrive + 32 cp.async arrivals
       mbar_init(&empty[s], W);      // one arrival per consumer warp
     }
     fence_mbar_init();
   }
   __syncthreads();
+  // programmatic dependent launch: everything above overlapped the previous
+  // kernel (e.g. the offsets builder); global memory is touched only after this
+  pdl_wait();
+  pdl_launch_dependents();
   if ((threadIdx.x >> 5) == 0) produce<VEC>(p, smem);
   else consume<CH, VEC>(p, smem);
 }
@@ -259,8 +318,17 @@ static cudaError_t launch_t(const SpmmParams& sp, const bspmm_plan_t& plan, cuda
     if (e != cudaSuccess) return e;
     configured_bytes[dev & 63] = plan.smem_bytes;
   }
-  kern<<<plan.grid, plan.threads, plan.smem_bytes, s>>>(sp);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.grid);
+  cfg.blockDim = dim3(plan.threads);
+  cfg.dynamicSmemBytes = plan.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, sp);
 }
 
 cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s) {
