@@ -95,6 +95,13 @@ class Handle:
         self._raise(lib.bspmm_set_tuning(self._h, int(kt), int(consumer_warps), int(ctas_per_sm)),
                     "bspmm_set_tuning")
 
+    def set_trace(self, buf: Optional[torch.Tensor]):
+        """Debug: record per-CTA phase timestamps of subsequent SpMM launches into
+        buf (int64 [grid, 8] on the handle's device); None disables."""
+        if buf is not None:
+            _check(buf, "trace", torch.int64, self.device)
+        self._raise(lib.bspmm_set_trace(self._h, _ptr(buf)), "bspmm_set_trace")
+
     def sync(self):
         self._raise(lib.bspmm_sync(self._h), "bspmm_sync")
 

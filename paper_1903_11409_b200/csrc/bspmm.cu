@@ -199,6 +199,12 @@ BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t 
   return BSPMM_SUCCESS;
 }
 
+BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  h->trace = reinterpret_cast<unsigned long long*>(dev_buf);
+  return BSPMM_SUCCESS;
+}
+
 BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h) {
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
   DeviceGuard g(h->device);
@@ -255,7 +261,7 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   bspmm_plan_t plan;
   bspmm_status_t st = plan_for(h, batch, k, aligned, &plan);
   if (st != BSPMM_SUCCESS) return st;
-  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc};
+  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace};
   CK(h, launch_spmm_csr(a, plan, h->stream));
   if (plan.units > 0) h->launches++;
   return BSPMM_SUCCESS;
@@ -269,7 +275,7 @@ BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, c
   if (batch == 0) return BSPMM_SUCCESS;
   // col_idx / vals / B / C may be NULL only when they have no elements (caller's promise)
   if ((!row_off && !sizes) || !row_ptr) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
-  if (B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
+  if (B && B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
   DeviceGuard g(h->device);
   if (!row_off) {
     bspmm_status_t st = grow(h, &h->ws, &h->ws_bytes, al256((size_t)(batch + 1) * 8));
@@ -369,7 +375,7 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
     return fail(h, BSPMM_ERROR_INVALID_VALUE, "csr_*_out must be all NULL or all non-NULL");
   if ((!row_off && !sizes) || !nnz_off || !B || !C || (total_nnz > 0 && (!idx || !vals)))
     return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
-  if (B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
+  if (B && B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
   DeviceGuard g(h->device);
   CooWs w;
   bspmm_status_t st = coo_workspace(h, batch, total_rows, total_nnz, row_off == nullptr, !out_given, &w);

@@ -49,6 +49,7 @@ struct CsrArgs {
   int64_t ldb;
   float* C;
   int64_t ldc;
+  unsigned long long* trace;  // debug phase timestamps (bspmm_set_trace) or null
 };
 
 // kernels (.cu)
@@ -87,6 +88,7 @@ struct bspmm_handle_s {
   int64_t hint_nnz = 0;
   int32_t tune_kt = 0, tune_warps = 0, tune_ctas = 0;
   bspmm_plan_t last_plan{};
+  unsigned long long* trace = nullptr;  // debug: per-CTA phase timestamps
   int64_t launches = 0;
   std::string err;
   // device workspace (grown on demand)

@@ -45,7 +45,22 @@ struct SpmmParams {
   int64_t ldb;
   float* __restrict__ C;
   int64_t ldc;
+  unsigned long long* trace;  // debug: per-CTA phase timestamps (globaltimer ns), or null
 };
+
+// trace slots per CTA (bspmm_set_trace): 0 entry, 1 after PDL wait, 2 producer has unit-0 row
+// offsets, 3 producer has unit-0 structure offsets, 4 producer issued its last unit, 5 first
+// consumer warp saw unit 0 land, 6 first consumer warp finished its last unit, 7 CTA exit
+constexpr int kTraceSlots = 8;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define BSPMM_TRACE(p, slot) \
+  do {                      \
+    if (p.trace) p.trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = gtime(); \
+  } while (0)
 
 struct __align__(16) UnitHdr {
   int64_t g0;     // first global row of the matrix
@@ -99,6 +114,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
     const int32_t n = __shfl_sync(0xffffffffu, m_n, src);
     const int32_t c0 = __shfl_sync(0xffffffffu, m_c0, src);
     const int32_t kw = __shfl_sync(0xffffffffu, m_kw, src);
+    if (j == 0 && lane == 0) BSPMM_TRACE(p, 2);
 
     const int s = j % p.stages;
     const uint32_t phase = (uint32_t)(j / p.stages) & 1u;
@@ -124,6 +140,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
     const int32_t nz0 = __shfl_sync(0xffffffffu, nz0r, src);
     const int32_t nnz = __shfl_sync(0xffffffffu, nz1r, src) - nz0;
     const bool sst = 8LL * nnz + 4LL * (n + 1) <= p.stage_s;
+    if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
     if (!VEC && bst) {
       float* dst = reinterpret_cast<float*>(st);
       const int32_t total = n * kw;
@@ -150,6 +167,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
     }
     cp_async_arrive_noinc(&full[s]);  // 32 arrivals, each after its lane's copies land
   }
+  if (lane == 0) BSPMM_TRACE(p, 4);
 }
 
 // a-5/a-6 for one unit: a sub-warp of L lanes owns a row; each lane owns CH
@@ -272,6 +290,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
   for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
     const int s = j % p.stages;
     mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
+    if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
     const UnitHdr h = hdr[s];
     const unsigned char* st = ring + (size_t)s * stage_bytes;
     switch (h.flags) {
@@ -283,6 +302,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  if (cw == 0 && lane == 0) BSPMM_TRACE(p, 6);
 }
 
 template <int CH, bool VEC>
@@ -290,6 +310,7 @@ __global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
+  if (threadIdx.x == 0) BSPMM_TRACE(p, 0);
   if (threadIdx.x == 0) {
     const uint32_t W = (blockDim.x >> 5) - 1;
     for (int s = 0; s < p.stages; ++s) {
@@ -303,8 +324,13 @@ __global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p) {
   // kernel (e.g. the offsets builder); global memory is touched only after this
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
   if ((threadIdx.x >> 5) == 0) produce<VEC>(p, smem);
   else consume<CH, VEC>(p, smem);
+  if (p.trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) BSPMM_TRACE(p, 7);
+  }
 }
 
 template <int CH, bool VEC>
@@ -351,6 +377,7 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.ldb = a.ldb;
   sp.C = a.C;
   sp.ldc = a.ldc;
+  sp.trace = a.trace;
   if (plan.vec) {
     switch (plan.chunks) {
       case 1: return launch_t<1, true>(sp, plan, s);

@@ -1,0 +1,66 @@
+#!/usr/bin/env python
+"""Phase timeline of one SpMM launch (bspmm_set_trace): per-CTA %globaltimer
+stamps, reported as min / median / max over CTAs relative to the earliest
+CTA entry.  L2 is flushed (256 MB write) before the traced launch.
+
+  python tools/trace.py --config 4 [--kt 128 --warps 16 --ctas 1]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1903_11409_b200 as bs  # noqa: E402
+import synth  # noqa: E402
+
+SLOTS = ["entry", "after_pdl_wait", "prod_rowoff", "prod_struct_off", "prod_done", "cons_first_full",
+         "cons_done", "exit"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--kt", type=int, default=0)
+    ap.add_argument("--warps", type=int, default=0)
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--launches", type=int, default=3)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    b = synth.config(args.config)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    h = bs.Handle(0)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    h.set_tuning(args.kt, args.warps, args.ctas)
+    ro, rp, col, vals, B = T(b.row_off), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)
+    C = torch.empty((b.n_rows, b.k), device=dev)
+    h.csr(ro, None, rp, col, vals, B, C)
+    grid = h.last_plan()["grid"]
+    buf = torch.zeros((grid, 8), dtype=torch.int64, device=dev)
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device=dev)
+    for it in range(args.launches):
+        flush.fill_(float(it))
+        torch.cuda.synchronize()
+        h.set_trace(buf)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h.csr(ro, None, rp, col, vals, B, C)
+        e1.record()
+        h.set_trace(None)
+        torch.cuda.synchronize()
+        t = buf.cpu().numpy().astype(np.int64)
+        t0 = t[:, 0].min()
+        rel = (t - t0) / 1e3  # us
+        out = {"config": args.config, "launch": it, "event_us": e0.elapsed_time(e1) * 1e3, "plan": h.last_plan(),
+               "span_us": float((t[:, 7].max() - t0) / 1e3)}
+        for k, name in enumerate(SLOTS):
+            col_ = rel[:, k]
+            out[name] = [round(float(col_.min()), 2), round(float(np.median(col_)), 2), round(float(col_.max()), 2)]
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
