@@ -122,16 +122,24 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
     unsigned char* st = ring + (size_t)s * stage_bytes;
     const bool bst = (int64_t)n * kw * 4 <= p.stage_b;
     const float* bsrc = p.B + g0 * p.ldb + c0;
-    // a-4: the B tile goes out first: it needs round trip 1 only
+    // a-4: the B tile goes out first: it needs round trip 1 only.  The whole
+    // contiguous B_i is one TMA bulk copy; a k-tile (strided rows) is moved
+    // with coalesced 16-byte cp.async (a warp instruction per 512 B of a row):
+    // many small bulk copies serialise on the TMA engine (tools/trace.py).
     if (VEC && bst && n > 0) {
-      const uint32_t tx = (uint32_t)n * (uint32_t)kw * 4u;
-      if (lane == 0) mbar_expect_tx(&full[s], tx);
-      __syncwarp();
-      if (kw == p.ldb) {  // the whole contiguous B_i: one bulk copy
-        if (lane == 0) bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
+      if (kw == p.ldb) {
+        const uint32_t tx = (uint32_t)n * (uint32_t)kw * 4u;
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], tx);
+          bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
+        }
       } else {
-        for (int r = lane; r < n; r += 32)
-          bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
+        const int32_t kw4 = kw >> 2, total = n * kw4;
+        float4* dst = reinterpret_cast<float4*>(st);
+        for (int32_t q = lane; q < total; q += 32) {
+          const int32_t r = q / kw4, c = q - r * kw4;
+          cp_async16(dst + q, bsrc + (int64_t)r * p.ldb + 4 * c);
+        }
       }
     }
     // now wait for round trip 2 (keeps the copies above ahead of this stall)
