@@ -122,11 +122,16 @@ BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t 
                                           int32_t ctas_per_sm);
 
 /* Debug: per-CTA phase timestamps (%globaltimer, ns) of subsequent SpMM
- * launches are written to dev_buf [grid x 8] uint64 (slots: entry, after the
+ * launches are written to dev_buf [grid x 16] uint64 (slots: entry, after the
  * programmatic-launch wait, producer has unit-0 offsets, producer has unit-0
  * structure, producer done, first consumer warp sees unit 0, first consumer
- * warp done, CTA exit).  NULL disables (the default). */
+ * warp done, CTA exit, first consumer warp done with unit 0).  NULL disables
+ * (the default). */
 BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
+
+/* Debug: timing-experiment bits for subsequent SpMM launches.  1 = compute but
+ * do not store C (the result is then undefined).  0 (default) = normal. */
+BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */
 BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h);

@@ -97,10 +97,14 @@ class Handle:
 
     def set_trace(self, buf: Optional[torch.Tensor]):
         """Debug: record per-CTA phase timestamps of subsequent SpMM launches into
-        buf (int64 [grid, 8] on the handle's device); None disables."""
+        buf (int64 [grid, 16] on the handle's device); None disables."""
         if buf is not None:
             _check(buf, "trace", torch.int64, self.device)
         self._raise(lib.bspmm_set_trace(self._h, _ptr(buf)), "bspmm_set_trace")
+
+    def set_debug(self, bits: int):
+        """Debug bits for timing experiments (1 = skip C stores; results undefined)."""
+        self._raise(lib.bspmm_set_debug(self._h, int(bits)), "bspmm_set_debug")
 
     def sync(self):
         self._raise(lib.bspmm_sync(self._h), "bspmm_sync")

@@ -33,6 +33,7 @@ _SIGS = {
     "bspmm_set_tuning": (I32, [P, I32, I32, I32]),
     "bspmm_sync": (I32, [P]),
     "bspmm_set_trace": (I32, [P, P]),
+    "bspmm_set_debug": (I32, [P, I32]),
     "bspmm_csr": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
     "bspmm_coo": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64, I64, I64, P, P, P]),
     "bspmm_coo2csr": (I32, [P, I32, P, P, P, P, P, I64, I64, P, P, P]),

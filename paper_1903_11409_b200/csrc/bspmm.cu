@@ -205,6 +205,12 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
   return BSPMM_SUCCESS;
 }
 
+BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
+  if (!h || bits < 0 || bits > 1) return BSPMM_ERROR_INVALID_VALUE;
+  h->dbg = bits;
+  return BSPMM_SUCCESS;
+}
+
 BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h) {
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
   DeviceGuard g(h->device);
@@ -261,7 +267,7 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   bspmm_plan_t plan;
   bspmm_status_t st = plan_for(h, batch, k, aligned, &plan);
   if (st != BSPMM_SUCCESS) return st;
-  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace};
+  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg};
   CK(h, launch_spmm_csr(a, plan, h->stream));
   if (plan.units > 0) h->launches++;
   return BSPMM_SUCCESS;

@@ -50,6 +50,7 @@ struct CsrArgs {
   float* C;
   int64_t ldc;
   unsigned long long* trace;  // debug phase timestamps (bspmm_set_trace) or null
+  int32_t dbg;                // debug bits (bspmm_set_debug)
 };
 
 // kernels (.cu)
@@ -89,6 +90,7 @@ struct bspmm_handle_s {
   int32_t tune_kt = 0, tune_warps = 0, tune_ctas = 0;
   bspmm_plan_t last_plan{};
   unsigned long long* trace = nullptr;  // debug: per-CTA phase timestamps
+  int32_t dbg = 0;                      // debug bits: 1 = skip C stores
   int64_t launches = 0;
   std::string err;
   // device workspace (grown on demand)

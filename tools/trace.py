@@ -18,7 +18,7 @@ import paper_1903_11409_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 
 SLOTS = ["entry", "after_pdl_wait", "prod_rowoff", "prod_struct_off", "prod_done", "cons_first_full",
-         "cons_done", "exit"]
+         "cons_done", "exit", "cons_unit0_done"]
 
 
 def main():
@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--launches", type=int, default=3)
+    ap.add_argument("--nostore", action="store_true")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     b = synth.config(args.config)
@@ -39,7 +40,9 @@ def main():
     C = torch.empty((b.n_rows, b.k), device=dev)
     h.csr(ro, None, rp, col, vals, B, C)
     grid = h.last_plan()["grid"]
-    buf = torch.zeros((grid, 8), dtype=torch.int64, device=dev)
+    buf = torch.zeros((grid, 16), dtype=torch.int64, device=dev)
+    if args.nostore:
+        h.set_debug(1)
     flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device=dev)
     for it in range(args.launches):
         flush.fill_(float(it))
@@ -54,7 +57,7 @@ def main():
         t = buf.cpu().numpy().astype(np.int64)
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3  # us
-        out = {"config": args.config, "launch": it, "event_us": e0.elapsed_time(e1) * 1e3, "plan": h.last_plan(),
+        out = {"config": args.config, "launch": it, "nostore": args.nostore, "event_us": e0.elapsed_time(e1) * 1e3, "plan": h.last_plan(),
                "span_us": float((t[:, 7].max() - t0) / 1e3)}
         for k, name in enumerate(SLOTS):
             col_ = rel[:, k]
