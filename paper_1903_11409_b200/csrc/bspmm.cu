@@ -8,6 +8,8 @@
 #include <new>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "internal.h"
 
 using namespace bspmm;
@@ -101,6 +103,44 @@ bspmm_status_t scan_state(bspmm_handle_t h, int32_t batch, ScanState* ss) {
   ss->incl = ss->agg + al256((size_t)h->scan_cap * 8) / 8;
   ss->epoch = h->scan_epoch;
   return BSPMM_SUCCESS;
+}
+
+// 2-D TMA descriptors for the k-tiled staging path, cached per (B, k, ldb, kt).
+// Encoded with the driver's cuTensorMapEncodeTiled, fetched through the runtime
+// (no link-time libcuda dependency).  Returns nullptr when not applicable.
+const TmaMaps* tma_maps(bspmm_handle_t h, const float* B, int32_t k, int64_t ldb, int32_t kt) {
+  if (kt % 32 != 0 || kt > 256 || ldb == kt) return nullptr;
+  if (h->maps_ok && h->maps_B == B && h->maps_k == k && h->maps_ldb == ldb && h->maps_kt == kt) return &h->maps;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)0x7fffffff};  // rows: never read out of range
+  const cuuint64_t strides[1] = {(cuuint64_t)ldb * 4};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int b = 0; b < kTmaMaps; ++b) {
+    const cuuint32_t box[2] = {(cuuint32_t)kt, (cuuint32_t)(1u << b)};
+    CUresult r = encode(&h->maps.m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(B), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      h->maps_ok = false;
+      return nullptr;
+    }
+  }
+  h->maps_B = B;
+  h->maps_k = k;
+  h->maps_ldb = ldb;
+  h->maps_kt = kt;
+  h->maps_ok = true;
+  return &h->maps;
 }
 
 bspmm_status_t plan_for(bspmm_handle_t h, int32_t batch, int32_t k, bool aligned, bspmm_plan_t* plan) {
@@ -267,7 +307,8 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   bspmm_plan_t plan;
   bspmm_status_t st = plan_for(h, batch, k, aligned, &plan);
   if (st != BSPMM_SUCCESS) return st;
-  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg};
+  const TmaMaps* maps = plan.vec ? tma_maps(h, B, k, ldb, plan.kt) : nullptr;
+  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps};
   CK(h, launch_spmm_csr(a, plan, h->stream));
   if (plan.units > 0) h->launches++;
   return BSPMM_SUCCESS;

@@ -1,5 +1,6 @@
 // internal.h — private declarations shared by the libbspmm.so sources.
 #pragma once
+#include <cuda.h>  // CUtensorMap type only; the encoder is fetched via cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 
 #include <string>
@@ -38,6 +39,13 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool aligned, int32_t max_row
                          int32_t num_sms, int32_t smem_per_cta, int32_t kt_override, int32_t warps,
                          int32_t ctas_per_sm, bspmm_plan_t* out);
 
+// 2-D TMA descriptors over B [rows x k] (row pitch ldb) with box {kt, 2^b rows},
+// b = 0..8: a unit of n_i rows is staged with popcount(n_i) tensor copies
+constexpr int kTmaMaps = 9;
+struct TmaMaps {
+  CUtensorMap m[kTmaMaps];
+};
+
 struct CsrArgs {
   int32_t batch, k;
   const int64_t* row_off;
@@ -51,6 +59,7 @@ struct CsrArgs {
   int64_t ldc;
   unsigned long long* trace;  // debug phase timestamps (bspmm_set_trace) or null
   int32_t dbg;                // debug bits (bspmm_set_debug)
+  const TmaMaps* maps;        // non-null: full k-tiles are staged with 2-D tensor TMA
 };
 
 // kernels (.cu)
@@ -91,6 +100,12 @@ struct bspmm_handle_s {
   bspmm_plan_t last_plan{};
   unsigned long long* trace = nullptr;  // debug: per-CTA phase timestamps
   int32_t dbg = 0;                      // debug bits: 1 = skip C stores
+  // cached 2-D TMA descriptors (key: B, k, ldb, kt)
+  bspmm::TmaMaps maps{};
+  const void* maps_B = nullptr;
+  int64_t maps_ldb = 0;
+  int32_t maps_k = 0, maps_kt = 0;
+  bool maps_ok = false;
   int64_t launches = 0;
   std::string err;
   // device workspace (grown on demand)

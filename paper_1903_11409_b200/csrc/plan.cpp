@@ -53,9 +53,10 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
     while ((int64_t)batch * ceil_div(k, kt) < target_units && kt > 32) kt = align_up(kt / 2, quantum);
   }
   // structure capacity: (col, val) pairs + row pointer
-  int64_t s_bytes64 = align_up(8 * (int32_t)std::min<int64_t>(Z, 1 << 20), 16) + align_up(4 * (R + 1), 16);
+  // (stage regions are 128-byte aligned: 2-D TMA destinations)
+  int64_t s_bytes64 = align_up(align_up(8 * (int32_t)std::min<int64_t>(Z, 1 << 20), 16) + align_up(4 * (R + 1), 16), 128);
   auto stages_for = [&](int32_t kt_) {
-    int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 16);
+    int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 128);
     int64_t per = b + s_bytes64;
     int64_t s = 0;
     while (s < kMaxStages && ring_prefix_bytes((int32_t)(s + 1)) + (s + 1) * per <= budget) ++s;
@@ -65,12 +66,12 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
     while (stages_for(kt) < 2 && kt > quantum * 8) kt = align_up(kt / 2, quantum);
 
   int32_t stages = stages_for(kt);
-  int32_t b_bytes = align_up(std::max<int32_t>(16, R * kt * 4), 16);
+  int32_t b_bytes = align_up(std::max<int32_t>(16, R * kt * 4), 128);
   int32_t s_bytes = (int32_t)s_bytes64;
   if (stages < 1) {
     // even one stage does not fit: shrink capacities; bigger matrices go direct
-    s_bytes = std::min<int32_t>(s_bytes, budget / 4) / 16 * 16;
-    b_bytes = (budget - ring_prefix_bytes(1) - s_bytes) / 16 * 16;
+    s_bytes = std::min<int32_t>(s_bytes, budget / 4) / 128 * 128;
+    b_bytes = (budget - ring_prefix_bytes(1) - s_bytes) / 128 * 128;
     stages = 1;
   }
   p.kt = kt;

@@ -47,6 +47,7 @@ struct SpmmParams {
   int64_t ldc;
   unsigned long long* trace;  // debug: per-CTA phase timestamps (globaltimer ns), or null
   int32_t dbg;                // debug bits: 1 = skip C stores (timing experiments only)
+  int32_t tma2d;              // 1: full k-tiles staged with 2-D tensor TMA (maps valid)
 };
 
 // trace slots per CTA (bspmm_set_trace): 0 entry, 1 after PDL wait, 2 producer has unit-0 row
@@ -114,7 +115,7 @@ __device__ __forceinline__ void meta_rt2(const SpmmParams& p, int64_t uu, Meta& 
 }
 
 template <bool VEC>
-__device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem) {
+__device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem) {
   UnitHdr* hdr = reinterpret_cast<UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
@@ -154,25 +155,35 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
     unsigned char* st = ring + (size_t)s * stage_bytes;
     const bool bst = (int64_t)n * kw * 4 <= p.stage_b;
     const bool sst = 8LL * nnz + 4LL * (n + 1) <= p.stage_s;
-    // the (small) CSR structure first, then the B tile
-    if (sst) {
-      int32_t* pairs = reinterpret_cast<int32_t*>(st + p.stage_b);
-      for (int32_t e = lane; e < nnz; e += 32) {
-        cp_async4(pairs + 2 * e, p.col + nz0 + e);
-        cp_async4(pairs + 2 * e + 1, p.vals + nz0 + e);
-      }
-      int32_t* rp = pairs + 2 * nnz;
-      for (int32_t r = lane; r <= n; r += 32) cp_async4(rp + r, p.row_ptr + g0 + r);
-    }
     const float* bsrc = p.B + g0 * p.ldb + c0;
     if (bst && n > 0) {
-      if (VEC) {  // a-4: TMA bulk copies (the whole contiguous B_i in one, else one per row)
+      if (VEC) {  // a-4: TMA (the whole contiguous B_i: one 1-D bulk copy; a full k-tile:
+                  // popcount(n) 2-D tensor copies; a ragged last tile: one bulk copy per row)
         const uint32_t tx = (uint32_t)n * (uint32_t)kw * 4u;
-        if (lane == 0) mbar_expect_tx(&full[s], tx);
-        __syncwarp();
         if (kw == p.ldb) {
-          if (lane == 0) bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
+          if (lane == 0) {
+            mbar_expect_tx(&full[s], tx);
+            bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
+          }
+        } else if (p.tma2d && kw == p.kt) {
+          if (lane == 0) {
+            mbar_expect_tx(&full[s], tx);
+            int32_t r0 = 0;
+            while (n - r0 >= 512) {
+              tma_load_2d(st + (size_t)r0 * kw * 4, &maps.m[kTmaMaps - 1], c0, (int32_t)(g0 + r0), &full[s]);
+              r0 += 256;
+            }
+#pragma unroll
+            for (int b = kTmaMaps - 1; b >= 0; --b) {
+              if ((n - r0) & (1 << b)) {
+                tma_load_2d(st + (size_t)r0 * kw * 4, &maps.m[b], c0, (int32_t)(g0 + r0), &full[s]);
+                r0 += 1 << b;
+              }
+            }
+          }
         } else {
+          if (lane == 0) mbar_expect_tx(&full[s], tx);
+          __syncwarp();
           for (int r = lane; r < n; r += 32)
             bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
         }
@@ -184,6 +195,16 @@ __device__ __forceinline__ void produce(const SpmmParams& p, unsigned char* smem
           cp_async4(dst + q, bsrc + (int64_t)r * p.ldb + c);
         }
       }
+    }
+    // then the (small) CSR structure
+    if (sst) {
+      int32_t* pairs = reinterpret_cast<int32_t*>(st + p.stage_b);
+      for (int32_t e = lane; e < nnz; e += 32) {
+        cp_async4(pairs + 2 * e, p.col + nz0 + e);
+        cp_async4(pairs + 2 * e + 1, p.vals + nz0 + e);
+      }
+      int32_t* rp = pairs + 2 * nnz;
+      for (int32_t r = lane; r <= n; r += 32) cp_async4(rp + r, p.row_ptr + g0 + r);
     }
     if (lane == 0) {
       UnitHdr h;
@@ -338,7 +359,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
 }
 
 template <int CH, bool VEC>
-__global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p) {
+__global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
@@ -357,7 +378,7 @@ __global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p) {
   pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
-  if ((threadIdx.x >> 5) == 0) produce<VEC>(p, smem);
+  if ((threadIdx.x >> 5) == 0) produce<VEC>(p, maps, smem);
   else consume<CH, VEC>(p, smem);
   if (p.trace) {
     __syncthreads();
@@ -366,7 +387,7 @@ __global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p) {
 }
 
 template <int CH, bool VEC>
-static cudaError_t launch_t(const SpmmParams& sp, const bspmm_plan_t& plan, cudaStream_t s) {
+static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bspmm_plan_t& plan, cudaStream_t s) {
   auto kern = spmm_csr_kernel<CH, VEC>;
   static thread_local int configured_bytes[64] = {};  // per device
   int dev = 0;
@@ -386,7 +407,7 @@ static cudaError_t launch_t(const SpmmParams& sp, const bspmm_plan_t& plan, cuda
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, sp);
+  return cudaLaunchKernelEx(&cfg, kern, sp, maps);
 }
 
 cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s) {
@@ -411,17 +432,20 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.ldc = a.ldc;
   sp.trace = a.trace;
   sp.dbg = a.dbg;
+  sp.tma2d = a.maps != nullptr ? 1 : 0;
+  static const TmaMaps no_maps{};
+  const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
     switch (plan.chunks) {
-      case 1: return launch_t<1, true>(sp, plan, s);
-      case 2: return launch_t<2, true>(sp, plan, s);
-      default: return launch_t<4, true>(sp, plan, s);
+      case 1: return launch_t<1, true>(sp, maps, plan, s);
+      case 2: return launch_t<2, true>(sp, maps, plan, s);
+      default: return launch_t<4, true>(sp, maps, plan, s);
     }
   }
   switch (plan.chunks) {
-    case 1: return launch_t<1, false>(sp, plan, s);
-    case 2: return launch_t<2, false>(sp, plan, s);
-    default: return launch_t<4, false>(sp, plan, s);
+    case 1: return launch_t<1, false>(sp, maps, plan, s);
+    case 2: return launch_t<2, false>(sp, maps, plan, s);
+    default: return launch_t<4, false>(sp, maps, plan, s);
   }
 }
 
