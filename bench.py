@@ -198,6 +198,7 @@ def main():
     ap.add_argument("--kt", type=int, default=0)
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--chunks", type=int, default=0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -224,8 +225,8 @@ def main():
     k = b.k
     h = bs.Handle(dev)
     h.set_hints(int(b.sizes.max()) if b.batch else 0, int(b.nnz.max()) if b.batch else 0)
-    if args.kt or args.warps or args.ctas:
-        h.set_tuning(args.kt, args.warps, args.ctas)
+    if args.kt or args.warps or args.ctas or args.chunks:
+        h.set_tuning(args.kt, args.warps, args.ctas, args.chunks)
 
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     sizes, row_ptr, col, vals, B = T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)

@@ -83,7 +83,7 @@ typedef enum {
 typedef struct {
   int32_t kt;             /* k-tile width in columns (column cache blocking) */
   int32_t tiles;          /* p = ceil(k / kt) column blocks per matrix    */
-  int32_t lanes;          /* lanes per row: the sub-warp, see bspmm_subwarp  */
+  int32_t lanes;          /* lanes per row: subWarp rule on per-lane chunks  */
   int32_t vec;            /* 1: float4 lanes + TMA bulk staging; 0: scalar lanes + cp.async     */
   int32_t chunks;         /* float4 (vec) or float (scalar) column chunks per lane              */
   int32_t stages;         /* shared-memory ring depth per CTA                                   */
@@ -117,9 +117,10 @@ BSPMM_API bspmm_status_t bspmm_set_stream(bspmm_handle_t h, void* stream);
 BSPMM_API bspmm_status_t bspmm_set_hints(bspmm_handle_t h, int32_t max_rows, int64_t max_nnz);
 
 /* Tuning override for experiments: kt (multiple of 4 on the vec path, 0 =
- * auto), consumer warps per CTA (0 = auto), CTAs per SM (0 = auto). */
+ * auto), consumer warps per CTA (0 = auto, <= 15), CTAs per SM (0 = auto,
+ * <= 4), column chunks per lane (0 = auto, <= 4). */
 BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t consumer_warps,
-                                          int32_t ctas_per_sm);
+                                          int32_t ctas_per_sm, int32_t chunks);
 
 /* Debug: per-CTA phase timestamps (%globaltimer, ns) of subsequent SpMM
  * launches are written to dev_buf [grid x 16] uint64 (slots: entry, after the
@@ -130,7 +131,9 @@ BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t 
 BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
 
 /* Debug: timing-experiment bits for subsequent SpMM launches.  1 = compute but
- * do not store C (the result is then undefined).  0 (default) = normal. */
+ * do not store C (the result is then undefined); 2 = read B from global memory
+ * instead of staging it; 4 = read the CSR structure from global memory.
+ * 0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */
@@ -226,11 +229,12 @@ BSPMM_API int32_t bspmm_subwarp(int32_t n_B);
 
 /* The launch plan bspmm_csr would use for (k, batch, aligned) on a device
  * with `num_sms` SMs and `smem_per_cta` bytes of opt-in shared memory
- * (max_rows / max_nnz: hints, 0 = unknown; kt_override / warps / ctas_per_sm:
- * tuning, 0 = auto).  Pure host function. */
+ * (max_rows / max_nnz: hints, 0 = unknown; kt_override / warps / ctas_per_sm /
+ * chunks: tuning, 0 = auto).  Pure host function. */
 BSPMM_API bspmm_status_t bspmm_plan(int32_t k, int32_t batch, int32_t aligned, int32_t max_rows, int64_t max_nnz,
                                     int32_t num_sms, int32_t smem_per_cta, int32_t kt_override,
-                                    int32_t consumer_warps, int32_t ctas_per_sm, bspmm_plan_t* out);
+                                    int32_t consumer_warps, int32_t ctas_per_sm, int32_t chunks,
+                                    bspmm_plan_t* out);
 
 /* The plan used by the most recent bspmm_csr / bspmm_coo on this handle. */
 BSPMM_API bspmm_status_t bspmm_last_plan(bspmm_handle_t h, bspmm_plan_t* out);

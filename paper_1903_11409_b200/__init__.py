@@ -91,8 +91,8 @@ class Handle:
     def set_hints(self, max_rows: int = 0, max_nnz: int = 0):
         self._raise(lib.bspmm_set_hints(self._h, int(max_rows), int(max_nnz)), "bspmm_set_hints")
 
-    def set_tuning(self, kt: int = 0, consumer_warps: int = 0, ctas_per_sm: int = 0):
-        self._raise(lib.bspmm_set_tuning(self._h, int(kt), int(consumer_warps), int(ctas_per_sm)),
+    def set_tuning(self, kt: int = 0, consumer_warps: int = 0, ctas_per_sm: int = 0, chunks: int = 0):
+        self._raise(lib.bspmm_set_tuning(self._h, int(kt), int(consumer_warps), int(ctas_per_sm), int(chunks)),
                     "bspmm_set_tuning")
 
     def set_trace(self, buf: Optional[torch.Tensor]):
@@ -252,11 +252,13 @@ def subwarp(n_B: int) -> int:
 
 
 def plan(k: int, batch: int, aligned: bool = True, max_rows: int = 0, max_nnz: int = 0, num_sms: int = 148,
-         smem_per_cta: int = 232448, kt: int = 0, consumer_warps: int = 0, ctas_per_sm: int = 0) -> dict:
+         smem_per_cta: int = 232448, kt: int = 0, consumer_warps: int = 0, ctas_per_sm: int = 0,
+         chunks: int = 0) -> dict:
     """The launch plan bspmm_csr would use (pure host)."""
     p = Plan()
     st = lib.bspmm_plan(int(k), int(batch), int(bool(aligned)), int(max_rows), int(max_nnz), int(num_sms),
-                        int(smem_per_cta), int(kt), int(consumer_warps), int(ctas_per_sm), ctypes.byref(p))
+                        int(smem_per_cta), int(kt), int(consumer_warps), int(ctas_per_sm), int(chunks),
+                        ctypes.byref(p))
     if st != _lib.SUCCESS:
         raise BspmmError(st, "bspmm_plan")
     return p.as_dict()

@@ -30,7 +30,7 @@ _SIGS = {
     "bspmm_destroy": (I32, [P]),
     "bspmm_set_stream": (I32, [P, P]),
     "bspmm_set_hints": (I32, [P, I32, I64]),
-    "bspmm_set_tuning": (I32, [P, I32, I32, I32]),
+    "bspmm_set_tuning": (I32, [P, I32, I32, I32, I32]),
     "bspmm_sync": (I32, [P]),
     "bspmm_set_trace": (I32, [P, P]),
     "bspmm_set_debug": (I32, [P, I32]),
@@ -41,7 +41,7 @@ _SIGS = {
     "bspmm_csr_host": (I32, [P, I32, I32, P, P, P, P, P, P, I64, I64]),
     "bspmm_partition": (I32, [I32, P, I32, I32, P]),
     "bspmm_subwarp": (I32, [I32]),
-    "bspmm_plan": (I32, [I32, I32, I32, I32, I64, I32, I32, I32, I32, I32, ctypes.POINTER(Plan)]),
+    "bspmm_plan": (I32, [I32, I32, I32, I32, I64, I32, I32, I32, I32, I32, I32, ctypes.POINTER(Plan)]),
     "bspmm_last_plan": (I32, [P, ctypes.POINTER(Plan)]),
     "bspmm_launch_count": (I64, [P]),
     "bspmm_status_string": (ctypes.c_char_p, [I32]),

@@ -145,7 +145,7 @@ const TmaMaps* tma_maps(bspmm_handle_t h, const float* B, int32_t k, int64_t ldb
 
 bspmm_status_t plan_for(bspmm_handle_t h, int32_t batch, int32_t k, bool aligned, bspmm_plan_t* plan) {
   bspmm_status_t st = make_plan(k, batch, aligned, h->hint_rows, h->hint_nnz, h->num_sms, h->smem_optin,
-                                h->tune_kt, h->tune_warps, h->tune_ctas, plan);
+                                h->tune_kt, h->tune_warps, h->tune_ctas, h->tune_chunks, plan);
   if (st != BSPMM_SUCCESS) return fail(h, st, "planner rejected the arguments");
   h->last_plan = *plan;
   return BSPMM_SUCCESS;
@@ -231,11 +231,14 @@ BSPMM_API bspmm_status_t bspmm_set_hints(bspmm_handle_t h, int32_t max_rows, int
   return BSPMM_SUCCESS;
 }
 
-BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t warps, int32_t ctas_per_sm) {
-  if (!h || kt < 0 || warps < 0 || warps > 16 || ctas_per_sm < 0 || ctas_per_sm > 4) return BSPMM_ERROR_INVALID_VALUE;
+BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t warps, int32_t ctas_per_sm,
+                                          int32_t chunks) {
+  if (!h || kt < 0 || warps < 0 || warps > 15 || ctas_per_sm < 0 || ctas_per_sm > 4 || chunks < 0 || chunks > 4)
+    return BSPMM_ERROR_INVALID_VALUE;
   h->tune_kt = kt;
   h->tune_warps = warps;
   h->tune_ctas = ctas_per_sm;
+  h->tune_chunks = chunks;
   return BSPMM_SUCCESS;
 }
 
@@ -246,7 +249,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 1) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 7) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }

@@ -18,7 +18,8 @@ namespace bspmm {
 constexpr int kMaxStages = 8;
 constexpr int kHdrBytes = 32;       // per-stage unit header
 constexpr int kDefaultRows = 64;    // planning assumption when no max_rows hint
-constexpr int kDefaultWarps = 16;   // consumer warps per CTA (C5 sweep: 16 > 8 by 5%)
+constexpr int kDefaultWarps = 15;   // consumer warps per CTA (512-thread CTA; C5 sweep: 16 > 8 by 5%)
+constexpr int kDefaultChunks = 4;   // column chunks per lane (fewer lanes per row, more rows per warp)
 constexpr int kMaxVecKt = 512;      // 4 float4 chunks x 32 lanes
 constexpr int kMaxScalarKt = 128;   // 4 float chunks x 32 lanes
 constexpr int kCooSmemCap = 2048;   // default COO entries sorted in shared memory
@@ -37,7 +38,7 @@ BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stag
 // planner (plan.cpp)
 bspmm_status_t make_plan(int32_t k, int32_t batch, bool aligned, int32_t max_rows, int64_t max_nnz,
                          int32_t num_sms, int32_t smem_per_cta, int32_t kt_override, int32_t warps,
-                         int32_t ctas_per_sm, bspmm_plan_t* out);
+                         int32_t ctas_per_sm, int32_t chunks_pref, bspmm_plan_t* out);
 
 // 2-D TMA descriptors over B [rows x k] (row pitch ldb) with box {kt, 2^b rows},
 // b = 0..8: a unit of n_i rows is staged with popcount(n_i) tensor copies
@@ -96,7 +97,7 @@ struct bspmm_handle_s {
   int smem_optin = 232448;
   int32_t hint_rows = 0;
   int64_t hint_nnz = 0;
-  int32_t tune_kt = 0, tune_warps = 0, tune_ctas = 0;
+  int32_t tune_kt = 0, tune_warps = 0, tune_ctas = 0, tune_chunks = 0;
   bspmm_plan_t last_plan{};
   unsigned long long* trace = nullptr;  // debug: per-CTA phase timestamps
   int32_t dbg = 0;                      // debug bits: 1 = skip C stores

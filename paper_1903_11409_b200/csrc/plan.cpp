@@ -9,7 +9,7 @@
 //    2 units per SM (the paper's "batch 50 fails to fill the SMs", :377) or a
 //    two-stage shared-memory ring of n_max x kt tiles does not fit;
 //  * lanes per row = the paper's subWarp rule (:150-155) applied to the
-//    tile's float4 columns (vec) or columns (scalar);
+//    tile's columns in per-lane chunks (float4 chunks on the vec path);
 //  * persistent grid = min(units, SMs x CTAs/SM); each CTA walks units
 //    blockIdx.x, +grid, ... through an S-stage TMA ring.
 #include <algorithm>
@@ -24,21 +24,14 @@ extern "C" BSPMM_API int32_t bspmm_subwarp(int32_t n_B) {
 
 namespace bspmm {
 
-static int32_t lanes_for(int32_t kt, bool vec) {
-  return bspmm_subwarp(vec ? (kt + 3) / 4 : kt);
-}
-
 bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, int64_t max_nnz,
                          int32_t num_sms, int32_t smem_per_cta, int32_t kt_override, int32_t warps,
-                         int32_t ctas_per_sm, bspmm_plan_t* out) {
+                         int32_t ctas_per_sm, int32_t chunks_pref, bspmm_plan_t* out) {
   if (!out || k < 1 || batch < 0 || num_sms < 1 || smem_per_cta < 1024) return BSPMM_ERROR_INVALID_VALUE;
   bspmm_plan_t p{};
   const int32_t R = max_rows > 0 ? max_rows : kDefaultRows;
   const int64_t Z = max_nnz > 0 ? max_nnz : 8LL * R;
-  const int32_t ctas = ctas_per_sm > 0 ? ctas_per_sm : 1;
-  const int32_t W = warps > 0 ? std::min(warps, 16) : kDefaultWarps;
-  // per-CTA shared-memory budget (B200: 228 KB per SM, 227 KB opt-in per CTA; 1 KB reserved per CTA)
-  const int32_t budget = std::min(smem_per_cta, (233472 / ctas) - 1024);
+  const int32_t W = warps > 0 ? std::min(warps, 15) : kDefaultWarps;
   const int32_t kmax = vec ? kMaxVecKt : kMaxScalarKt;
   const int32_t quantum = vec ? 4 : 1;
 
@@ -48,22 +41,35 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
     if (vec) kt = align_up(kt, 4);
     kt = std::min(kt, align_up(k, quantum));
   } else {
+    // column blocking only while the batch leaves SMs idle AND the units are
+    // big: many small units cost more (per-unit TMA + metadata) than idle SMs
+    // (measured, tools/kbench.py sweeps)
     kt = std::min(align_up(k, quantum), kmax);
-    const int64_t target_units = 2LL * num_sms;
-    while ((int64_t)batch * ceil_div(k, kt) < target_units && kt > 32) kt = align_up(kt / 2, quantum);
+    while ((int64_t)batch * ceil_div(k, kt) < num_sms && (int64_t)R * kt * 4 > 32768 && kt > 32)
+      kt = align_up(kt / 2, quantum);
   }
+  // CTAs per SM: two for small batches (more TMA issue and latency hiding per SM)
+  int32_t ctas = ctas_per_sm > 0 ? ctas_per_sm : 0;
+  // per-CTA shared-memory budget (B200: 228 KB per SM, 227 KB opt-in per CTA; 1 KB reserved per CTA)
+  auto budget_for = [&](int32_t c) { return std::min(smem_per_cta, (233472 / c) - 1024); };
   // structure capacity: (col, val) pairs + row pointer
   // (stage regions are 128-byte aligned: 2-D TMA destinations)
   int64_t s_bytes64 = align_up(align_up(8 * (int32_t)std::min<int64_t>(Z, 1 << 20), 16) + align_up(4 * (R + 1), 16), 128);
-  auto stages_for = [&](int32_t kt_) {
+  auto stages_in = [&](int32_t kt_, int32_t budget_) {
     int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 128);
     int64_t per = b + s_bytes64;
     int64_t s = 0;
-    while (s < kMaxStages && ring_prefix_bytes((int32_t)(s + 1)) + (s + 1) * per <= budget) ++s;
+    while (s < kMaxStages && ring_prefix_bytes((int32_t)(s + 1)) + (s + 1) * per <= budget_) ++s;
     return (int32_t)s;
   };
   if (kt_override <= 0)
-    while (stages_for(kt) < 2 && kt > quantum * 8) kt = align_up(kt / 2, quantum);
+    while (stages_in(kt, budget_for(1)) < 2 && kt > quantum * 8) kt = align_up(kt / 2, quantum);
+  if (ctas == 0) {
+    const int64_t units_ = (int64_t)batch * ceil_div(k, kt);
+    ctas = (units_ <= 16LL * num_sms && stages_in(kt, budget_for(2)) >= 1) ? 2 : 1;
+  }
+  const int32_t budget = budget_for(ctas);
+  auto stages_for = [&](int32_t kt_) { return stages_in(kt_, budget); };
 
   int32_t stages = stages_for(kt);
   int32_t b_bytes = align_up(std::max<int32_t>(16, R * kt * 4), 128);
@@ -77,8 +83,12 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   p.kt = kt;
   p.tiles = (int32_t)ceil_div(k, kt);
   p.vec = vec ? 1 : 0;
-  p.lanes = lanes_for(kt, vec);
+  // lanes per row: the paper's subWarp rule applied to the
+  // tile's columns grouped in chunks of `pref` per lane (float4 chunks on the
+  // vec path): one warp covers 32 / lanes rows per instruction
   const int32_t cols = vec ? (kt + 3) / 4 : kt;
+  const int32_t pref = chunks_pref > 0 ? std::min(chunks_pref, 4) : kDefaultChunks;
+  p.lanes = bspmm_subwarp((int32_t)ceil_div(cols, pref));
   const int32_t ch = (int32_t)ceil_div(cols, p.lanes);
   p.chunks = ch <= 1 ? 1 : (ch <= 2 ? 2 : 4);
   p.stages = stages;
@@ -98,7 +108,7 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
 extern "C" BSPMM_API bspmm_status_t bspmm_plan(int32_t k, int32_t batch, int32_t aligned, int32_t max_rows,
                                                int64_t max_nnz, int32_t num_sms, int32_t smem_per_cta,
                                                int32_t kt_override, int32_t consumer_warps,
-                                               int32_t ctas_per_sm, bspmm_plan_t* out) {
+                                               int32_t ctas_per_sm, int32_t chunks, bspmm_plan_t* out) {
   return bspmm::make_plan(k, batch, aligned != 0, max_rows, max_nnz, num_sms, smem_per_cta, kt_override,
-                          consumer_warps, ctas_per_sm, out);
+                          consumer_warps, ctas_per_sm, chunks, out);
 }

@@ -46,7 +46,7 @@ struct SpmmParams {
   float* __restrict__ C;
   int64_t ldc;
   unsigned long long* trace;  // debug: per-CTA phase timestamps (globaltimer ns), or null
-  int32_t dbg;                // debug bits: 1 = skip C stores (timing experiments only)
+  int32_t dbg;                // debug bits: 1 skip C stores, 2 B direct, 4 structure direct (experiments)
   int32_t tma2d;              // 1: full k-tiles staged with 2-D tensor TMA (maps valid)
 };
 
@@ -153,8 +153,9 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
     const uint32_t phase = (uint32_t)(j / p.stages) & 1u;
     mbar_wait(&empty[s], phase ^ 1u);
     unsigned char* st = ring + (size_t)s * stage_bytes;
-    const bool bst = (int64_t)n * kw * 4 <= p.stage_b;
-    const bool sst = 8LL * nnz + 4LL * (n + 1) <= p.stage_s;
+    // a unit is staged whole (tile + structure) or not at all (read from global memory)
+    const bool bst = (int64_t)n * kw * 4 <= p.stage_b && 8LL * nnz + 4LL * (n + 1) <= p.stage_s && !(p.dbg & 2);
+    const bool sst = bst;
     const float* bsrc = p.B + g0 * p.ldb + c0;
     if (bst && n > 0) {
       if (VEC) {  // a-4: TMA (the whole contiguous B_i: one 1-D bulk copy; a full k-tile:
@@ -219,32 +220,31 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
 }
 
 // a-5/a-6 for one unit: a sub-warp of L lanes owns a row; each lane owns CH
-// column chunks (float4 when VEC).  Up to G entries of a row are loaded ahead
-// (independent shared-memory loads), then accumulated strictly in storage
-// order, so the result is bitwise the fp32 storage-order FMA sum (O3').
+// column chunks (float4 when VEC) at lane-strided positions li + v*L (the
+// paper's j = lane, lane + subWarp, ..., in 128-bit chunks).  Up
+// to G entries of a row are loaded ahead (independent shared-memory loads),
+// then accumulated strictly in storage order, so the result is bitwise the
+// fp32 storage-order FMA sum (O3').  Per-unit address math is hoisted; the
+// row loop touches shared memory with 32-bit offsets only.
 template <int CH, bool VEC, bool BST, bool SST>
 __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
                                      int step, int li) {
-  constexpr int G = CH >= 4 ? 2 : 4;
+  constexpr int G = CH >= 2 ? 2 : 4;
+  constexpr int FW = VEC ? 4 : 1;  // floats per chunk
   const int L = p.lanes;
-  const int32_t cols = VEC ? (h.kw >> 2) : h.kw;  // chunks of 4 (VEC) or 1 column
-  const int32_t* rp;
-  const int2* pr = nullptr;
-  const float* Bbase;
-  int64_t bstride;  // floats between consecutive B rows
-  if (SST) {
-    pr = reinterpret_cast<const int2*>(st + p.stage_b);
-    rp = reinterpret_cast<const int32_t*>(st + p.stage_b) + 2 * h.nnz;
-  } else {
-    rp = p.row_ptr + h.g0;
-  }
-  if (BST) {
-    Bbase = reinterpret_cast<const float*>(st);
-    bstride = h.kw;
-  } else {
-    Bbase = p.B + h.g0 * p.ldb + h.c0;
-    bstride = p.ldb;
-  }
+  const int32_t cols = VEC ? (h.kw >> 2) : h.kw;
+  bool ok[CH];
+#pragma unroll
+  for (int v = 0; v < CH; ++v) ok[v] = li + v * L < cols;
+  // row pointers and (col, val) pairs, indexed by ABSOLUTE entry position
+  const int32_t* rp = SST ? reinterpret_cast<const int32_t*>(st + p.stage_b) + 2 * h.nnz : p.row_ptr + h.g0;
+  const int2* pr = SST ? reinterpret_cast<const int2*>(st + p.stage_b) - h.nz0 : nullptr;
+  const float* col_v = p.vals;
+  const int32_t* col_i = p.col;
+  // B rows of the tile (lane offset folded in) and C rows
+  const float* Bt = BST ? reinterpret_cast<const float*>(st) + FW * li : p.B + h.g0 * p.ldb + h.c0 + FW * li;
+  const int64_t bstride = BST ? (int64_t)h.kw : p.ldb;
+  float* Ct = p.C + h.g0 * p.ldc + h.c0 + FW * li;
   int r = first;
   int32_t nx0 = 0, nx1 = 0;
   if (r < h.n) {
@@ -252,7 +252,7 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
     nx1 = rp[r + 1];
   }
   for (; r < h.n; r += step) {
-    const int32_t e0 = nx0 - h.nz0, e1 = nx1 - h.nz0;
+    const int32_t e0 = nx0, e1 = nx1;
     if (r + step < h.n) {  // next row's range, loaded ahead
       nx0 = rp[r + step];
       nx1 = rp[r + step + 1];
@@ -266,30 +266,28 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
       float a[G];
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        cidx[q] = 0;
-        a[q] = 0.f;
         if (q < cnt) {
           if (SST) {
             const int2 cv = pr[e + q];
             cidx[q] = cv.x;
             a[q] = __int_as_float(cv.y);
           } else {
-            cidx[q] = __ldg(p.col + h.nz0 + e + q);
-            a[q] = __ldg(p.vals + h.nz0 + e + q);
+            cidx[q] = __ldg(col_i + e + q);
+            a[q] = __ldg(col_v + e + q);
           }
         }
       }
       float4 b[G][CH];
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        const float* brow = Bbase + (int64_t)cidx[q] * bstride;
+        if (q < cnt) {
+          const float* brow = BST ? Bt + (int32_t)(cidx[q] * (int32_t)bstride) : Bt + (int64_t)cidx[q] * bstride;
 #pragma unroll
-        for (int v = 0; v < CH; ++v) {
-          const int c = li + v * L;
-          b[q][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (q < cnt && c < cols) {
-            if (VEC) b[q][v] = BST ? reinterpret_cast<const float4*>(brow)[c] : ldg_nc_f4(brow + 4 * c);
-            else b[q][v].x = BST ? brow[c] : __ldg(brow + c);
+          for (int v = 0; v < CH; ++v) {
+            if (ok[v]) {
+              if (VEC) b[q][v] = BST ? *reinterpret_cast<const float4*>(brow + FW * v * L) : ldg_nc_f4(brow + FW * v * L);
+              else b[q][v].x = BST ? brow[v * L] : __ldg(brow + v * L);
+            }
           }
         }
       }
@@ -308,17 +306,62 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
         }
       }
     }
-    float* crow = p.C + (h.g0 + r) * p.ldc + h.c0;
+    float* crow = Ct + (int64_t)r * p.ldc;
     if (p.dbg & 1) {
       if (acc[0].x == 1.2345e-38f) crow[0] = 0.f;  // keep the math alive, store nothing
       continue;
     }
 #pragma unroll
     for (int v = 0; v < CH; ++v) {
-      const int c = li + v * L;
-      if (c < cols) {
-        if (VEC) stg_cs_f4(crow + 4 * c, acc[v]);
-        else stg_cs_f1(crow + c, acc[v].x);
+      if (ok[v]) {
+        if (VEC) stg_cs_f4(crow + FW * v * L, acc[v]);
+        else stg_cs_f1(crow + v * L, acc[v].x);
+      }
+    }
+  }
+}
+
+// units that did not fit a stage (the paper's case 3): the
+// same storage-order sum read straight from global memory (L1/L2-cached B
+// gathers), a plain loop to keep the register allocation of the staged path
+template <int CH, bool VEC>
+__device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& h, int first, int step, int li) {
+  constexpr int FW = VEC ? 4 : 1;
+  const int L = p.lanes;
+  const int32_t cols = VEC ? (h.kw >> 2) : h.kw;
+  const int32_t* rp = p.row_ptr + h.g0;
+  const float* Bt = p.B + h.g0 * p.ldb + h.c0 + FW * li;
+  float* Ct = p.C + h.g0 * p.ldc + h.c0 + FW * li;
+  for (int r = first; r < h.n; r += step) {
+    const int32_t e0 = __ldg(rp + r), e1 = __ldg(rp + r + 1);
+    float4 acc[CH];
+#pragma unroll
+    for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t e = e0; e < e1; ++e) {
+      const int32_t c = __ldg(p.col + e);
+      const float a = __ldg(p.vals + e);
+      const float* brow = Bt + (int64_t)c * p.ldb;
+#pragma unroll
+      for (int v = 0; v < CH; ++v) {
+        if (li + v * L < cols) {
+          if (VEC) {
+            const float4 b = ldg_nc_f4(brow + FW * v * L);
+            acc[v].x = fmaf(a, b.x, acc[v].x);
+            acc[v].y = fmaf(a, b.y, acc[v].y);
+            acc[v].z = fmaf(a, b.z, acc[v].z);
+            acc[v].w = fmaf(a, b.w, acc[v].w);
+          } else {
+            acc[v].x = fmaf(a, __ldg(brow + v * L), acc[v].x);
+          }
+        }
+      }
+    }
+    float* crow = Ct + (int64_t)r * p.ldc;
+#pragma unroll
+    for (int v = 0; v < CH; ++v) {
+      if (li + v * L < cols) {
+        if (VEC) stg_cs_f4(crow + FW * v * L, acc[v]);
+        else stg_cs_f1(crow + v * L, acc[v].x);
       }
     }
   }
@@ -345,12 +388,8 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
     const UnitHdr h = hdr[s];
     const unsigned char* st = ring + (size_t)s * stage_bytes;
-    switch (h.flags) {
-      case 3: rows<CH, VEC, true, true>(p, h, st, first, step, li); break;
-      case 1: rows<CH, VEC, true, false>(p, h, st, first, step, li); break;
-      case 2: rows<CH, VEC, false, true>(p, h, st, first, step, li); break;
-      default: rows<CH, VEC, false, false>(p, h, st, first, step, li); break;
-    }
+    if (h.flags == 3) rows<CH, VEC, true, true>(p, h, st, first, step, li);  // the hot, staged case
+    else rows_direct<CH, VEC>(p, h, first, step, li);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 8);
@@ -359,7 +398,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
 }
 
 template <int CH, bool VEC>
-__global__ void __launch_bounds__(544) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(512, 1) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;

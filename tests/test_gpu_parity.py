@@ -155,12 +155,13 @@ def test_tuning_space_bitwise(h):
     b = synth.config(4)
     ref = run_csr(h, b)
     for kt in (32, 64, 128, 256, 512):
-        for warps in (1, 4, 8, 16):
+        for warps in (1, 4, 15):
             for ctas in (1, 2):
-                h.set_tuning(kt, warps, ctas)
-                C = run_csr(h, b)
-                assert np.array_equal(C.view(np.uint32), ref.view(np.uint32)), (kt, warps, ctas)
-    h.set_tuning(0, 0, 0)
+                for chunks in (1, 2, 4):
+                    h.set_tuning(kt, warps, ctas, chunks)
+                    C = run_csr(h, b)
+                    assert np.array_equal(C.view(np.uint32), ref.view(np.uint32)), (kt, warps, ctas, chunks)
+    h.set_tuning(0, 0, 0, 0)
 
 
 def test_deterministic_repeat(h):

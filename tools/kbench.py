@@ -87,7 +87,9 @@ def main():
     ap.add_argument("--kts", default="0,32,64,128,256,512")
     ap.add_argument("--warps", default="0,4,8,12,16")
     ap.add_argument("--ctas", default="0,1,2")
+    ap.add_argument("--chunks", default="0")
     ap.add_argument("--ncu-mode", action="store_true", help="plain launches only (for ncu)")
+    ap.add_argument("--dbg", default="0", help="comma list of debug bit sets to sweep (bspmm_set_debug)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -105,15 +107,18 @@ def main():
             del reps
             torch.cuda.empty_cache()
             continue
-        combos = [(0, 0, 0)]
+        combos = [(0, 0, 0, 0)]
         if args.sweep:
             combos = list(itertools.product([int(x) for x in args.kts.split(",")],
                                             [int(x) for x in args.warps.split(",")],
-                                            [int(x) for x in args.ctas.split(",")]))
-        for kt, w, c in combos:
+                                            [int(x) for x in args.ctas.split(",")],
+                                            [int(x) for x in args.chunks.split(",")]))
+        combos = [(kt, w, c, ch, d) for kt, w, c, ch in combos for d in [int(x) for x in args.dbg.split(",")]]
+        for kt, w, c, ch, dbg in combos:
             if kt and kt > b.k:
                 continue
-            h.set_tuning(kt, w, c)
+            h.set_tuning(kt, w, c, ch)
+            h.set_debug(dbg)
             try:
                 ms = time_calls(h, reps, R, spmm_only)
             except Exception as e:  # noqa: BLE001
@@ -121,10 +126,11 @@ def main():
                 continue
             plan = h.last_plan()
             gbs = per / (ms / 1e3) / 1e9
-            print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "us": ms * 1e3, "GBs": gbs,
+            print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "chunks": ch, "dbg": dbg, "us": ms * 1e3, "GBs": gbs,
                               "frac": gbs / peak, "GFLOPs": 2 * b.n_nnz * b.k / (ms / 1e3) / 1e9,
                               "replicas": len(reps), "plan": plan}), flush=True)
         h.set_tuning(0, 0, 0)
+        h.set_debug(0)
         ms_step = time_calls(h, reps, R, full_step)
         ms_off = time_calls(h, reps, R, offsets_only)
         ms_ng = time_calls(h, reps, min(R, 50), spmm_only, graph=False)

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--kt", type=int, default=0)
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--nostore", action="store_true")
     args = ap.parse_args()
@@ -35,7 +36,7 @@ def main():
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     h = bs.Handle(0)
     h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
-    h.set_tuning(args.kt, args.warps, args.ctas)
+    h.set_tuning(args.kt, args.warps, args.ctas, args.chunks)
     ro, rp, col, vals, B = T(b.row_off), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)
     C = torch.empty((b.n_rows, b.k), device=dev)
     h.csr(ro, None, rp, col, vals, B, C)
