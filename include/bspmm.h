@@ -117,7 +117,7 @@ BSPMM_API bspmm_status_t bspmm_set_stream(bspmm_handle_t h, void* stream);
 BSPMM_API bspmm_status_t bspmm_set_hints(bspmm_handle_t h, int32_t max_rows, int64_t max_nnz);
 
 /* Tuning override for experiments: kt (multiple of 4 on the vec path, 0 =
- * auto), consumer warps per CTA (0 = auto, <= 15), CTAs per SM (0 = auto,
+ * auto), consumer warps per CTA (0 = auto, <= 16; 15 with 4 chunks), CTAs per SM (0 = auto,
  * <= 4), column chunks per lane (0 = auto, <= 4). */
 BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t consumer_warps,
                                           int32_t ctas_per_sm, int32_t chunks);

@@ -233,7 +233,7 @@ BSPMM_API bspmm_status_t bspmm_set_hints(bspmm_handle_t h, int32_t max_rows, int
 
 BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t warps, int32_t ctas_per_sm,
                                           int32_t chunks) {
-  if (!h || kt < 0 || warps < 0 || warps > 15 || ctas_per_sm < 0 || ctas_per_sm > 4 || chunks < 0 || chunks > 4)
+  if (!h || kt < 0 || warps < 0 || warps > 16 || ctas_per_sm < 0 || ctas_per_sm > 4 || chunks < 0 || chunks > 4)
     return BSPMM_ERROR_INVALID_VALUE;
   h->tune_kt = kt;
   h->tune_warps = warps;

@@ -18,8 +18,7 @@ namespace bspmm {
 constexpr int kMaxStages = 8;
 constexpr int kHdrBytes = 32;       // per-stage unit header
 constexpr int kDefaultRows = 64;    // planning assumption when no max_rows hint
-constexpr int kDefaultWarps = 15;   // consumer warps per CTA (512-thread CTA; C5 sweep: 16 > 8 by 5%)
-constexpr int kDefaultChunks = 4;   // column chunks per lane (fewer lanes per row, more rows per warp)
+constexpr int kDefaultChunks = 2;   // column chunks per lane (fewer lanes per row, more rows per warp)
 constexpr int kMaxVecKt = 512;      // 4 float4 chunks x 32 lanes
 constexpr int kMaxScalarKt = 128;   // 4 float chunks x 32 lanes
 constexpr int kCooSmemCap = 2048;   // default COO entries sorted in shared memory

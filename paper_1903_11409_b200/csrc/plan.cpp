@@ -31,7 +31,6 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   bspmm_plan_t p{};
   const int32_t R = max_rows > 0 ? max_rows : kDefaultRows;
   const int64_t Z = max_nnz > 0 ? max_nnz : 8LL * R;
-  const int32_t W = warps > 0 ? std::min(warps, 15) : kDefaultWarps;
   const int32_t kmax = vec ? kMaxVecKt : kMaxScalarKt;
   const int32_t quantum = vec ? 4 : 1;
 
@@ -45,11 +44,12 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
     // big: many small units cost more (per-unit TMA + metadata) than idle SMs
     // (measured, tools/kbench.py sweeps)
     kt = std::min(align_up(k, quantum), kmax);
-    while ((int64_t)batch * ceil_div(k, kt) < num_sms && (int64_t)R * kt * 4 > 32768 && kt > 32)
+    while ((int64_t)batch * ceil_div(k, kt) < 2LL * num_sms && (int64_t)R * kt * 4 > 32768 && kt > 32)
       kt = align_up(kt / 2, quantum);
   }
-  // CTAs per SM: two for small batches (more TMA issue and latency hiding per SM)
-  int32_t ctas = ctas_per_sm > 0 ? ctas_per_sm : 0;
+  // CTAs per SM: one by default (sweeps: 2 never won once the consumers cover
+  // several rows per warp); the knob stays for experiments
+  int32_t ctas = ctas_per_sm > 0 ? ctas_per_sm : 1;
   // per-CTA shared-memory budget (B200: 228 KB per SM, 227 KB opt-in per CTA; 1 KB reserved per CTA)
   auto budget_for = [&](int32_t c) { return std::min(smem_per_cta, (233472 / c) - 1024); };
   // structure capacity: (col, val) pairs + row pointer
@@ -64,10 +64,6 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   };
   if (kt_override <= 0)
     while (stages_in(kt, budget_for(1)) < 2 && kt > quantum * 8) kt = align_up(kt / 2, quantum);
-  if (ctas == 0) {
-    const int64_t units_ = (int64_t)batch * ceil_div(k, kt);
-    ctas = (units_ <= 16LL * num_sms && stages_in(kt, budget_for(2)) >= 1) ? 2 : 1;
-  }
   const int32_t budget = budget_for(ctas);
   auto stages_for = [&](int32_t kt_) { return stages_in(kt_, budget); };
 
@@ -91,6 +87,9 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   p.lanes = bspmm_subwarp((int32_t)ceil_div(cols, pref));
   const int32_t ch = (int32_t)ceil_div(cols, p.lanes);
   p.chunks = ch <= 1 ? 1 : (ch <= 2 ? 2 : 4);
+  // consumer warps: 16 (544-thread CTA) up to 2 chunks per lane, 15 with 4
+  const int32_t wmax = p.chunks >= 4 ? 15 : 16;
+  const int32_t W = warps > 0 ? std::min(warps, wmax) : wmax;
   p.stages = stages;
   p.stage_b_bytes = b_bytes;
   p.stage_s_bytes = s_bytes;

@@ -65,6 +65,10 @@ __device__ __forceinline__ unsigned long long gtime() {
     if (p.trace) p.trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = gtime(); \
   } while (0)
 
+// CTA size cap per chunk count: 16 consumer warps fit the register budget with
+// up to 2 chunks per lane; 4 chunks need ~128 registers -> 15 consumer warps
+constexpr int kMaxThreads(int ch) { return ch >= 4 ? 512 : 544; }
+
 struct __align__(16) UnitHdr {
   int64_t g0;     // first global row of the matrix
   int32_t n;      // rows (n_i)
@@ -398,7 +402,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
 }
 
 template <int CH, bool VEC>
-__global__ void __launch_bounds__(512, 1) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(kMaxThreads(CH), 1) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;

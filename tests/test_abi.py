@@ -104,13 +104,14 @@ def test_plan_invariants(k, batch):
             assert p["tiles"] == -(-k // p["kt"])                            # tiles cover [0, k)
             assert p["kt"] * (p["tiles"] - 1) < k <= p["kt"] * p["tiles"]    # disjoint, no empty tile
             cols = -(-p["kt"] // 4) if p["vec"] else p["kt"]
-            assert p["lanes"] == bs.subwarp(-(-cols // 4))                   # PAPER.md:150-155 on 4-chunks
+            assert p["lanes"] == bs.subwarp(-(-cols // 2))                   # PAPER.md:150-155 on 2-chunks
             assert p["lanes"] * p["chunks"] >= cols and p["chunks"] in (1, 2, 4)
             p1 = bs.plan(k, batch, aligned=aligned, max_rows=rows, chunks=1)
             assert p1["lanes"] == bs.subwarp(cols)                           # the paper's rule, 1 chunk/lane
             assert p["smem_bytes"] <= 232448 and p["stages"] >= 1
             assert p["units"] == batch * p["tiles"]
-            assert 1 <= p["grid"] <= min(p["units"], 148 * 2)
+            assert 1 <= p["grid"] <= min(p["units"], 148)
+            assert p["threads"] == 32 * (1 + (15 if p["chunks"] == 4 else 16))
             if aligned:
                 assert p["kt"] % 4 == 0
             if rows and rows * p["kt"] * 4 <= 100000:
@@ -120,7 +121,7 @@ def test_plan_invariants(k, batch):
 def test_plan_paper_shapes():
     # C4 (PAPER.md:366 shape): 100 matrices cannot fill 148 SMs whole -> column blocking (p > 1)
     p = bs.plan(512, 100, max_rows=50)
-    assert p["tiles"] > 1 and p["units"] >= 148
+    assert p["tiles"] > 1 and p["units"] >= 2 * 148
     # C5: whole rows, one unit per matrix
     p = bs.plan(256, 65536, max_rows=60)
     assert p["tiles"] == 1 and p["stages"] >= 2

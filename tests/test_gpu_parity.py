@@ -155,7 +155,7 @@ def test_tuning_space_bitwise(h):
     b = synth.config(4)
     ref = run_csr(h, b)
     for kt in (32, 64, 128, 256, 512):
-        for warps in (1, 4, 15):
+        for warps in (1, 4, 16):
             for ctas in (1, 2):
                 for chunks in (1, 2, 4):
                     h.set_tuning(kt, warps, ctas, chunks)
