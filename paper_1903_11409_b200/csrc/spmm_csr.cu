@@ -233,7 +233,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
 template <int CH, bool VEC, bool BST, bool SST>
 __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
                                      int step, int li) {
-  constexpr int G = CH >= 2 ? 2 : 4;
+  constexpr int G = CH >= 4 ? 2 : 4;
   constexpr int FW = VEC ? 4 : 1;  // floats per chunk
   const int L = p.lanes;
   const int32_t cols = VEC ? (h.kw >> 2) : h.kw;
