@@ -54,7 +54,9 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   auto budget_for = [&](int32_t c) { return std::min(smem_per_cta, (233472 / c) - 1024); };
   // structure capacity: (col, val) pairs + row pointer
   // (stage regions are 128-byte aligned: 2-D TMA destinations)
-  int64_t s_bytes64 = align_up(align_up(8 * (int32_t)std::min<int64_t>(Z, 1 << 20), 16) + align_up(4 * (R + 1), 16), 128);
+  // CSR slice: col, vals, row pointers, each 16 + 4*count bytes rounded to 16 (spmm_csr.cu slice_bytes)
+  const int64_t Zc = std::min<int64_t>(Z, 1 << 20);
+  int64_t s_bytes64 = align_up((int32_t)(2 * ((16 + 4 * Zc + 15) / 16 * 16) + (16 + 4 * (R + 1) + 15) / 16 * 16), 128);
   auto stages_in = [&](int32_t kt_, int32_t budget_) {
     int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 128);
     int64_t per = b + s_bytes64;

@@ -46,9 +46,20 @@ struct SpmmParams {
   float* __restrict__ C;
   int64_t ldc;
   unsigned long long* trace;  // debug: per-CTA phase timestamps (globaltimer ns), or null
-  int32_t dbg;                // debug bits: 1 skip C stores, 2 B direct, 4 structure direct (experiments)
+  int32_t dbg;                // debug bits: 1 skip C stores, 2 unit direct, 8 consumer work x4 (experiments)
   int32_t tma2d;              // 1: full k-tiles staged with 2-D tensor TMA (maps valid)
+  int32_t sbulk;              // 1: col / vals / row_ptr bases are 16-byte aligned (bulk-copy the CSR slice)
 };
+
+// Stage layout of a unit's CSR slice, after the B tile: three int32 arrays
+// (col, vals, row pointers), each in a region of 16 + 4*count bytes rounded
+// to 16, with element 0 at byte (first & 3) * 4 so that the 16-byte-aligned
+// interior of the source lands 16-byte aligned (TMA bulk copy).
+__device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int32_t slice_region(int64_t count) { return (int32_t)((16 + 4 * count + 15) & ~15LL); }
+__host__ __device__ __forceinline__ int64_t slice_bytes(int64_t nnz, int64_t n) {
+  return 2LL * slice_region(nnz) + slice_region(n + 1);
+}
 
 // trace slots per CTA (bspmm_set_trace): 0 entry, 1 after PDL wait, 2 producer has unit-0 row
 // offsets, 3 producer has unit-0 structure offsets, 4 producer issued its last unit, 5 first
@@ -68,6 +79,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // CTA size cap per chunk count: 16 consumer warps fit the register budget with
 // up to 2 chunks per lane; 4 chunks need ~128 registers -> 15 consumer warps
 constexpr int kMaxThreads(int ch) { return ch >= 4 ? 512 : 544; }
+constexpr int kMaxRegs(int ch) { return ch >= 4 ? 128 : 120; }
 
 struct __align__(16) UnitHdr {
   int64_t g0;     // first global row of the matrix
@@ -158,21 +170,36 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
     mbar_wait(&empty[s], phase ^ 1u);
     unsigned char* st = ring + (size_t)s * stage_bytes;
     // a unit is staged whole (tile + structure) or not at all (read from global memory)
-    const bool bst = (int64_t)n * kw * 4 <= p.stage_b && 8LL * nnz + 4LL * (n + 1) <= p.stage_s && !(p.dbg & 2);
+    const bool bst = (int64_t)n * kw * 4 <= p.stage_b && slice_bytes(nnz, n) <= p.stage_s && !(p.dbg & 2);
     const bool sst = bst;
     const float* bsrc = p.B + g0 * p.ldb + c0;
-    if (bst && n > 0) {
-      if (VEC) {  // a-4: TMA (the whole contiguous B_i: one 1-D bulk copy; a full k-tile:
-                  // popcount(n) 2-D tensor copies; a ragged last tile: one bulk copy per row)
-        const uint32_t tx = (uint32_t)n * (uint32_t)kw * 4u;
-        if (kw == p.ldb) {
-          if (lane == 0) {
-            mbar_expect_tx(&full[s], tx);
-            bulk_g2s_hint(st, bsrc, tx, &full[s], pol);
-          }
-        } else if (p.tma2d && kw == p.kt) {
-          if (lane == 0) {
-            mbar_expect_tx(&full[s], tx);
+    unsigned char* sreg = st + p.stage_b;
+    if (bst) {
+      // a-4 + the CSR slice. Lane 0 announces every TMA byte of the unit once,
+      // then issues the copies; the <= 3 unaligned head/tail elements of each
+      // slice array go by 4-byte cp.async on lanes 0..17.
+      const int32_t a_col = p.sbulk ? (int32_t)(i64min(nz0 + nnz, (nz0 + 3) & ~3LL) - nz0) : nnz;
+      const int32_t b_col = p.sbulk ? max(a_col, (int32_t)(((nz0 + nnz) & ~3LL) - nz0)) : nnz;
+      const int64_t r_lo = g0, r_cnt = n + 1;
+      const int32_t a_rp = p.sbulk ? (int32_t)(i64min(r_lo + r_cnt, (r_lo + 3) & ~3LL) - r_lo) : (int32_t)r_cnt;
+      const int32_t b_rp = p.sbulk ? max(a_rp, (int32_t)(((r_lo + r_cnt) & ~3LL) - r_lo)) : (int32_t)r_cnt;
+      int32_t* dcol = reinterpret_cast<int32_t*>(sreg) + (nz0 & 3);
+      int32_t* dval = reinterpret_cast<int32_t*>(sreg + slice_region(nnz)) + (nz0 & 3);
+      int32_t* drp = reinterpret_cast<int32_t*>(sreg + 2 * slice_region(nnz)) + (r_lo & 3);
+      const bool b_bulk = VEC && n > 0;
+      if (lane == 0) {
+        uint32_t tx = 2u * 4u * (uint32_t)(b_col - a_col) + 4u * (uint32_t)(b_rp - a_rp);
+        if (b_bulk) tx += (uint32_t)n * (uint32_t)kw * 4u;
+        if (tx) mbar_expect_tx(&full[s], tx);
+        if (b_col > a_col) {
+          bulk_g2s(dcol + a_col, p.col + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+          bulk_g2s(dval + a_col, p.vals + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+        }
+        if (b_rp > a_rp) bulk_g2s(drp + a_rp, p.row_ptr + r_lo + a_rp, 4u * (uint32_t)(b_rp - a_rp), &full[s]);
+        if (b_bulk) {  // TMA: whole contiguous B_i (1-D) or a full k-tile (2-D boxes)
+          if (kw == p.ldb) {
+            bulk_g2s_hint(st, bsrc, (uint32_t)n * (uint32_t)kw * 4u, &full[s], pol);
+          } else if (p.tma2d && kw == p.kt) {
             int32_t r0 = 0;
             while (n - r0 >= 512) {
               tma_load_2d(st + (size_t)r0 * kw * 4, &maps.m[kTmaMaps - 1], c0, (int32_t)(g0 + r0), &full[s]);
@@ -186,13 +213,14 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
               }
             }
           }
-        } else {
-          if (lane == 0) mbar_expect_tx(&full[s], tx);
-          __syncwarp();
-          for (int r = lane; r < n; r += 32)
-            bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
         }
-      } else {
+      }
+      __syncwarp();
+      if (b_bulk && kw != p.ldb && !(p.tma2d && kw == p.kt)) {  // ragged last tile: one bulk copy per row
+        for (int r = lane; r < n; r += 32)
+          bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
+      }
+      if (!VEC) {
         float* dst = reinterpret_cast<float*>(st);
         const int32_t total = n * kw;
         for (int32_t q = lane; q < total; q += 32) {
@@ -200,16 +228,17 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
           cp_async4(dst + q, bsrc + (int64_t)r * p.ldb + c);
         }
       }
-    }
-    // then the (small) CSR structure
-    if (sst) {
-      int32_t* pairs = reinterpret_cast<int32_t*>(st + p.stage_b);
-      for (int32_t e = lane; e < nnz; e += 32) {
-        cp_async4(pairs + 2 * e, p.col + nz0 + e);
-        cp_async4(pairs + 2 * e + 1, p.vals + nz0 + e);
+      // head / tail (or everything when the bases are not 16-byte aligned)
+      for (int32_t e = lane; e < a_col; e += 32) {
+        cp_async4(dcol + e, p.col + nz0 + e);
+        cp_async4(dval + e, p.vals + nz0 + e);
       }
-      int32_t* rp = pairs + 2 * nnz;
-      for (int32_t r = lane; r <= n; r += 32) cp_async4(rp + r, p.row_ptr + g0 + r);
+      for (int32_t e = b_col + lane; e < nnz; e += 32) {
+        cp_async4(dcol + e, p.col + nz0 + e);
+        cp_async4(dval + e, p.vals + nz0 + e);
+      }
+      for (int32_t r = lane; r < a_rp; r += 32) cp_async4(drp + r, p.row_ptr + r_lo + r);
+      for (int32_t r = b_rp + lane; r < r_cnt; r += 32) cp_async4(drp + r, p.row_ptr + r_lo + r);
     }
     if (lane == 0) {
       UnitHdr h;
@@ -240,11 +269,12 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
   bool ok[CH];
 #pragma unroll
   for (int v = 0; v < CH; ++v) ok[v] = li + v * L < cols;
-  // row pointers and (col, val) pairs, indexed by ABSOLUTE entry position
-  const int32_t* rp = SST ? reinterpret_cast<const int32_t*>(st + p.stage_b) + 2 * h.nnz : p.row_ptr + h.g0;
-  const int2* pr = SST ? reinterpret_cast<const int2*>(st + p.stage_b) - h.nz0 : nullptr;
-  const float* col_v = p.vals;
-  const int32_t* col_i = p.col;
+  // row pointers, column ids and values of the slice, indexed by ABSOLUTE entry position
+  const unsigned char* sreg = st + p.stage_b;
+  const int32_t* rp = SST ? reinterpret_cast<const int32_t*>(sreg + 2 * slice_region(h.nnz)) + (h.g0 & 3)
+                          : p.row_ptr + h.g0;
+  const int32_t* col_i = SST ? reinterpret_cast<const int32_t*>(sreg) + (h.nz0 & 3) - h.nz0 : p.col;
+  const float* col_v = SST ? reinterpret_cast<const float*>(sreg + slice_region(h.nnz)) + (h.nz0 & 3) - h.nz0 : p.vals;
   // B rows of the tile (lane offset folded in) and C rows
   const float* Bt = BST ? reinterpret_cast<const float*>(st) + FW * li : p.B + h.g0 * p.ldb + h.c0 + FW * li;
   const int64_t bstride = BST ? (int64_t)h.kw : p.ldb;
@@ -272,9 +302,8 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
       for (int q = 0; q < G; ++q) {
         if (q < cnt) {
           if (SST) {
-            const int2 cv = pr[e + q];
-            cidx[q] = cv.x;
-            a[q] = __int_as_float(cv.y);
+            cidx[q] = col_i[e + q];
+            a[q] = col_v[e + q];
           } else {
             cidx[q] = __ldg(col_i + e + q);
             a[q] = __ldg(col_v + e + q);
@@ -392,8 +421,11 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
     const UnitHdr h = hdr[s];
     const unsigned char* st = ring + (size_t)s * stage_bytes;
-    if (h.flags == 3) rows<CH, VEC, true, true>(p, h, st, first, step, li);  // the hot, staged case
-    else rows_direct<CH, VEC>(p, h, first, step, li);
+    const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
+    for (int rep = 0; rep < reps; ++rep) {
+      if (h.flags == 3) rows<CH, VEC, true, true>(p, h, st, first, step, li);  // the hot, staged case
+      else rows_direct<CH, VEC>(p, h, first, step, li);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 8);
@@ -402,7 +434,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
 }
 
 template <int CH, bool VEC>
-__global__ void __launch_bounds__(kMaxThreads(CH), 1) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
@@ -476,6 +508,8 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.trace = a.trace;
   sp.dbg = a.dbg;
   sp.tma2d = a.maps != nullptr ? 1 : 0;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  sp.sbulk = (al16(a.col) && al16(a.vals) && al16(a.row_ptr)) ? 1 : 0;
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
