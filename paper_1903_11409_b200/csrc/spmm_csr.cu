@@ -357,6 +357,82 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
 // units that did not fit a stage (the paper's case 3): the
 // same storage-order sum read straight from global memory (L1/L2-cached B
 // gathers), a plain loop to keep the register allocation of the staged path
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void fma4(float4& acc, float a, const float4& b) {
+  acc.x = fmaf(a, b.x, acc.x);
+  acc.y = fmaf(a, b.y, acc.y);
+  acc.z = fmaf(a, b.z, acc.z);
+  acc.w = fmaf(a, b.w, acc.w);
+}
+
+// The hot loop for a staged unit whose tile is covered exactly by the lanes
+// (cols == lanes * CH, float4 chunks): no per-chunk predicates, 32-bit shared
+// addressing, two entries per iteration (independent loads first, FMAs in
+// storage order).  Same arithmetic as rows<> (bitwise O3').
+template <int CH>
+__device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const UnitHdr& h, const unsigned char* st,
+                                                 int first, int step, int li) {
+  const int L = p.lanes;
+  const uint32_t pitch = (uint32_t)h.kw * 4u;
+  const uint32_t sB = smem_addr(st) + 16u * (uint32_t)li;
+  const uint32_t vstep = 16u * (uint32_t)L;
+  const unsigned char* sreg = st + p.stage_b;
+  const int32_t* rp = reinterpret_cast<const int32_t*>(sreg + 2 * slice_region(h.nnz)) + (h.g0 & 3);
+  const int32_t* ci = reinterpret_cast<const int32_t*>(sreg) + (h.nz0 & 3) - h.nz0;
+  const float* cv = reinterpret_cast<const float*>(sreg + slice_region(h.nnz)) + (h.nz0 & 3) - h.nz0;
+  float* Ct = p.C + h.g0 * p.ldc + h.c0 + 4 * li;
+  int r = first;
+  int32_t nx0 = 0, nx1 = 0;
+  if (r < h.n) {
+    nx0 = rp[r];
+    nx1 = rp[r + 1];
+  }
+  for (; r < h.n; r += step) {
+    int32_t e = nx0;
+    const int32_t e1 = nx1;
+    if (r + step < h.n) {
+      nx0 = rp[r + step];
+      nx1 = rp[r + step + 1];
+    }
+    float4 acc[CH];
+#pragma unroll
+    for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (; e + 1 < e1; e += 2) {
+      const int32_t c0 = ci[e], c1 = ci[e + 1];
+      const float a0 = cv[e], a1 = cv[e + 1];
+      const uint32_t p0 = sB + (uint32_t)c0 * pitch, p1 = sB + (uint32_t)c1 * pitch;
+      float4 x0[CH], x1[CH];
+#pragma unroll
+      for (int v = 0; v < CH; ++v) {
+        x0[v] = lds128(p0 + v * vstep);
+        x1[v] = lds128(p1 + v * vstep);
+      }
+#pragma unroll
+      for (int v = 0; v < CH; ++v) fma4(acc[v], a0, x0[v]);
+#pragma unroll
+      for (int v = 0; v < CH; ++v) fma4(acc[v], a1, x1[v]);
+    }
+    if (e < e1) {
+      const int32_t c0 = ci[e];
+      const float a0 = cv[e];
+      const uint32_t p0 = sB + (uint32_t)c0 * pitch;
+#pragma unroll
+      for (int v = 0; v < CH; ++v) fma4(acc[v], a0, lds128(p0 + v * vstep));
+    }
+    float* crow = Ct + (int64_t)r * p.ldc;
+    if (p.dbg & 1) {
+      if (acc[0].x == 1.2345e-38f) crow[0] = 0.f;  // keep the math alive, store nothing
+      continue;
+    }
+#pragma unroll
+    for (int v = 0; v < CH; ++v) stg_cs_f4(crow + 4 * v * L, acc[v]);
+  }
+}
+
 template <int CH, bool VEC>
 __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& h, int first, int step, int li) {
   constexpr int FW = VEC ? 4 : 1;
@@ -423,8 +499,12 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     const unsigned char* st = ring + (size_t)s * stage_bytes;
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
     for (int rep = 0; rep < reps; ++rep) {
-      if (h.flags == 3) rows<CH, VEC, true, true>(p, h, st, first, step, li);  // the hot, staged case
-      else rows_direct<CH, VEC>(p, h, first, step, li);
+      if (h.flags == 3) {  // the hot, staged case
+        if (VEC && (h.kw >> 2) == p.lanes * CH) rows_staged_full<CH>(p, h, st, first, step, li);
+        else rows<CH, VEC, true, true>(p, h, st, first, step, li);
+      } else {
+        rows_direct<CH, VEC>(p, h, first, step, li);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
