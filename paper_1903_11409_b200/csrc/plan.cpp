@@ -85,7 +85,12 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   // tile's columns grouped in chunks of `pref` per lane (float4 chunks on the
   // vec path): one warp covers 32 / lanes rows per instruction
   const int32_t cols = vec ? (kt + 3) / 4 : kt;
-  const int32_t pref = chunks_pref > 0 ? std::min(chunks_pref, 4) : kDefaultChunks;
+  // 4 chunks per lane (4x more rows per warp instruction) pays off for small,
+  // latency-bound batches with wide tiles (C4: 8.5 vs 9.7 us); large batches
+  // prefer 2 (C5: 851 vs 860 us) -- tools/kbench.py sweeps
+  const int64_t units_ = (int64_t)batch * ceil_div(k, kt);
+  const int32_t pref_auto = (vec && kt >= 128 && units_ <= 4LL * num_sms) ? 4 : kDefaultChunks;
+  const int32_t pref = chunks_pref > 0 ? std::min(chunks_pref, 4) : pref_auto;
   p.lanes = bspmm_subwarp((int32_t)ceil_div(cols, pref));
   const int32_t ch = (int32_t)ceil_div(cols, p.lanes);
   p.chunks = ch <= 1 ? 1 : (ch <= 2 ? 2 : 4);

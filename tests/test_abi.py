@@ -104,7 +104,8 @@ def test_plan_invariants(k, batch):
             assert p["tiles"] == -(-k // p["kt"])                            # tiles cover [0, k)
             assert p["kt"] * (p["tiles"] - 1) < k <= p["kt"] * p["tiles"]    # disjoint, no empty tile
             cols = -(-p["kt"] // 4) if p["vec"] else p["kt"]
-            assert p["lanes"] == bs.subwarp(-(-cols // 2))                   # PAPER.md:150-155 on 2-chunks
+            pref = 4 if (p["vec"] and p["kt"] >= 128 and p["units"] <= 4 * 148) else 2
+            assert p["lanes"] == bs.subwarp(-(-cols // pref))                # PAPER.md:150-155 on chunks
             assert p["lanes"] * p["chunks"] >= cols and p["chunks"] in (1, 2, 4)
             p1 = bs.plan(k, batch, aligned=aligned, max_rows=rows, chunks=1)
             assert p1["lanes"] == bs.subwarp(cols)                           # the paper's rule, 1 chunk/lane
