@@ -35,8 +35,10 @@ def _load():
         lib.oracle_spmm_f32.argtypes = [I64, I32, P, P, P, P, P, P, I64, P, I64]
         lib.oracle_spmm_rows.argtypes = [I64, P, P, I32, P, P, P, P, P, I64, P, P]
         lib.oracle_partition.argtypes = [I64, P, I32, I32, P]
+        lib.oracle_csr_transpose.argtypes = [I64, P, P, P, P, P, P, P, P]
+        lib.oracle_sddmm.argtypes = [I64, I32, P, P, P, P, P, I64, P, I64, P, P]
         for f in (lib.oracle_offsets, lib.oracle_coo2csr, lib.oracle_spmm, lib.oracle_spmm_f32,
-                  lib.oracle_spmm_rows, lib.oracle_partition):
+                  lib.oracle_spmm_rows, lib.oracle_partition, lib.oracle_csr_transpose, lib.oracle_sddmm):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -147,3 +149,39 @@ def check_bound(C, C_ref, bound) -> tuple[bool, float]:
     with np.errstate(divide="ignore", invalid="ignore"):
         r = np.where(b > 0, d / b, np.where(d > 0, np.inf, 0.0))
     return ok, float(r.max()) if r.size else 0.0
+
+
+def csr_transpose(row_off, sizes, row_ptr, col, vals):
+    """O5: per-matrix A_i^T in canonical order. Returns (rowT, colT, valsT)."""
+    row_off = _c(row_off, np.int64)
+    sz = None if sizes is None else _c(sizes, np.int32)
+    row_ptr, col, vals = _c(row_ptr, np.int32), _c(col, np.int32), _c(vals, np.float32)
+    rt = np.zeros_like(row_ptr)
+    ct = np.zeros_like(col)
+    vt = np.zeros_like(vals)
+    assert _load().oracle_csr_transpose(row_off.shape[0] - 1, _p(row_off), _p(sz), _p(row_ptr), _p(col), _p(vals),
+                                        _p(rt), _p(ct), _p(vt)) == 0
+    return rt, ct, vt
+
+
+def sddmm(k, row_off, sizes, row_ptr, col, B, D, ldb=None, ldd=None):
+    """O6: out[e] = <D[row_e], B[col_e]> (fp64 -> fp32) and the per-entry bound."""
+    row_off = _c(row_off, np.int64)
+    sz = None if sizes is None else _c(sizes, np.int32)
+    row_ptr, col = _c(row_ptr, np.int32), _c(col, np.int32)
+    B, D = _c(B, np.float32), _c(D, np.float32)
+    ldb = B.shape[1] if ldb is None else ldb
+    ldd = D.shape[1] if ldd is None else ldd
+    out = np.zeros(col.shape[0], dtype=np.float32)
+    bound = np.zeros(col.shape[0], dtype=np.float64)
+    assert _load().oracle_sddmm(row_off.shape[0] - 1, k, _p(row_off), _p(sz), _p(row_ptr), _p(col), _p(B), ldb,
+                                _p(D), ldd, _p(out), _p(bound)) == 0
+    return out, bound
+
+
+def backward(k, row_off, row_ptr, col, vals, B, grad_C):
+    """grad_B = A^T grad_C (O5 + O3) and grad_vals = SDDMM (O6), each with its bound."""
+    rt, ct, vt = csr_transpose(row_off, None, row_ptr, col, vals)
+    gB, gB_bound = spmm(k, row_off, None, rt, ct, vt, grad_C)
+    gv, gv_bound = sddmm(k, row_off, None, row_ptr, col, B, grad_C)
+    return gB, gB_bound, gv, gv_bound

@@ -27,11 +27,18 @@
  *   O3s oracle_spmm_rows   O3 for a list of sampled (matrix, row) pairs.
  *   O4 oracle_partition    contiguous split of graphs over G ranks by nnz*k
  *                          prefix (north_star; R25).
+ *   O5 oracle_csr_transpose per-matrix A_i^T (backward), canonical
+ *                          (row, col, original position) order.
+ *   O6 oracle_sddmm        grad_vals[e] = <grad_C[row_e], B[col_e]> in fp64
+ *                          with bound 1e-5 * sum |d||b| (adjoint of C = A B,
+ *                          SPEC.md:178-186).
  *
  * Pins (tests/test_oracle_pins.py): dense brute force A@B (numpy fp64) on
  * >=1000 tiny batches, identity -> C == B, SPEC.md:140 example, zero rows,
  * linearity in B, integer-valued exactness, COO permutation invariance and
- * brute-force sorted(), partition invariants and closed forms.
+ * brute-force sorted(), partition invariants and closed forms; backward:
+ * central finite differences of L = sum(C * G), dense A^T brute force,
+ * SPEC.md:177/:185 worked examples.
  */
 #include <math.h>
 #include <stdint.h>
@@ -185,6 +192,73 @@ int oracle_partition(int64_t batch, const int64_t* nnz_off, int32_t k, int32_t p
     int64_t j = 0;
     while (j < batch && (nnz_off[j] - nnz_off[0]) * (int64_t)k * parts < (int64_t)r * T) ++j;
     split[r] = (int32_t)j;
+  }
+  return 0;
+}
+
+/* ---- backward (NEXT-2): "The Batched SpMM is also applied to
+ * backward propagation"; formulas are the standard adjoints of C = A B
+ * (SPEC.md:169-186): grad_B = A^T grad_C, grad_vals[e] = <grad_C[row_e], B[col_e]>. */
+
+/* O5 per-matrix transpose of a block-diagonal CSR: entries (r, c, v) of A_i
+ * become (c, r, v) of A_i^T, emitted in canonical (row, col, original
+ * position) order; absolute row pointers, LOCAL column ids. */
+int oracle_csr_transpose(int64_t batch, const int64_t* row_off, const int32_t* sizes,
+                         const int32_t* row_ptr, const int32_t* col, const float* vals,
+                         int32_t* rowT, int32_t* colT, float* valsT) {
+  if (batch < 0) return 1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < batch; ++i) {
+    int64_t n = rows_of(row_off, sizes, i);
+    int64_t g0 = row_off[i];
+    int64_t z0 = row_ptr[g0], m = row_ptr[g0 + n] - z0;
+    trip_t* t = (trip_t*)malloc(sizeof(trip_t) * (size_t)(m > 0 ? m : 1));
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t e = row_ptr[g0 + r]; e < row_ptr[g0 + r + 1]; ++e) {
+        t[e - z0].row = col[e];        /* transposed: column becomes row */
+        t[e - z0].col = (int32_t)r;
+        t[e - z0].pos = e - z0;
+      }
+    qsort(t, (size_t)m, sizeof(trip_t), cmp_trip);
+    int64_t e = 0;
+    for (int64_t r = 0; r < n; ++r) {
+      rowT[g0 + r] = (int32_t)(z0 + e);
+      while (e < m && t[e].row == r) ++e;
+    }
+    for (int64_t g = g0 + n; g < row_off[i + 1]; ++g) rowT[g] = (int32_t)(z0 + m);
+    for (int64_t q = 0; q < m; ++q) {
+      colT[z0 + q] = t[q].col;
+      valsT[z0 + q] = vals[z0 + t[q].pos];
+    }
+    free(t);
+  }
+  if (batch > 0) rowT[row_off[batch]] = row_ptr[row_off[batch]];
+  return 0;
+}
+
+/* O6 SDDMM at the sparsity pattern: out[e] = sum_c D[row_e][c] * B[col_e][c]
+ * (fp64 accumulation, one rounding), bound[e] = 1e-5 * sum_c |D||B|. */
+int oracle_sddmm(int64_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
+                 const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb,
+                 const float* D, int64_t ldd, float* out, double* bound) {
+  if (batch < 0 || k < 0) return 1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < batch; ++i) {
+    int64_t n = rows_of(row_off, sizes, i);
+    for (int64_t r = 0; r < n; ++r) {
+      int64_t g = row_off[i] + r;
+      for (int64_t e = row_ptr[g]; e < row_ptr[g + 1]; ++e) {
+        double acc = 0.0, s = 0.0;
+        for (int32_t c = 0; c < k; ++c) {
+          double d = (double)D[g * ldd + c];
+          double b = (double)B[(row_off[i] + col[e]) * ldb + c];
+          acc += d * b;
+          s += fabs(d) * fabs(b);
+        }
+        out[e] = (float)acc;
+        if (bound) bound[e] = 1e-5 * s;
+      }
+    }
   }
   return 0;
 }

@@ -310,3 +310,95 @@ def test_partition_equal_cost_closed_form():
     for batch, G in ((64, 8), (65536, 8), (100, 4), (12, 3)):
         nnz_off = np.arange(batch + 1, dtype=np.int64) * 5
         assert list(oracle.partition(nnz_off, 256, G)) == [r * batch // G for r in range(G + 1)]
+
+
+# ---------------------------------------------------------------- O5 / O6 (backward, NEXT-2)
+
+def test_transpose_dense_and_involution():
+    rng = np.random.default_rng(12)
+    for trial in range(200):
+        b = synth.random_batch(rng, int(rng.integers(0, 5)), 1, nmax=9, dmax=4, duplicates=bool(trial % 2))
+        rt, ct, vt = oracle.csr_transpose(b.row_off, None, b.row_ptr, b.col, b.vals)
+        At = dense_blocks(b, vals=vt, col=ct, row_ptr=rt)
+        for A, T_ in zip(dense_blocks(b), At):
+            assert np.array_equal(A.T, T_)
+        # canonical order: columns non-decreasing within every transposed row
+        for g in range(b.n_rows):
+            assert np.all(np.diff(ct[rt[g]:rt[g + 1]]) >= 0)
+    # (A^T)^T == A exactly on canonical input (sorted rows, no duplicates)
+    b = synth.config(3, coo=False)
+    rt, ct, vt = oracle.csr_transpose(b.row_off, None, b.row_ptr, b.col, b.vals)
+    r2, c2, v2 = oracle.csr_transpose(b.row_off, None, rt, ct, vt)
+    assert np.array_equal(r2, b.row_ptr) and np.array_equal(c2, b.col)
+    assert np.array_equal(v2.view(np.uint32), b.vals.view(np.uint32))
+
+
+def test_sddmm_dense_brute_force():
+    rng = np.random.default_rng(13)
+    for trial in range(300):
+        k = int(rng.integers(1, 12))
+        b = synth.random_batch(rng, int(rng.integers(0, 5)), k, nmax=9, dmax=4, duplicates=bool(trial % 2))
+        G = (rng.integers(-(1 << 23), 1 << 23, size=b.B.shape) / float(1 << 23)).astype(np.float32)
+        out, bound = oracle.sddmm(k, b.row_off, None, b.row_ptr, b.col, b.B, G)
+        for i in range(b.batch):
+            g0, g1 = int(b.row_off[i]), int(b.row_off[i + 1])
+            M = G[g0:g1].astype(np.float64) @ b.B[g0:g1].astype(np.float64).T      # library matmul
+            for r in range(g1 - g0):
+                for e in range(b.row_ptr[g0 + r], b.row_ptr[g0 + r + 1]):
+                    ref = M[r, b.col[e]]
+                    assert abs(float(out[e]) - ref) <= 1e-6 * (bound[e] / 1e-5) + abs(ref) * 2 ** -23
+
+
+def test_backward_finite_differences():
+    """L(B, vals) = sum(C * G): dL/dB = A^T G and dL/dvals = SDDMM(G, B) (central differences, fp64)."""
+    rng = np.random.default_rng(14)
+    b = synth.random_batch(rng, 3, 3, nmax=5, dmax=2, allow_empty_graphs=False, duplicates=True)
+    G = rng.standard_normal(b.B.shape)
+    gB, _, gv, _ = oracle.backward(b.k, b.row_off, b.row_ptr, b.col, b.vals, b.B, G.astype(np.float32))
+
+    def L(Bm, vals):
+        tot = 0.0
+        for i in range(b.batch):
+            g0, g1 = int(b.row_off[i]), int(b.row_off[i + 1])
+            A = np.zeros((g1 - g0, g1 - g0))
+            for r in range(g1 - g0):
+                for e in range(b.row_ptr[g0 + r], b.row_ptr[g0 + r + 1]):
+                    A[r, b.col[e]] += vals[e]
+            tot += float(np.sum((A @ Bm[g0:g1]) * G[g0:g1]))
+        return tot
+
+    h = 1e-3
+    B64, v64 = b.B.astype(np.float64), b.vals.astype(np.float64)
+    for idx in np.ndindex(*B64.shape):
+        Bp, Bm = B64.copy(), B64.copy()
+        Bp[idx] += h
+        Bm[idx] -= h
+        fd = (L(Bp, v64) - L(Bm, v64)) / (2 * h)
+        assert abs(fd - gB[idx]) < 1e-4 * (1 + abs(fd))
+    for e in range(v64.shape[0]):
+        vp, vm = v64.copy(), v64.copy()
+        vp[e] += h
+        vm[e] -= h
+        fd = (L(B64, vp) - L(B64, vm)) / (2 * h)
+        assert abs(fd - gv[e]) < 1e-4 * (1 + abs(fd))
+
+
+def test_backward_golden(golden):
+    for ex in golden["backward"]:
+        n, k = ex["n"], ex["k"]
+        ent = sorted((r, c, v) for r, c, v in ex["entries"])
+        rp = np.zeros(n + 1, dtype=np.int32)
+        for r, _, _ in ent:
+            rp[r + 1] += 1
+        rp = np.cumsum(rp).astype(np.int32)
+        col = np.array([c for _, c, _ in ent], dtype=np.int32)
+        vals = np.array([v for _, _, v in ent], dtype=np.float32)
+        B = np.array(ex["B"], dtype=np.float32)
+        G = np.array(ex["grad_C"], dtype=np.float32)
+        gB, _, gv, _ = oracle.backward(k, [0, n], rp, col, vals, B, G)
+        assert np.array_equal(gB, np.array(ex["grad_B"], dtype=np.float32)), ex["cite"]
+        assert list(gv) == ex["grad_vals"], ex["cite"]
+    # zero upstream gradient -> zero gradients
+    b = synth.config(1)
+    gB, _, gv, _ = oracle.backward(b.k, b.row_off, b.row_ptr, b.col, b.vals, b.B, np.zeros_like(b.B))
+    assert not gB.any() and not gv.any()
