@@ -201,6 +201,37 @@ BSPMM_API bspmm_status_t bspmm_coo2csr(bspmm_handle_t h, int32_t batch, const in
 BSPMM_API bspmm_status_t bspmm_build_offsets(bspmm_handle_t h, int32_t batch, const int32_t* sizes,
                                              int64_t* offsets_out);
 
+/* ---- backward ("also applied to backward propagation") ------
+ * For C_i = A_i B_i and an upstream gradient G = dL/dC (layout of C), the
+ * standard adjoints: dL/dB_i = A_i^T G_i and dL/dval_e = <G[row_e], B[col_e]>. */
+
+/* Per-matrix transpose of a block-diagonal CSR: A_i^T in canonical (row, col,
+ * original position) order, absolute row pointers, LOCAL column ids, values
+ * moved bitwise.  row_off (dev) required; outputs [total_rows+1],
+ * [total_nnz], [total_nnz] dev.  A static graph can be transposed once and
+ * then multiplied with bspmm_csr. */
+BSPMM_API bspmm_status_t bspmm_csr_transpose(bspmm_handle_t h, int32_t batch, const int64_t* row_off,
+                                             const int32_t* sizes, const int32_t* row_ptr, const int32_t* col,
+                                             const float* vals, int64_t total_rows, int64_t total_nnz,
+                                             int32_t* rowT_out, int32_t* colT_out, float* valsT_out);
+
+/* Batched SDDMM at A's pattern: out[e] = sum_{c<k} G[row_e][c] * B[col_e][c]
+ * for every stored entry e (fp32, deterministic warp-shuffle reduction;
+ * accurate to the fp32 dot-product bound).  out [nnz] dev. */
+BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                     const int32_t* sizes, const int32_t* row_ptr, const int32_t* col, const float* B,
+                                     int64_t ldb, const float* G, int64_t ldg, float* out);
+
+/* Backward of bspmm_csr: grad_B (nullable) = A^T grad_C via an internal
+ * transpose + the forward kernel (bitwise the fp32 storage-order sum over the
+ * canonical A^T); grad_vals (nullable) = SDDMM(grad_C, B).  grad_B must not
+ * alias grad_C.  total_rows / total_nnz: host sizes of the CSR. */
+BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                            const int32_t* sizes, const int32_t* row_ptr, const int32_t* col,
+                                            const float* vals, const float* B, int64_t ldb, const float* grad_C,
+                                            int64_t ldgc, float* grad_B, int64_t ldgb, float* grad_vals,
+                                            int64_t total_rows, int64_t total_nnz);
+
 /* End-to-end call on HOST buffers (packed layout, ldb = ldc = k): copies the
  * inputs host->device (pinned memory recommended), builds offsets, runs the
  * CSR kernel and copies C back, pipelined in row chunks across copy and

@@ -197,6 +197,62 @@ class Handle:
         self._raise(st, "bspmm_coo2csr")
         return rp, col, v
 
+    # ---- backward (NEXT-2) ---------------------------------------------------------
+    def csr_transpose(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], row_ptr: torch.Tensor,
+                      col: torch.Tensor, vals: torch.Tensor):
+        """Per-matrix A_i^T (canonical order) on the device: (rowT, colT, valsT)."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("row_ptr", row_ptr, torch.int32), ("col", col, torch.int32),
+                            ("vals", vals, torch.float32)):
+            _check(t, name, dt, dev)
+        rt = torch.empty_like(row_ptr)
+        ct = torch.empty_like(col)
+        vt = torch.empty_like(vals)
+        self._stream()
+        st = lib.bspmm_csr_transpose(self._h, row_off.shape[0] - 1, _ptr(row_off), _ptr(sizes), _ptr(row_ptr),
+                                     _ptr(col), _ptr(vals), int(row_ptr.shape[0] - 1), int(col.shape[0]), _ptr(rt),
+                                     _ptr(ct), _ptr(vt))
+        self._raise(st, "bspmm_csr_transpose")
+        return rt, ct, vt
+
+    def sddmm(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], row_ptr: torch.Tensor, col: torch.Tensor,
+              B: torch.Tensor, G: torch.Tensor, out: Optional[torch.Tensor] = None, k: Optional[int] = None):
+        """out[e] = <G[row_e], B[col_e]> at A's pattern (bspmm_sddmm)."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("row_ptr", row_ptr, torch.int32), ("col", col, torch.int32),
+                            ("B", B, torch.float32), ("G", G, torch.float32)):
+            _check(t, name, dt, dev)
+        k = B.shape[1] if k is None else k
+        if out is None:
+            out = torch.empty(col.shape[0], dtype=torch.float32, device=dev)
+        self._stream()
+        st = lib.bspmm_sddmm(self._h, row_off.shape[0] - 1, k, _ptr(row_off), _ptr(sizes), _ptr(row_ptr), _ptr(col),
+                             _ptr(B), _ld(B, k, "B"), _ptr(G), _ld(G, k, "G"), _ptr(out))
+        self._raise(st, "bspmm_sddmm")
+        return out
+
+    def csr_backward(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], row_ptr: torch.Tensor,
+                     col: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, grad_C: torch.Tensor,
+                     want_B: bool = True, want_vals: bool = True):
+        """(grad_B, grad_vals) of C = A B for upstream grad_C (bspmm_csr_backward)."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("row_ptr", row_ptr, torch.int32), ("col", col, torch.int32),
+                            ("vals", vals, torch.float32), ("B", B, torch.float32), ("grad_C", grad_C, torch.float32)):
+            _check(t, name, dt, dev)
+        k = grad_C.shape[1]
+        gB = torch.empty((grad_C.shape[0], k), dtype=torch.float32, device=dev) if want_B else None
+        gv = torch.empty(col.shape[0], dtype=torch.float32, device=dev) if want_vals else None
+        self._stream()
+        st = lib.bspmm_csr_backward(self._h, row_off.shape[0] - 1, k, _ptr(row_off), _ptr(sizes), _ptr(row_ptr),
+                                    _ptr(col), _ptr(vals), _ptr(B), _ld(B, k, "B"), _ptr(grad_C),
+                                    _ld(grad_C, k, "grad_C"), _ptr(gB), _ld(gB, k, "grad_B") if want_B else k,
+                                    _ptr(gv), int(row_ptr.shape[0] - 1), int(col.shape[0]))
+        self._raise(st, "bspmm_csr_backward")
+        return gB, gv
+
     def csr_host(self, sizes: np.ndarray, row_ptr: np.ndarray, col: np.ndarray, vals: np.ndarray, B: np.ndarray,
                  C: Optional[np.ndarray] = None) -> np.ndarray:
         """End-to-end on host buffers (bspmm_csr_host): H2D, offsets, SpMM, D2H, pipelined; synchronous.

@@ -39,6 +39,9 @@ _SIGS = {
     "bspmm_coo2csr": (I32, [P, I32, P, P, P, P, P, I64, I64, P, P, P]),
     "bspmm_build_offsets": (I32, [P, I32, P, P]),
     "bspmm_csr_host": (I32, [P, I32, I32, P, P, P, P, P, P, I64, I64]),
+    "bspmm_csr_transpose": (I32, [P, I32, P, P, P, P, P, I64, I64, P, P, P]),
+    "bspmm_sddmm": (I32, [P, I32, I32, P, P, P, P, P, I64, P, I64, P]),
+    "bspmm_csr_backward": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64, P, I64, P, I64, I64]),
     "bspmm_partition": (I32, [I32, P, I32, I32, P]),
     "bspmm_subwarp": (I32, [I32]),
     "bspmm_plan": (I32, [I32, I32, I32, I32, I64, I32, I32, I32, I32, I32, I32, ctypes.POINTER(Plan)]),

@@ -445,6 +445,131 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
   return csr_impl(h, batch, k, ro, sizes, rp, col, val, B, ldb, C, ldc, false);
 }
 
+// ---- backward (NEXT-2) ------------------------------------------------------
+// workspace: [idx 2*NNZ i32][nnz_off (batch+1) i64][keys 2*NNZ u64][pay 2*NNZ u32]
+//            [+ rowT (N+1) i32, colT NNZ i32, valsT NNZ f32 when the transpose is internal]
+struct TransWs {
+  int32_t* idx;
+  int64_t* nnz_off;
+  uint64_t* keys;
+  uint32_t* pay;
+  int32_t *rowT, *colT;
+  float* valsT;
+};
+
+static bspmm_status_t trans_workspace(bspmm_handle_t h, int32_t batch, int64_t N, int64_t NNZ, bool internal,
+                                      TransWs* w) {
+  size_t off = 0;
+  const size_t o_idx = off;
+  off += al256((size_t)2 * NNZ * 4 + 4);
+  const size_t o_no = off;
+  off += al256((size_t)(batch + 1) * 8);
+  const size_t o_keys = off;
+  off += al256((size_t)2 * NNZ * 8 + 8);
+  const size_t o_pay = off;
+  off += al256((size_t)2 * NNZ * 4 + 4);
+  const size_t o_rt = off;
+  off += internal ? al256((size_t)(N + 1) * 4) : 0;
+  const size_t o_ct = off;
+  off += internal ? al256((size_t)NNZ * 4 + 4) : 0;
+  const size_t o_vt = off;
+  off += internal ? al256((size_t)NNZ * 4 + 4) : 0;
+  bspmm_status_t st = grow(h, &h->ws, &h->ws_bytes, off);
+  if (st != BSPMM_SUCCESS) return st;
+  char* b = static_cast<char*>(h->ws);
+  w->idx = reinterpret_cast<int32_t*>(b + o_idx);
+  w->nnz_off = reinterpret_cast<int64_t*>(b + o_no);
+  w->keys = reinterpret_cast<uint64_t*>(b + o_keys);
+  w->pay = reinterpret_cast<uint32_t*>(b + o_pay);
+  w->rowT = internal ? reinterpret_cast<int32_t*>(b + o_rt) : nullptr;
+  w->colT = internal ? reinterpret_cast<int32_t*>(b + o_ct) : nullptr;
+  w->valsT = internal ? reinterpret_cast<float*>(b + o_vt) : nullptr;
+  return BSPMM_SUCCESS;
+}
+
+static bspmm_status_t transpose_impl(bspmm_handle_t h, int32_t batch, const int64_t* row_off, const int32_t* sizes,
+                                     const int32_t* row_ptr, const int32_t* col, const float* vals, int64_t NNZ,
+                                     int32_t* rowT, int32_t* colT, float* valsT, const TransWs& w) {
+  if (h->flags & BSPMM_VALIDATE) {
+    CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
+    CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr, col, h->dev_flag, h->stream));
+    h->launches++;
+    bspmm_status_t st = check_validate_flag(h);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  CK(h, launch_transpose_expand(batch, row_off, sizes, row_ptr, col, w.idx, w.nnz_off, h->stream));
+  h->launches++;
+  const int32_t cap = coo_smem_cap(h->hint_nnz, h->smem_optin);
+  CK(h, launch_coo2csr(batch, row_off, sizes, w.nnz_off, w.idx, vals, rowT, colT, valsT, w.keys, w.pay, NNZ, cap,
+                       h->stream));
+  h->launches++;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_csr_transpose(bspmm_handle_t h, int32_t batch, const int64_t* row_off,
+                                             const int32_t* sizes, const int32_t* row_ptr, const int32_t* col,
+                                             const float* vals, int64_t total_rows, int64_t total_nnz,
+                                             int32_t* rowT_out, int32_t* colT_out, float* valsT_out) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || total_rows < 0 || total_nnz < 0 || total_nnz > INT32_MAX)
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "bad batch / totals");
+  if (batch == 0) return BSPMM_SUCCESS;
+  if (!row_off || !row_ptr || !rowT_out || (total_nnz > 0 && (!col || !vals || !colT_out || !valsT_out)))
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  DeviceGuard g(h->device);
+  TransWs w;
+  bspmm_status_t st = trans_workspace(h, batch, total_rows, total_nnz, false, &w);
+  if (st != BSPMM_SUCCESS) return st;
+  return transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, total_nnz, rowT_out, colT_out, valsT_out, w);
+}
+
+BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                     const int32_t* sizes, const int32_t* row_ptr, const int32_t* col, const float* B,
+                                     int64_t ldb, const float* G, int64_t ldg, float* out) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || k < 1 || ldb < k || ldg < k) return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1 or ld<k");
+  if (batch == 0) return BSPMM_SUCCESS;
+  if (!row_off || !row_ptr) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  DeviceGuard g(h->device);
+  if (h->flags & BSPMM_VALIDATE) {
+    CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
+    CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr, col, h->dev_flag, h->stream));
+    h->launches++;
+    bspmm_status_t st = check_validate_flag(h);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  CK(h, launch_sddmm(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, h->stream));
+  h->launches++;
+  return BSPMM_SUCCESS;
+}
+
+BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                            const int32_t* sizes, const int32_t* row_ptr, const int32_t* col,
+                                            const float* vals, const float* B, int64_t ldb, const float* grad_C,
+                                            int64_t ldgc, float* grad_B, int64_t ldgb, float* grad_vals,
+                                            int64_t total_rows, int64_t total_nnz) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || k < 1 || ldgc < k || (grad_B && ldgb < k) || (grad_vals && ldb < k) || total_rows < 0 ||
+      total_nnz < 0 || total_nnz > INT32_MAX)
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1, ld<k or bad totals");
+  if (batch == 0 || (!grad_B && !grad_vals)) return BSPMM_SUCCESS;
+  if (!row_off || !row_ptr) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  DeviceGuard g(h->device);
+  if (grad_vals) {  // dL/dval_e = <grad_C[row_e], B[col_e]>
+    bspmm_status_t st = bspmm_sddmm(h, batch, k, row_off, sizes, row_ptr, col, B, ldb, grad_C, ldgc, grad_vals);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  if (grad_B) {  // dL/dB_i = A_i^T grad_C_i: transpose, then the forward kernel
+    TransWs w;
+    bspmm_status_t st = trans_workspace(h, batch, total_rows, total_nnz, true, &w);
+    if (st != BSPMM_SUCCESS) return st;
+    st = transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, total_nnz, w.rowT, w.colT, w.valsT, w);
+    if (st != BSPMM_SUCCESS) return st;
+    return csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
+  }
+  return BSPMM_SUCCESS;
+}
+
 // ---- end-to-end host-buffer path ------------------------------------------
 BSPMM_API bspmm_status_t bspmm_csr_host(bspmm_handle_t h, int32_t batch, int32_t k, const int32_t* sizes_host,
                                         const int32_t* row_ptr_host, const int32_t* col_host,

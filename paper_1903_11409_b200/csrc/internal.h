@@ -80,6 +80,12 @@ cudaError_t launch_coo2csr(int32_t batch, const int64_t* row_off, const int32_t*
                            int32_t* col_out, float* val_out, uint64_t* ws_keys, uint32_t* ws_pay,
                            int64_t ws_stride, int32_t smem_cap, cudaStream_t s);
 int32_t coo_smem_cap(int64_t max_nnz_hint, int32_t smem_optin);
+cudaError_t launch_transpose_expand(int32_t batch, const int64_t* row_off, const int32_t* sizes,
+                                    const int32_t* row_ptr, const int32_t* col, int32_t* idx, int64_t* nnz_off,
+                                    cudaStream_t s);
+cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
+                         const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
+                         int64_t ldg, float* out, cudaStream_t s);
 cudaError_t launch_validate_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes,
                                 const int32_t* row_ptr, const int32_t* col, int* flag, cudaStream_t s);
 cudaError_t launch_validate_coo(int32_t batch, const int64_t* row_off, const int32_t* sizes,
