@@ -49,6 +49,7 @@ struct SpmmParams {
   int32_t dbg;                // debug bits: 1 skip C stores, 2 unit direct, 8 consumer work x4 (experiments)
   int32_t tma2d;              // 1: full k-tiles staged with 2-D tensor TMA (maps valid)
   int32_t sbulk;              // 1: col / vals / row_ptr bases are 16-byte aligned (bulk-copy the CSR slice)
+  int32_t prefetch;           // 1: L2-prefetch every unit of a batch up front (small problems)
 };
 
 // Stage layout of a unit's CSR slice, after the B tile: three int32 arrays
@@ -157,6 +158,37 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
       if (j == 0 && lane == 0) BSPMM_TRACE(p, 2);
     }
     if (jj == 8 || (jj == 0 && u + 8 * G >= p.units)) meta_rt2(p, u + (32 - jj + lane) * G, nxt);
+    if (jj == 0 && p.prefetch) {
+      // small problem: prefetch this lane's unit of the batch (B tile + CSR
+      // slice) into L2 now; the smem TMA loads below then hit L2 instead of
+      // queueing DRAM-latency-bound behind the SM's outstanding-copy limit
+      const int64_t uu = u + (int64_t)lane * G;
+      if (uu < p.units && cur.n > 0) {
+        const int32_t nnz_ = cur.nz1 - cur.nz0;
+        const int64_t z0 = cur.nz0 & ~3LL, z1 = (cur.nz1 + 3) & ~3LL;
+        if (nnz_ > 0 && p.sbulk) {
+          prefetch_l2(p.col + z0, (uint32_t)(z1 - z0) * 4u);
+          prefetch_l2(p.vals + z0, (uint32_t)(z1 - z0) * 4u);
+        }
+        if (VEC) {
+          const float* bsrc = p.B + cur.g0 * p.ldb + cur.c0;
+          if (cur.kw == p.ldb) {
+            prefetch_l2(bsrc, (uint32_t)cur.n * (uint32_t)cur.kw * 4u);
+          } else if (p.tma2d && cur.kw == p.kt) {
+            int32_t r0 = 0;
+            while (cur.n - r0 >= 512) {
+              prefetch_l2_2d(&maps.m[kTmaMaps - 1], cur.c0, (int32_t)(cur.g0 + r0));
+              r0 += 256;
+            }
+            for (int b = kTmaMaps - 1; b >= 0; --b)
+              if ((cur.n - r0) & (1 << b)) {
+                prefetch_l2_2d(&maps.m[b], cur.c0, (int32_t)(cur.g0 + r0));
+                r0 += 1 << b;
+              }
+          }
+        }
+      }
+    }
     const int64_t g0 = __shfl_sync(0xffffffffu, cur.g0, jj);
     const int32_t n = __shfl_sync(0xffffffffu, cur.n, jj);
     const int32_t c0 = __shfl_sync(0xffffffffu, cur.c0, jj);
@@ -590,6 +622,9 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.tma2d = a.maps != nullptr ? 1 : 0;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   sp.sbulk = (al16(a.col) && al16(a.vals) && al16(a.row_ptr)) ? 1 : 0;
+  // prefetch only when every CTA's whole share is one metadata batch (<= 32 units):
+  // the prefetched bytes then never exceed the problem (small, L2-resident)
+  sp.prefetch = (plan.units <= 32LL * plan.grid && !(a.dbg & 16)) ? 1 : 0;
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
