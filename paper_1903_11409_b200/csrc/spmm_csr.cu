@@ -624,7 +624,8 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.sbulk = (al16(a.col) && al16(a.vals) && al16(a.row_ptr)) ? 1 : 0;
   // prefetch only when every CTA's whole share is one metadata batch (<= 32 units):
   // the prefetched bytes then never exceed the problem (small, L2-resident)
-  sp.prefetch = (plan.units <= 32LL * plan.grid && !(a.dbg & 16)) ? 1 : 0;
+  // (measured: no gain on C3/C4, so off unless requested with debug bit 16)
+  sp.prefetch = (plan.units <= 32LL * plan.grid && (a.dbg & 16)) ? 1 : 0;
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
