@@ -200,6 +200,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
     const int s = j % p.stages;
     const uint32_t phase = (uint32_t)(j / p.stages) & 1u;
     mbar_wait(&empty[s], phase ^ 1u);
+    if (j == 0 && lane == 0) BSPMM_TRACE(p, 9);
     unsigned char* st = ring + (size_t)s * stage_bytes;
     // a unit is staged whole (tile + structure) or not at all (read from global memory)
     const bool bst = (int64_t)n * kw * 4 <= p.stage_b && slice_bytes(nnz, n) <= p.stage_s && !(p.dbg & 2);
@@ -219,39 +220,40 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
       int32_t* dval = reinterpret_cast<int32_t*>(sreg + slice_region(nnz)) + (nz0 & 3);
       int32_t* drp = reinterpret_cast<int32_t*>(sreg + 2 * slice_region(nnz)) + (r_lo & 3);
       const bool b_bulk = VEC && n > 0;
+      // lane 0 announces every TMA byte of the unit, then each copy is issued
+      // by its own lane: on a cold start every issue stalls its thread ~0.1 us
+      // (measured with tools/trace.py), so serial issue from one lane cost
+      // ~1 us per unit; spread over lanes the stalls overlap
       if (lane == 0) {
         uint32_t tx = 2u * 4u * (uint32_t)(b_col - a_col) + 4u * (uint32_t)(b_rp - a_rp);
         if (b_bulk) tx += (uint32_t)n * (uint32_t)kw * 4u;
         if (tx) mbar_expect_tx(&full[s], tx);
-        if (b_col > a_col) {
-          bulk_g2s(dcol + a_col, p.col + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
-          bulk_g2s(dval + a_col, p.vals + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
-        }
-        if (b_rp > a_rp) bulk_g2s(drp + a_rp, p.row_ptr + r_lo + a_rp, 4u * (uint32_t)(b_rp - a_rp), &full[s]);
-        if (b_bulk) {  // TMA: whole contiguous B_i (1-D) or a full k-tile (2-D boxes)
-          if (kw == p.ldb) {
-            bulk_g2s_hint(st, bsrc, (uint32_t)n * (uint32_t)kw * 4u, &full[s], pol);
-          } else if (p.tma2d && kw == p.kt) {
-            int32_t r0 = 0;
-            while (n - r0 >= 512) {
-              tma_load_2d(st + (size_t)r0 * kw * 4, &maps.m[kTmaMaps - 1], c0, (int32_t)(g0 + r0), &full[s]);
-              r0 += 256;
-            }
-#pragma unroll
-            for (int b = kTmaMaps - 1; b >= 0; --b) {
-              if ((n - r0) & (1 << b)) {
-                tma_load_2d(st + (size_t)r0 * kw * 4, &maps.m[b], c0, (int32_t)(g0 + r0), &full[s]);
-                r0 += 1 << b;
-              }
-            }
-          }
-        }
       }
       __syncwarp();
-      if (b_bulk && kw != p.ldb && !(p.tma2d && kw == p.kt)) {  // ragged last tile: one bulk copy per row
-        for (int r = lane; r < n; r += 32)
-          bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
+      if (b_col > a_col) {
+        if (lane == 0) bulk_g2s(dcol + a_col, p.col + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+        if (lane == 1) bulk_g2s(dval + a_col, p.vals + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
       }
+      if (lane == 2 && b_rp > a_rp) bulk_g2s(drp + a_rp, p.row_ptr + r_lo + a_rp, 4u * (uint32_t)(b_rp - a_rp), &full[s]);
+      if (b_bulk) {  // TMA: whole contiguous B_i (1-D), a full k-tile (2-D boxes), else one bulk copy per row
+        if (kw == p.ldb) {
+          if (lane == 3) bulk_g2s_hint(st, bsrc, (uint32_t)n * (uint32_t)kw * 4u, &full[s], pol);
+        } else if (p.tma2d && kw == p.kt) {
+          // boxes: floor(n / 256) of 256 rows (lanes 4..), then the set bits of n % 256 (lanes 16 + b)
+          const int32_t big = n >> 8, rem = n & 255;
+          for (int32_t q = lane - 4; q >= 0 && q < big && lane < 16; q += 12)
+            tma_load_2d(st + (size_t)q * 256 * kw * 4, &maps.m[kTmaMaps - 1], c0, (int32_t)(g0 + q * 256), &full[s]);
+          const int b = lane - 16;
+          if (b >= 0 && b < 8 && (rem & (1 << b))) {
+            const int32_t r0 = big * 256 + (rem >> (b + 1) << (b + 1));
+            tma_load_2d(st + (size_t)r0 * kw * 4, &maps.m[b], c0, (int32_t)(g0 + r0), &full[s]);
+          }
+        } else {
+          for (int r = lane; r < n; r += 32)
+            bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
+        }
+      }
+      if (j == 0 && lane == 0) BSPMM_TRACE(p, 10);
       if (!VEC) {
         float* dst = reinterpret_cast<float*>(st);
         const int32_t total = n * kw;
@@ -260,17 +262,26 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
           cp_async4(dst + q, bsrc + (int64_t)r * p.ldb + c);
         }
       }
-      // head / tail (or everything when the bases are not 16-byte aligned)
-      for (int32_t e = lane; e < a_col; e += 32) {
-        cp_async4(dcol + e, p.col + nz0 + e);
-        cp_async4(dval + e, p.vals + nz0 + e);
+      if (p.sbulk) {  // <= 3 head and <= 3 tail elements per array, on lanes not issuing TMA
+        if (lane >= 24 && lane < 27 && lane - 24 < a_col) {
+          cp_async4(dcol + (lane - 24), p.col + nz0 + (lane - 24));
+          cp_async4(dval + (lane - 24), p.vals + nz0 + (lane - 24));
+        }
+        if (lane >= 27 && lane < 30 && b_col + (lane - 27) < nnz) {
+          cp_async4(dcol + b_col + (lane - 27), p.col + nz0 + b_col + (lane - 27));
+          cp_async4(dval + b_col + (lane - 27), p.vals + nz0 + b_col + (lane - 27));
+        }
+        if (lane == 30)
+          for (int32_t r = 0; r < a_rp; ++r) cp_async4(drp + r, p.row_ptr + r_lo + r);
+        if (lane == 31)
+          for (int32_t r = b_rp; r < r_cnt; ++r) cp_async4(drp + r, p.row_ptr + r_lo + r);
+      } else {  // unaligned bases: the whole slice by 4-byte copies
+        for (int32_t e = lane; e < nnz; e += 32) {
+          cp_async4(dcol + e, p.col + nz0 + e);
+          cp_async4(dval + e, p.vals + nz0 + e);
+        }
+        for (int32_t r = lane; r < r_cnt; r += 32) cp_async4(drp + r, p.row_ptr + r_lo + r);
       }
-      for (int32_t e = b_col + lane; e < nnz; e += 32) {
-        cp_async4(dcol + e, p.col + nz0 + e);
-        cp_async4(dval + e, p.vals + nz0 + e);
-      }
-      for (int32_t r = lane; r < a_rp; r += 32) cp_async4(drp + r, p.row_ptr + r_lo + r);
-      for (int32_t r = b_rp + lane; r < r_cnt; r += 32) cp_async4(drp + r, p.row_ptr + r_lo + r);
     }
     if (lane == 0) {
       UnitHdr h;
@@ -279,7 +290,9 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
       hdr[s] = h;
       mbar_arrive(&full[s]);  // release: header visible to consumers
     }
+    if (j < 2 && lane == 0) BSPMM_TRACE(p, 11 + j);
     cp_async_arrive_noinc(&full[s]);  // 32 arrivals, each after its lane's copies land
+    if (j < 2 && lane == 0) BSPMM_TRACE(p, 13 + j);
   }
   if (lane == 0) BSPMM_TRACE(p, 4);
 }

@@ -18,7 +18,8 @@ import paper_1903_11409_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 
 SLOTS = ["entry", "after_pdl_wait", "prod_rowoff", "prod_struct_off", "prod_done", "cons_first_full",
-         "cons_done", "exit", "cons_unit0_done"]
+         "cons_done", "exit", "cons_unit0_done", "p0_after_empty", "p0_after_tma", "p0_before_arrive",
+         "p1_before_arrive", "p0_after_arrive", "p1_after_arrive"]
 
 
 def main():
