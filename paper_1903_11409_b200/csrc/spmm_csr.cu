@@ -224,17 +224,19 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
       // by its own lane: on a cold start every issue stalls its thread ~0.1 us
       // (measured with tools/trace.py), so serial issue from one lane cost
       // ~1 us per unit; spread over lanes the stalls overlap
-      if (lane == 0) {
-        uint32_t tx = 2u * 4u * (uint32_t)(b_col - a_col) + 4u * (uint32_t)(b_rp - a_rp);
-        if (b_bulk) tx += (uint32_t)n * (uint32_t)kw * 4u;
-        if (tx) mbar_expect_tx(&full[s], tx);
-      }
+      if (lane == 0 && b_bulk) mbar_expect_tx(&full[s], (uint32_t)n * (uint32_t)kw * 4u);
       __syncwarp();
-      if (b_col > a_col) {
-        if (lane == 0) bulk_g2s(dcol + a_col, p.col + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
-        if (lane == 1) bulk_g2s(dval + a_col, p.vals + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+      // the CSR slice's 16-byte-aligned interior by 16-byte cp.async (LSU path):
+      // the SM's TMA front-end accepts copies one at a time on a cold start, so
+      // TMA is kept for the B tile only
+      if (p.sbulk) {
+        const int32_t ncol4 = (b_col - a_col) >> 2, nrp4 = (b_rp - a_rp) >> 2;
+        for (int32_t q = lane; q < ncol4; q += 32) {
+          cp_async16(dcol + a_col + 4 * q, p.col + nz0 + a_col + 4 * q);
+          cp_async16(dval + a_col + 4 * q, p.vals + nz0 + a_col + 4 * q);
+        }
+        for (int32_t q = lane; q < nrp4; q += 32) cp_async16(drp + a_rp + 4 * q, p.row_ptr + r_lo + a_rp + 4 * q);
       }
-      if (lane == 2 && b_rp > a_rp) bulk_g2s(drp + a_rp, p.row_ptr + r_lo + a_rp, 4u * (uint32_t)(b_rp - a_rp), &full[s]);
       if (b_bulk) {  // TMA: whole contiguous B_i (1-D), a full k-tile (2-D boxes), else one bulk copy per row
         if (kw == p.ldb) {
           if (lane == 3) bulk_g2s_hint(st, bsrc, (uint32_t)n * (uint32_t)kw * 4u, &full[s], pol);
