@@ -50,6 +50,7 @@ struct SpmmParams {
   int32_t tma2d;              // 1: full k-tiles staged with 2-D tensor TMA (maps valid)
   int32_t sbulk;              // 1: col / vals / row_ptr bases are 16-byte aligned (bulk-copy the CSR slice)
   int32_t prefetch;           // 1: L2-prefetch every unit of a batch up front (small problems)
+  int32_t slice_lsu;          // 1: CSR slice by 16-byte cp.async instead of TMA bulk (small problems)
 };
 
 // Stage layout of a unit's CSR slice, after the B tile: three int32 arrays
@@ -224,12 +225,25 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
       // by its own lane: on a cold start every issue stalls its thread ~0.1 us
       // (measured with tools/trace.py), so serial issue from one lane cost
       // ~1 us per unit; spread over lanes the stalls overlap
-      if (lane == 0 && b_bulk) mbar_expect_tx(&full[s], (uint32_t)n * (uint32_t)kw * 4u);
+      // the CSR slice's 16-byte-aligned interior: TMA bulk copies for streaming
+      // batches (fewest instructions), 16-byte cp.async (LSU path) for small
+      // latency-bound batches, where the SM's TMA front-end accepting copies one
+      // at a time on a cold start is on the critical path (tools/trace.py)
+      const bool slice_tma = p.sbulk && !p.slice_lsu;
+      if (lane == 0) {
+        uint32_t tx = b_bulk ? (uint32_t)n * (uint32_t)kw * 4u : 0u;
+        if (slice_tma) tx += 2u * 4u * (uint32_t)(b_col - a_col) + 4u * (uint32_t)(b_rp - a_rp);
+        if (tx) mbar_expect_tx(&full[s], tx);
+      }
       __syncwarp();
-      // the CSR slice's 16-byte-aligned interior by 16-byte cp.async (LSU path):
-      // the SM's TMA front-end accepts copies one at a time on a cold start, so
-      // TMA is kept for the B tile only
-      if (p.sbulk) {
+      if (slice_tma) {
+        if (b_col > a_col) {
+          if (lane == 0) bulk_g2s(dcol + a_col, p.col + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+          if (lane == 1) bulk_g2s(dval + a_col, p.vals + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+        }
+        if (lane == 2 && b_rp > a_rp)
+          bulk_g2s(drp + a_rp, p.row_ptr + r_lo + a_rp, 4u * (uint32_t)(b_rp - a_rp), &full[s]);
+      } else if (p.sbulk) {
         const int32_t ncol4 = (b_col - a_col) >> 2, nrp4 = (b_rp - a_rp) >> 2;
         for (int32_t q = lane; q < ncol4; q += 32) {
           cp_async16(dcol + a_col + 4 * q, p.col + nz0 + a_col + 4 * q);
@@ -641,6 +655,7 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   // the prefetched bytes then never exceed the problem (small, L2-resident)
   // (measured: no gain on C3/C4, so off unless requested with debug bit 16)
   sp.prefetch = (plan.units <= 32LL * plan.grid && (a.dbg & 16)) ? 1 : 0;
+  sp.slice_lsu = (plan.units <= 32LL * plan.grid) ? 1 : 0;  // C4: 8.4 vs 9.0 us; C5 (TMA): 835 vs 849 us
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
