@@ -133,7 +133,8 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
 /* Debug: timing-experiment bits for subsequent SpMM launches.  1 = compute but
  * do not store C (the result is then undefined); 2 = compute every unit from
  * global memory (no staging); 8 = consumers repeat each unit's work 4 times;
- * 16 = L2-prefetch every unit of small problems up front.  0 (default) = normal. */
+ * 16 = L2-prefetch every unit of small problems up front; 32 = always copy
+ * the CSR slice with TMA.  0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */

@@ -655,7 +655,7 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   // the prefetched bytes then never exceed the problem (small, L2-resident)
   // (measured: no gain on C3/C4, so off unless requested with debug bit 16)
   sp.prefetch = (plan.units <= 32LL * plan.grid && (a.dbg & 16)) ? 1 : 0;
-  sp.slice_lsu = (plan.units <= 32LL * plan.grid) ? 1 : 0;  // C4: 8.4 vs 9.0 us; C5 (TMA): 835 vs 849 us
+  sp.slice_lsu = (plan.units <= 32LL * plan.grid && !(a.dbg & 32)) ? 1 : 0;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {

@@ -22,6 +22,8 @@ def main():
     dev = torch.device("cuda", 0)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     h = bs.Handle(0)
+    if len(sys.argv) > 1:
+        h.set_debug(int(sys.argv[1]))
     for cid in (1, 2, 3):
         b = synth.config(cid, coo=True)
         h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
@@ -34,6 +36,10 @@ def main():
         torch.cuda.synchronize()
         assert torch.equal(C, C2)
     # direct path (tiny stage capacity) and scalar path (k % 4 != 0)
+    if len(sys.argv) > 1:  # the TMA-only variant: C1-C3 vectorised paths only
+        h.sync()
+        print("sanitize workload ok")
+        return
     b = synth.generate(synth.MIX, (100, 300, 1, 5), 6, 7, seed=3)
     h.set_hints(16, 64)
     h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
