@@ -11,7 +11,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
              -ftz=false -prec-div=true -prec-sqrt=true -Iinclude -Xptxas -v
 LIB       := $(PKG)/libbspmm.so
-CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu $(CSRC)/backward.cu
+CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu $(CSRC)/backward.cu $(CSRC)/spmm_coo_atomic.cu
 HOST_SRCS := $(CSRC)/partition.cpp $(CSRC)/plan.cpp
 HDRS      := include/bspmm.h $(CSRC)/internal.h $(CSRC)/ptx.cuh
 

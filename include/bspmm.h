@@ -185,6 +185,20 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
                                    int64_t total_rows, int64_t total_nnz, int32_t* csr_row_ptr_out,
                                    int32_t* csr_col_out, float* csr_val_out);
 
+/* The paper's own SWA SpMM for SparseTensor (Fig.
+ * algo:code_swa_spmm_st, output tile in shared memory per Fig.
+ * batched_spmm_algo (a)/(b)): one thread block per (matrix, column block), a
+ * sub-warp per nonzero, atomic accumulation into the shared C tile; matrices
+ * above the tile capacity accumulate with global atomics (case 3,
+ * PAPER.md:249-252).  Same arguments and result as bspmm_coo (C overwritten)
+ * but the summation order is NOT deterministic (results agree within the
+ * north_star bound, not bitwise).  Requires k, ldb, ldc % 4 == 0 and 16-byte
+ * aligned B, C (else BSPMM_ERROR_NOT_SUPPORTED).  Planner hint max_rows sizes
+ * the shared tile. */
+BSPMM_API bspmm_status_t bspmm_coo_atomic(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                          const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
+                                          const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc);
+
 /* COO -> CSR alone (hot-path row a-2; exported for the bit-exact tests).
  * Output order per matrix: by (row, col, original position); row_ptr holds
  * absolute positions (nnz_off[i] + local); padding rows between matrices get

@@ -179,6 +179,24 @@ class Handle:
         self._raise(st, "bspmm_coo")
         return C
 
+    def coo_atomic(self, row_off: Optional[torch.Tensor], sizes: Optional[torch.Tensor], nnz_off: torch.Tensor,
+                   idx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None,
+                   k: Optional[int] = None) -> torch.Tensor:
+        """The paper's atomic SWA SpMM for SparseTensor (bspmm_coo_atomic): nondeterministic order."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("nnz_off", nnz_off, torch.int64), ("idx", idx, torch.int32),
+                            ("vals", vals, torch.float32), ("B", B, torch.float32), ("C", C, torch.float32)):
+            _check(t, name, dt, dev)
+        k = B.shape[1] if k is None else k
+        if C is None:
+            C = torch.empty((B.shape[0], k), dtype=torch.float32, device=dev)
+        self._stream()
+        st = lib.bspmm_coo_atomic(self._h, nnz_off.shape[0] - 1, k, _ptr(row_off), _ptr(sizes), _ptr(nnz_off),
+                                  _ptr(idx), _ptr(vals), _ptr(B), _ld(B, k, "B"), _ptr(C), _ld(C, k, "C"))
+        self._raise(st, "bspmm_coo_atomic")
+        return C
+
     def coo2csr(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], nnz_off: torch.Tensor,
                 idx: torch.Tensor, vals: torch.Tensor, total_rows: int):
         """Row a-2 alone: canonical CSR (row_ptr, col, vals) built on the device."""

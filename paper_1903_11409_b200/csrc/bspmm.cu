@@ -445,6 +445,40 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
   return csr_impl(h, batch, k, ro, sizes, rp, col, val, B, ldb, C, ldc, false);
 }
 
+// ---- the paper's atomic SWA SpMM for SparseTensor (NEXT-3) -----------------
+BSPMM_API bspmm_status_t bspmm_coo_atomic(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                          const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
+                                          const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || k < 1 || ldb < k || ldc < k) return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1 or ld<k");
+  if (batch == 0) return BSPMM_SUCCESS;
+  if ((!row_off && !sizes) || !nnz_off) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  if (B && B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
+  if (!(k % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && aligned16(B) && aligned16(C)))
+    return fail(h, BSPMM_ERROR_NOT_SUPPORTED, "bspmm_coo_atomic needs k, ldb, ldc % 4 == 0 and 16-byte aligned B, C");
+  DeviceGuard g(h->device);
+  const int64_t* ro = row_off;
+  if (!ro) {
+    bspmm_status_t st = grow(h, &h->ws, &h->ws_bytes, al256((size_t)(batch + 1) * 8));
+    if (st != BSPMM_SUCCESS) return st;
+    int64_t* w = static_cast<int64_t*>(h->ws);
+    st = bspmm_build_offsets(h, batch, sizes, w);
+    if (st != BSPMM_SUCCESS) return st;
+    ro = w;
+  }
+  if (h->flags & BSPMM_VALIDATE) {
+    CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
+    CK(h, launch_validate_coo(batch, ro, sizes, nnz_off, idx, h->dev_flag, h->stream));
+    h->launches++;
+    bspmm_status_t st = check_validate_flag(h);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  CK(h, launch_spmm_coo_atomic(batch, k, ro, sizes, nnz_off, idx, vals, B, ldb, C, ldc, h->hint_rows, h->smem_optin,
+                               h->stream));
+  h->launches++;
+  return BSPMM_SUCCESS;
+}
+
 // ---- backward (NEXT-2) ------------------------------------------------------
 // workspace: [idx 2*NNZ i32][nnz_off (batch+1) i64][keys 2*NNZ u64][pay 2*NNZ u32]
 //            [+ rowT (N+1) i32, colT NNZ i32, valsT NNZ f32 when the transpose is internal]

@@ -80,6 +80,10 @@ cudaError_t launch_coo2csr(int32_t batch, const int64_t* row_off, const int32_t*
                            int32_t* col_out, float* val_out, uint64_t* ws_keys, uint32_t* ws_pay,
                            int64_t ws_stride, int32_t smem_cap, cudaStream_t s);
 int32_t coo_smem_cap(int64_t max_nnz_hint, int32_t smem_optin);
+cudaError_t launch_spmm_coo_atomic(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
+                                   const int64_t* nnz_off, const int32_t* idx, const float* vals, const float* B,
+                                   int64_t ldb, float* C, int64_t ldc, int32_t max_rows, int32_t smem_optin,
+                                   cudaStream_t s);
 cudaError_t launch_transpose_expand(int32_t batch, const int64_t* row_off, const int32_t* sizes,
                                     const int32_t* row_ptr, const int32_t* col, int32_t* idx, int64_t* nnz_off,
                                     cudaStream_t s);

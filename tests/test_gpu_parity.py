@@ -334,3 +334,29 @@ def test_c5_full_size_sampled(h):
     assert oracle.check_bound(C[b.row_off[mats] + rl], ref, bound)[0]
     # property at any size: every row written (no NaN left), empty rows exact zero
     assert not np.isnan(C).any()
+
+
+# ------------------------------------------------------------ NEXT-3: the paper's atomic SWA-ST kernel
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_coo_atomic_within_bound(h, cid):
+    b = synth.config(cid, coo=True)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    C = h.coo_atomic(T(b.row_off), None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B)).cpu().numpy()
+    Cref, bound = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+    ok, worst = oracle.check_bound(C, Cref, bound)
+    assert ok, worst
+
+
+def test_coo_atomic_edge_cases(h):
+    rng = np.random.default_rng(77)
+    for trial in range(6):
+        b = synth.random_batch(rng, 30, 64, nmax=50, dmax=6, duplicates=True)
+        h.set_hints(16 if trial % 2 else 0, 0)        # small hint: global-atomic case 3 for big matrices
+        Cd = torch.full((b.n_rows, 64), float("nan"), device=DEV)
+        C = h.coo_atomic(None, T(b.sizes), T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B), Cd).cpu().numpy()
+        Cref, bound = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+        assert oracle.check_bound(C, Cref, bound)[0], trial
+    with pytest.raises(bs.BspmmError, match="NOT_SUPPORTED"):
+        b = synth.random_batch(rng, 3, 5, nmax=5)
+        h.coo_atomic(T(b.row_off), None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B))
