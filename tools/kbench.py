@@ -24,14 +24,15 @@ L2 = 126 * 2 ** 20
 
 
 def setup(cid, dev):
-    b = synth.config(cid)
+    b = synth.config(cid, coo=True)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     per = alg_bytes(b.n_rows, b.n_nnz, b.k, b.batch)
     M = max(1, min(64, int(np.ceil(2 * L2 / per))))
     reps = []
     for _ in range(M):
         reps.append(dict(ro=T(b.row_off), rp=T(b.row_ptr), col=T(b.col), vals=T(b.vals), B=T(b.B),
-                         C=torch.empty((b.n_rows, b.k), device=dev), sizes=T(b.sizes)))
+                         C=torch.empty((b.n_rows, b.k), device=dev), sizes=T(b.sizes), no=T(b.nnz_off),
+                         idx=T(b.coo_idx), cv=T(b.coo_vals), N=b.n_rows))
     return b, reps, per
 
 
@@ -73,6 +74,14 @@ def spmm_only(h, r):
 def full_step(h, r):
     h.build_offsets(r["sizes"], out=r["ro"])
     h.csr(r["ro"], None, r["rp"], r["col"], r["vals"], r["B"], r["C"])
+
+
+def coo_convert_csr(h, r):  # deterministic COO path: device COO->CSR + the CSR kernel
+    h.coo(r["ro"], None, r["no"], r["idx"], r["cv"], r["B"], r["C"], total_rows=r["N"])
+
+
+def coo_atomic(h, r):  # the paper's atomic SWA-ST kernel
+    h.coo_atomic(r["ro"], None, r["no"], r["idx"], r["cv"], r["B"], r["C"])
 
 
 def offsets_only(h, r):
@@ -134,8 +143,12 @@ def main():
         ms_step = time_calls(h, reps, R, full_step)
         ms_off = time_calls(h, reps, R, offsets_only)
         ms_ng = time_calls(h, reps, min(R, 50), spmm_only, graph=False)
+        extra = {}
+        if b.k % 4 == 0 and cid != 5:
+            extra["coo_convert_csr_us"] = time_calls(h, reps, R, coo_convert_csr) * 1e3
+            extra["coo_atomic_us"] = time_calls(h, reps, R, coo_atomic) * 1e3
         print(json.dumps({"config": cid, "step_us": ms_step * 1e3, "offsets_us": ms_off * 1e3,
-                          "spmm_us_no_graph": ms_ng * 1e3, "alg_bytes": per}), flush=True)
+                          "spmm_us_no_graph": ms_ng * 1e3, "alg_bytes": per, **extra}), flush=True)
         del reps
         torch.cuda.empty_cache()
 
