@@ -37,8 +37,9 @@ def _load():
         lib.oracle_partition.argtypes = [I64, P, I32, I32, P]
         lib.oracle_csr_transpose.argtypes = [I64, P, P, P, P, P, P, P, P]
         lib.oracle_sddmm.argtypes = [I64, I32, P, P, P, P, P, I64, P, I64, P, P]
+        lib.oracle_gcn_layer.argtypes = [I64, I32, I32, I32, P, P, P, P, P, I64, P, P, P, I64, P]
         for f in (lib.oracle_offsets, lib.oracle_coo2csr, lib.oracle_spmm, lib.oracle_spmm_f32,
-                  lib.oracle_spmm_rows, lib.oracle_partition, lib.oracle_csr_transpose, lib.oracle_sddmm):
+                  lib.oracle_spmm_rows, lib.oracle_partition, lib.oracle_csr_transpose, lib.oracle_sddmm, lib.oracle_gcn_layer):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -185,3 +186,20 @@ def backward(k, row_off, row_ptr, col, vals, B, grad_C):
     gB, gB_bound = spmm(k, row_off, None, rt, ct, vt, grad_C)
     gv, gv_bound = sddmm(k, row_off, None, row_ptr, col, B, grad_C)
     return gB, gB_bound, gv, gv_bound
+
+
+def gcn_layer(row_off, row_ptrs, col, vals, X, W, bias):
+    """O7: Y = sum_ch A_ch (X W_ch + 1 bias_ch^T) in fp64 -> fp32, and the magnitude
+    sum M = sum_ch sum_e |a| (sum_l |x||w| + |b|).  row_ptrs: [channels, N+1]."""
+    row_off = _c(row_off, np.int64)
+    rp = _c(row_ptrs, np.int32)
+    channels = rp.shape[0]
+    col, vals, X = _c(col, np.int32), _c(vals, np.float32), _c(X, np.float32)
+    W, bias = _c(W, np.float32), _c(bias, np.float32)
+    n_x, k = W.shape[1], W.shape[2]
+    N = int(row_off[-1])
+    Y = np.zeros((N, k), dtype=np.float32)
+    mag = np.zeros((N, k), dtype=np.float64)
+    assert _load().oracle_gcn_layer(row_off.shape[0] - 1, channels, n_x, k, _p(row_off), _p(rp), _p(col), _p(vals),
+                                    _p(X), X.shape[1], _p(W), _p(bias), _p(Y), k, _p(mag)) == 0
+    return Y, mag

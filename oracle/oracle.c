@@ -32,6 +32,9 @@
  *   O6 oracle_sddmm        grad_vals[e] = <grad_C[row_e], B[col_e]> in fp64
  *                          with bound 1e-5 * sum |d||b| (adjoint of C = A B,
  *                          SPEC.md:178-186).
+ *   O7 oracle_gcn_layer    Y = sum_ch A_ch (X W_ch + 1 bias_ch^T) (PAPER.md Fig.
+ *                          algo:graph_conv_batched, Eq. (2)), fp64, with the
+ *                          magnitude sum that scales its tolerance.
  *
  * Pins (tests/test_oracle_pins.py): dense brute force A@B (numpy fp64) on
  * >=1000 tiny batches, identity -> C == B, SPEC.md:140 example, zero rows,
@@ -259,6 +262,59 @@ int oracle_sddmm(int64_t batch, int32_t k, const int64_t* row_off, const int32_t
         if (bound) bound[e] = 1e-5 * s;
       }
     }
+  }
+  return 0;
+}
+
+/* ---- fused GCN layer (NEXT-1): PAPER.md Fig. algo:graph_conv_batched
+ * (:304-321) and Eq. (2) (:66-68): for every channel ch,
+ *   U_ch = X W_ch,  B_ch = U_ch + 1 bias_ch^T,  C_ch = A_ch B_ch;  Y = sum_ch C_ch.
+ * X [N x n_x] (ldx), W [channels][n_x][k] dense, bias [channels][k]; one
+ * block-diagonal CSR per channel: row_ptr [channels][N+1] (absolute positions
+ * into col / vals), LOCAL column ids.  fp64 throughout, one rounding at the
+ * end; mag[g][c] = sum_ch sum_e |a_e| (sum_l |x_{j l}| |w_{l c}| + |b_c|). */
+int oracle_gcn_layer(int64_t batch, int32_t channels, int32_t n_x, int32_t k, const int64_t* row_off,
+                     const int32_t* row_ptr, const int32_t* col, const float* vals, const float* X,
+                     int64_t ldx, const float* W, const float* bias, float* Y, int64_t ldy, double* mag) {
+  if (batch < 0 || channels < 1 || n_x < 0 || k < 1) return 1;
+  const int64_t N = row_off[batch];
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t i = 0; i < batch; ++i) {
+    const int64_t n = row_off[i + 1] - row_off[i];
+    double* acc = (double*)malloc(sizeof(double) * (size_t)k * 2);
+    double* u = (double*)malloc(sizeof(double) * (size_t)k * 2);
+    for (int64_t r = 0; r < n; ++r) {
+      const int64_t g = row_off[i] + r;
+      for (int32_t c = 0; c < k; ++c) acc[c] = 0.0, acc[k + c] = 0.0;
+      for (int32_t ch = 0; ch < channels; ++ch) {
+        const int32_t* rp = row_ptr + (int64_t)ch * (N + 1);
+        const float* Wc = W + (int64_t)ch * n_x * k;
+        const float* bc = bias + (int64_t)ch * k;
+        for (int64_t e = rp[g]; e < rp[g + 1]; ++e) {
+          const int64_t j = row_off[i] + col[e];  /* neighbour's global row */
+          const double a = (double)vals[e];
+          for (int32_t c = 0; c < k; ++c) {      /* u = X[j] W_ch + bias_ch */
+            double s = 0.0, sm = 0.0;
+            for (int32_t l = 0; l < n_x; ++l) {
+              s += (double)X[j * ldx + l] * (double)Wc[(int64_t)l * k + c];
+              sm += fabs((double)X[j * ldx + l]) * fabs((double)Wc[(int64_t)l * k + c]);
+            }
+            u[c] = s + (double)bc[c];
+            u[k + c] = sm + fabs((double)bc[c]);
+          }
+          for (int32_t c = 0; c < k; ++c) {
+            acc[c] += a * u[c];
+            acc[k + c] += fabs(a) * u[k + c];
+          }
+        }
+      }
+      for (int32_t c = 0; c < k; ++c) {
+        Y[g * ldy + c] = (float)acc[c];
+        if (mag) mag[g * ldy + c] = acc[k + c];
+      }
+    }
+    free(acc);
+    free(u);
   }
   return 0;
 }

@@ -402,3 +402,65 @@ def test_backward_golden(golden):
     b = synth.config(1)
     gB, _, gv, _ = oracle.backward(b.k, b.row_off, b.row_ptr, b.col, b.vals, b.B, np.zeros_like(b.B))
     assert not gB.any() and not gv.any()
+
+
+# ---------------------------------------------------------------- O7 (fused GCN layer, NEXT-1)
+
+def gcn_inputs(rng, channels=2, n_x=5, k=4, batch=3):
+    """Per-channel adjacency patterns over the same graphs (bond-type channels)."""
+    base = synth.random_batch(rng, batch, k, nmax=7, dmax=3, allow_empty_graphs=False)
+    N = base.n_rows
+    rps, cols, vals = [], [], []
+    z = 0
+    for ch in range(channels):
+        rp = np.zeros(N + 1, np.int32)
+        cl, vl = [], []
+        for i in range(batch):
+            n = int(base.sizes[i])
+            for r in range(n):
+                g = int(base.row_off[i]) + r
+                rp[g] = z
+                d = int(rng.integers(0, min(3, n) + 1))
+                cs = sorted(rng.choice(n, size=d, replace=False).tolist())
+                cl += cs
+                vl += list(rng.standard_normal(d))
+                z += d
+        rp[N] = z
+        rps.append(rp)
+        cols += cl
+        vals += vl
+    X = rng.standard_normal((N, n_x)).astype(np.float32)
+    W = rng.standard_normal((channels, n_x, k)).astype(np.float32)
+    bias = rng.standard_normal((channels, k)).astype(np.float32)
+    return base, np.stack(rps), np.array(cols, np.int32), np.array(vals, np.float32), X, W, bias
+
+
+def test_gcn_layer_dense_brute_force():
+    rng = np.random.default_rng(15)
+    for trial in range(40):
+        base, rps, col, vals, X, W, bias = gcn_inputs(rng, channels=int(rng.integers(1, 4)))
+        Y, mag = oracle.gcn_layer(base.row_off, rps, col, vals, X, W, bias)
+        ref = np.zeros_like(Y, dtype=np.float64)
+        for ch in range(rps.shape[0]):
+            U = X.astype(np.float64) @ W[ch].astype(np.float64) + bias[ch].astype(np.float64)   # library matmul
+            for i in range(base.batch):
+                g0, g1 = int(base.row_off[i]), int(base.row_off[i + 1])
+                A = np.zeros((g1 - g0, g1 - g0))
+                for r in range(g1 - g0):
+                    for e in range(rps[ch][g0 + r], rps[ch][g0 + r + 1]):
+                        A[r, col[e]] += vals[e]
+                ref[g0:g1] += A @ U[g0:g1]
+        assert np.all(np.abs(Y - ref) <= 1e-6 * mag + 1e-30), trial
+
+
+def test_gcn_layer_special_cases():
+    rng = np.random.default_rng(16)
+    base, rps, col, vals, X, W, bias = gcn_inputs(rng, channels=1, n_x=4, k=4)
+    # W = I, bias = 0: the layer is the plain SpMM of A with X (closed form)
+    Y, _ = oracle.gcn_layer(base.row_off, rps, col, vals, X, np.eye(4, dtype=np.float32)[None], np.zeros((1, 4), np.float32))
+    C, _ = oracle.spmm(4, base.row_off, None, rps[0], col, vals, X)
+    assert np.array_equal(Y, C)
+    # W = 0: Y = rowsum(A) (x) bias
+    Y, _ = oracle.gcn_layer(base.row_off, rps, col, vals, X, np.zeros((1, 4, 4), np.float32), bias[:1])
+    rs = np.array([vals[rps[0][g]:rps[0][g + 1]].astype(np.float64).sum() for g in range(base.n_rows)])
+    assert np.allclose(Y, rs[:, None] * bias[0][None, :].astype(np.float64), rtol=1e-6, atol=1e-6)
