@@ -21,7 +21,8 @@ lib: $(LIB)
 
 $(LIB): $(CU_SRCS) $(HOST_SRCS) $(HDRS)
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) $(HOST_SRCS) 2> build/ptxas.log || (cat build/ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) $(HOST_SRCS) -lcublas -Xlinker -rpath=/usr/local/cuda/lib64 \
+	  2> build/ptxas.log || (cat build/ptxas.log; false)
 	@grep -E "registers|spill|smem" build/ptxas.log | sed 's/^ptxas info *: //' > build/ptxas_summary.txt || true
 
 oracle: oracle/liboracle.so

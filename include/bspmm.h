@@ -185,6 +185,24 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
                                    int64_t total_rows, int64_t total_nnz, int32_t* csr_row_ptr_out,
                                    int32_t* csr_col_out, float* csr_val_out);
 
+/* Fused batched graph-convolution layer (PAPER.md Fig. algo:graph_conv_batched,
+ * :304-321; Eq. (2) :66-68):  Y = sum_ch A_ch (X W_ch + 1 bias_ch^T).
+ *  X      [total_rows x ldx] dev fp32 (node features, stacked graphs; n_x used)
+ *  W      [channels][n_x][k] dev fp32, dense contiguous
+ *  bias   [channels][k] dev fp32, nullable (= 0)
+ *  row_ptr [channels][total_rows + 1] dev int32: one block-diagonal CSR per
+ *         channel (channel-specific adjacency), absolute positions into the
+ *         shared col / vals arrays; col LOCAL ids.
+ *  Y      [total_rows x ldy] dev fp32 (overwritten).
+ * One GEMM for all channels (cuBLAS, fp32-accurate) into handle workspace
+ * (total_rows x channels x k floats), then one SpMM per channel with the bias
+ * (as rowsum(A) * bias) and the channel sum fused into its epilogue. */
+BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_t channels, int32_t n_x, int32_t k,
+                                         const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
+                                         const int32_t* col, const float* vals, const float* X, int64_t ldx,
+                                         const float* W, const float* bias, float* Y, int64_t ldy,
+                                         int64_t total_rows);
+
 /* The paper's own SWA SpMM for SparseTensor (Fig.
  * algo:code_swa_spmm_st, output tile in shared memory per Fig.
  * batched_spmm_algo (a)/(b)): one thread block per (matrix, column block), a

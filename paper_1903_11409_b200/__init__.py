@@ -215,6 +215,30 @@ class Handle:
         self._raise(st, "bspmm_coo2csr")
         return rp, col, v
 
+    # ---- fused GCN layer (NEXT-1) -------------------------------------------------
+    def gcn_layer(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], row_ptrs: torch.Tensor,
+                  col: torch.Tensor, vals: torch.Tensor, X: torch.Tensor, W: torch.Tensor,
+                  bias: Optional[torch.Tensor] = None, Y: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Y = sum_ch A_ch (X W_ch + 1 bias_ch^T) (bspmm_gcn_layer).  row_ptrs: int32 [channels, N+1];
+        W: [channels, n_x, k]; bias: [channels, k]."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("row_ptrs", row_ptrs, torch.int32), ("col", col, torch.int32),
+                            ("vals", vals, torch.float32), ("X", X, torch.float32), ("W", W, torch.float32),
+                            ("bias", bias, torch.float32), ("Y", Y, torch.float32)):
+            _check(t, name, dt, dev)
+        channels, n_x, k = W.shape
+        N = X.shape[0]
+        assert row_ptrs.shape == (channels, N + 1) and W.is_contiguous() and row_ptrs.is_contiguous()
+        if Y is None:
+            Y = torch.empty((N, k), dtype=torch.float32, device=dev)
+        self._stream()
+        st = lib.bspmm_gcn_layer(self._h, row_off.shape[0] - 1, channels, n_x, k, _ptr(row_off), _ptr(sizes),
+                                 _ptr(row_ptrs), _ptr(col), _ptr(vals), _ptr(X), _ld(X, n_x, "X"), _ptr(W),
+                                 _ptr(bias), _ptr(Y), _ld(Y, k, "Y"), N)
+        self._raise(st, "bspmm_gcn_layer")
+        return Y
+
     # ---- backward (NEXT-2) ---------------------------------------------------------
     def csr_transpose(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], row_ptr: torch.Tensor,
                       col: torch.Tensor, vals: torch.Tensor):

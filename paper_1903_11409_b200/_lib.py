@@ -38,6 +38,7 @@ _SIGS = {
     "bspmm_coo": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64, I64, I64, P, P, P]),
     "bspmm_coo2csr": (I32, [P, I32, P, P, P, P, P, I64, I64, P, P, P]),
     "bspmm_coo_atomic": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
+    "bspmm_gcn_layer": (I32, [P, I32, I32, I32, I32, P, P, P, P, P, P, I64, P, P, P, I64, I64]),
     "bspmm_build_offsets": (I32, [P, I32, P, P]),
     "bspmm_csr_host": (I32, [P, I32, I32, P, P, P, P, P, P, I64, I64]),
     "bspmm_csr_transpose": (I32, [P, I32, P, P, P, P, P, I64, I64, P, P, P]),

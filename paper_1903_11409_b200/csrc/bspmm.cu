@@ -8,6 +8,7 @@
 #include <new>
 #include <string>
 
+#include <cublas_v2.h>
 #include <cudaTypedefs.h>
 
 #include "internal.h"
@@ -213,6 +214,8 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (h->hbuf) cudaFree(h->hbuf);
     if (h->dev_flag) cudaFree(h->dev_flag);
     if (h->scan_ws) cudaFree(h->scan_ws);
+    if (h->gcn_ws) cudaFree(h->gcn_ws);
+    if (h->cublas) cublasDestroy(static_cast<cublasHandle_t>(h->cublas));
   }
   delete h;
   return st;
@@ -298,7 +301,7 @@ BSPMM_API bspmm_status_t bspmm_build_offsets(bspmm_handle_t h, int32_t batch, co
 static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
                                const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
                                const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc,
-                               bool validate) {
+                               bool validate, const float* bias = nullptr, int32_t accumulate = 0) {
   if (validate) {
     CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
     CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr, col_idx, h->dev_flag, h->stream));
@@ -311,7 +314,7 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   bspmm_status_t st = plan_for(h, batch, k, aligned, &plan);
   if (st != BSPMM_SUCCESS) return st;
   const TmaMaps* maps = plan.vec ? tma_maps(h, B, k, ldb, plan.kt) : nullptr;
-  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps};
+  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias, accumulate};
   CK(h, launch_spmm_csr(a, plan, h->stream));
   if (plan.units > 0) h->launches++;
   return BSPMM_SUCCESS;
@@ -443,6 +446,55 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
   if (st != BSPMM_SUCCESS) return st;
   // indices were validated on the COO side; the built CSR is consistent by construction
   return csr_impl(h, batch, k, ro, sizes, rp, col, val, B, ldb, C, ldc, false);
+}
+
+// ---- fused batched GCN layer (NEXT-1) ----------------------------------------
+// PAPER.md Fig. algo:graph_conv_batched: for ch: U = X W[ch]; B = U + bias[ch];
+// C[ch] = BatchedSpMM(A[ch], B); Y = sum_ch C[ch].  Here: ONE strided-batched
+// GEMM computes U for every channel (cuBLAS, fp32-accurate BF16x9 tensor-core
+// emulation when available, else plain fp32), then ONE SpMM launch per channel
+// folds the bias (A (U + 1 b^T) = A U + rowsum(A) b^T) and the channel sum
+// into its epilogue: channels + 1 launches instead of the paper's 3 x channels.
+BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_t channels, int32_t n_x, int32_t k,
+                                         const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
+                                         const int32_t* col, const float* vals, const float* X, int64_t ldx,
+                                         const float* W, const float* bias, float* Y, int64_t ldy,
+                                         int64_t total_rows) {
+  if (!h) return BSPMM_ERROR_INVALID_VALUE;
+  if (batch < 0 || channels < 1 || n_x < 1 || k < 1 || ldx < n_x || ldy < k || total_rows < 0)
+    return fail(h, BSPMM_ERROR_INVALID_VALUE, "bad batch / channels / sizes / leading dimensions");
+  if (batch == 0 || total_rows == 0) return BSPMM_SUCCESS;
+  if (!row_off || !row_ptr || !X || !W || !Y) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  DeviceGuard g(h->device);
+  const int64_t N = total_rows, ldu = (int64_t)channels * k;
+  bspmm_status_t st = grow(h, &h->gcn_ws, &h->gcn_ws_bytes, al256((size_t)N * ldu * 4));
+  if (st != BSPMM_SUCCESS) return st;
+  float* U = static_cast<float*>(h->gcn_ws);
+  if (!h->cublas) {
+    cublasHandle_t cb;
+    if (cublasCreate(&cb) != CUBLAS_STATUS_SUCCESS) return fail(h, BSPMM_ERROR_CUDA, "cublasCreate failed");
+    h->cublas = cb;
+  }
+  cublasHandle_t cb = static_cast<cublasHandle_t>(h->cublas);
+  cublasSetStream(cb, h->stream);
+  // column-major view: U_ch^T (k x N, ld channels*k) = W_ch^T (k x n_x, ld k) * X^T (n_x x N, ld ldx)
+  const float one = 1.f, zero = 0.f;
+  cublasStatus_t cs = cublasGemmStridedBatchedEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, W, CUDA_R_32F, k,
+                                                 (long long)n_x * k, X, CUDA_R_32F, (int)ldx, 0, &zero, U, CUDA_R_32F,
+                                                 (int)ldu, k, channels, CUBLAS_COMPUTE_32F_EMULATED_16BFX9,
+                                                 CUBLAS_GEMM_DEFAULT);
+  if (cs != CUBLAS_STATUS_SUCCESS)  // emulation unavailable in the loaded cuBLAS: plain fp32
+    cs = cublasGemmStridedBatchedEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, W, CUDA_R_32F, k,
+                                    (long long)n_x * k, X, CUDA_R_32F, (int)ldx, 0, &zero, U, CUDA_R_32F, (int)ldu,
+                                    k, channels, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+  if (cs != CUBLAS_STATUS_SUCCESS) return fail(h, BSPMM_ERROR_CUDA, "cuBLAS GEMM failed");
+  h->launches++;
+  for (int32_t ch = 0; ch < channels; ++ch) {
+    st = csr_impl(h, batch, k, row_off, sizes, row_ptr + (int64_t)ch * (N + 1), col, vals, U + (int64_t)ch * k, ldu,
+                  Y, ldy, (h->flags & BSPMM_VALIDATE) != 0, bias ? bias + (int64_t)ch * k : nullptr, ch > 0 ? 1 : 0);
+    if (st != BSPMM_SUCCESS) return st;
+  }
+  return BSPMM_SUCCESS;
 }
 
 // ---- the paper's atomic SWA SpMM for SparseTensor (NEXT-3) -----------------

@@ -60,6 +60,8 @@ struct CsrArgs {
   unsigned long long* trace;  // debug phase timestamps (bspmm_set_trace) or null
   int32_t dbg;                // debug bits (bspmm_set_debug)
   const TmaMaps* maps;        // non-null: full k-tiles are staged with 2-D tensor TMA
+  const float* bias = nullptr;  // GCN epilogue: C += rowsum(A) (x) bias (k floats), or null
+  int32_t accumulate = 0;       // GCN epilogue: C += previous C
 };
 
 // kernels (.cu)
@@ -116,6 +118,9 @@ struct bspmm_handle_s {
   int64_t maps_ldb = 0;
   int32_t maps_k = 0, maps_kt = 0;
   bool maps_ok = false;
+  void* cublas = nullptr;  // cublasHandle_t, created on first bspmm_gcn_layer
+  void* gcn_ws = nullptr;  // U = X W_ch for all channels
+  size_t gcn_ws_bytes = 0;
   int64_t launches = 0;
   std::string err;
   // device workspace (grown on demand)

@@ -51,7 +51,39 @@ struct SpmmParams {
   int32_t sbulk;              // 1: col / vals / row_ptr bases are 16-byte aligned (bulk-copy the CSR slice)
   int32_t prefetch;           // 1: L2-prefetch every unit of a batch up front (small problems)
   int32_t slice_lsu;          // 1: CSR slice by 16-byte cp.async instead of TMA bulk (small problems)
+  const float* __restrict__ bias;  // GCN epilogue (NEXT-1): C += rowsum(A) (x) bias[c0..], or null
+  int32_t accumulate;              // GCN epilogue: C += previous C (channel accumulation)
 };
+
+// GCN epilogue (NEXT-1, PAPER.md Fig. algo:graph_conv_batched): A (U + 1 b^T)
+// = A U + rowsum(A) b^T, so the bias add folds into the SpMM as rs * b after
+// the storage-order sum; channels accumulate into C.
+template <bool EPI, bool VEC>
+__device__ __forceinline__ void epilogue(const SpmmParams& p, float4& acc, float rs, int64_t colf, const float* cptr) {
+  if (!EPI) return;
+  if (p.bias) {
+    if (VEC) {
+      const float4 b = ldg_nc_f4(p.bias + colf);
+      acc.x = fmaf(rs, b.x, acc.x);
+      acc.y = fmaf(rs, b.y, acc.y);
+      acc.z = fmaf(rs, b.z, acc.z);
+      acc.w = fmaf(rs, b.w, acc.w);
+    } else {
+      acc.x = fmaf(rs, __ldg(p.bias + colf), acc.x);
+    }
+  }
+  if (p.accumulate) {
+    if (VEC) {
+      const float4 o = *reinterpret_cast<const float4*>(cptr);
+      acc.x += o.x;
+      acc.y += o.y;
+      acc.z += o.z;
+      acc.w += o.w;
+    } else {
+      acc.x += *cptr;
+    }
+  }
+}
 
 // Stage layout of a unit's CSR slice, after the B tile: three int32 arrays
 // (col, vals, row pointers), each in a region of 16 + 4*count bytes rounded
@@ -320,7 +352,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
 // then accumulated strictly in storage order, so the result is bitwise the
 // fp32 storage-order FMA sum (O3').  Per-unit address math is hoisted; the
 // row loop touches shared memory with 32-bit offsets only.
-template <int CH, bool VEC, bool BST, bool SST>
+template <int CH, bool VEC, bool BST, bool SST, bool EPI>
 __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
                                      int step, int li) {
   constexpr int G = CH >= 4 ? 2 : 4;
@@ -355,6 +387,7 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
     float4 acc[CH];
 #pragma unroll
     for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float rs = 0.f;  // row sum of A (GCN bias epilogue)
     for (int32_t e = e0; e < e1; e += G) {
       const int32_t cnt = min(G, e1 - e);
       int32_t cidx[G];
@@ -388,6 +421,7 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
 #pragma unroll
       for (int q = 0; q < G; ++q) {
         if (q < cnt) {
+          if (EPI) rs += a[q];
 #pragma unroll
           for (int v = 0; v < CH; ++v) {
             acc[v].x = fmaf(a[q], b[q][v].x, acc[v].x);
@@ -408,6 +442,7 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
 #pragma unroll
     for (int v = 0; v < CH; ++v) {
       if (ok[v]) {
+        epilogue<EPI, VEC>(p, acc[v], rs, h.c0 + FW * (li + v * L), crow + FW * v * L);
         if (VEC) stg_cs_f4(crow + FW * v * L, acc[v]);
         else stg_cs_f1(crow + v * L, acc[v].x);
       }
@@ -434,7 +469,7 @@ __device__ __forceinline__ void fma4(float4& acc, float a, const float4& b) {
 // (cols == lanes * CH, float4 chunks): no per-chunk predicates, 32-bit shared
 // addressing, two entries per iteration (independent loads first, FMAs in
 // storage order).  Same arithmetic as rows<> (bitwise O3').
-template <int CH>
+template <int CH, bool EPI>
 __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const UnitHdr& h, const unsigned char* st,
                                                  int first, int step, int li) {
   const int L = p.lanes;
@@ -462,6 +497,7 @@ __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const Unit
     float4 acc[CH];
 #pragma unroll
     for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float rs = 0.f;  // row sum of A (GCN bias epilogue)
     for (; e + 1 < e1; e += 2) {
       const int32_t c0 = ci[e], c1 = ci[e + 1];
       const float a0 = cv[e], a1 = cv[e + 1];
@@ -476,10 +512,12 @@ __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const Unit
       for (int v = 0; v < CH; ++v) fma4(acc[v], a0, x0[v]);
 #pragma unroll
       for (int v = 0; v < CH; ++v) fma4(acc[v], a1, x1[v]);
+      if (EPI) rs += a0, rs += a1;
     }
     if (e < e1) {
       const int32_t c0 = ci[e];
       const float a0 = cv[e];
+      if (EPI) rs += a0;
       const uint32_t p0 = sB + (uint32_t)c0 * pitch;
 #pragma unroll
       for (int v = 0; v < CH; ++v) fma4(acc[v], a0, lds128(p0 + v * vstep));
@@ -490,11 +528,14 @@ __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const Unit
       continue;
     }
 #pragma unroll
-    for (int v = 0; v < CH; ++v) stg_cs_f4(crow + 4 * v * L, acc[v]);
+    for (int v = 0; v < CH; ++v) {
+      epilogue<EPI, true>(p, acc[v], rs, h.c0 + 4 * (li + v * L), crow + 4 * v * L);
+      stg_cs_f4(crow + 4 * v * L, acc[v]);
+    }
   }
 }
 
-template <int CH, bool VEC>
+template <int CH, bool VEC, bool EPI>
 __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& h, int first, int step, int li) {
   constexpr int FW = VEC ? 4 : 1;
   const int L = p.lanes;
@@ -507,9 +548,11 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
     float4 acc[CH];
 #pragma unroll
     for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float rs = 0.f;
     for (int32_t e = e0; e < e1; ++e) {
       const int32_t c = __ldg(p.col + e);
       const float a = __ldg(p.vals + e);
+      if (EPI) rs += a;
       const float* brow = Bt + (int64_t)c * p.ldb;
 #pragma unroll
       for (int v = 0; v < CH; ++v) {
@@ -530,6 +573,7 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
 #pragma unroll
     for (int v = 0; v < CH; ++v) {
       if (li + v * L < cols) {
+        epilogue<EPI, VEC>(p, acc[v], rs, h.c0 + FW * (li + v * L), crow + FW * v * L);
         if (VEC) stg_cs_f4(crow + FW * v * L, acc[v]);
         else stg_cs_f1(crow + v * L, acc[v].x);
       }
@@ -537,7 +581,7 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
   }
 }
 
-template <int CH, bool VEC>
+template <int CH, bool VEC, bool EPI>
 __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem) {
   const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -561,10 +605,10 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
     for (int rep = 0; rep < reps; ++rep) {
       if (h.flags == 3) {  // the hot, staged case
-        if (VEC && (h.kw >> 2) == p.lanes * CH) rows_staged_full<CH>(p, h, st, first, step, li);
-        else rows<CH, VEC, true, true>(p, h, st, first, step, li);
+        if (VEC && (h.kw >> 2) == p.lanes * CH) rows_staged_full<CH, EPI>(p, h, st, first, step, li);
+        else rows<CH, VEC, true, true, EPI>(p, h, st, first, step, li);
       } else {
-        rows_direct<CH, VEC>(p, h, first, step, li);
+        rows_direct<CH, VEC, EPI>(p, h, first, step, li);
       }
     }
     __syncwarp();
@@ -574,7 +618,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
   if (cw == 0 && lane == 0) BSPMM_TRACE(p, 6);
 }
 
-template <int CH, bool VEC>
+template <int CH, bool VEC, bool EPI>
 __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -595,16 +639,16 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
   pdl_launch_dependents();
   if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
   if ((threadIdx.x >> 5) == 0) produce<VEC>(p, maps, smem);
-  else consume<CH, VEC>(p, smem);
+  else consume<CH, VEC, EPI>(p, smem);
   if (p.trace) {
     __syncthreads();
     if (threadIdx.x == 0) BSPMM_TRACE(p, 7);
   }
 }
 
-template <int CH, bool VEC>
+template <int CH, bool VEC, bool EPI>
 static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bspmm_plan_t& plan, cudaStream_t s) {
-  auto kern = spmm_csr_kernel<CH, VEC>;
+  auto kern = spmm_csr_kernel<CH, VEC, EPI>;
   static thread_local int configured_bytes[64] = {};  // per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -655,20 +699,23 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   // the prefetched bytes then never exceed the problem (small, L2-resident)
   // (measured: no gain on C3/C4, so off unless requested with debug bit 16)
   sp.prefetch = (plan.units <= 32LL * plan.grid && (a.dbg & 16)) ? 1 : 0;
-  sp.slice_lsu = (plan.units <= 32LL * plan.grid && !(a.dbg & 32)) ? 1 : 0;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
+  sp.slice_lsu = (plan.units <= 32LL * plan.grid && !(a.dbg & 32)) ? 1 : 0;
+  sp.bias = a.bias;
+  sp.accumulate = a.accumulate;
+  const bool sp_epi = a.bias != nullptr || a.accumulate != 0;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
     switch (plan.chunks) {
-      case 1: return launch_t<1, true>(sp, maps, plan, s);
-      case 2: return launch_t<2, true>(sp, maps, plan, s);
-      default: return launch_t<4, true>(sp, maps, plan, s);
+      case 1: return sp_epi ? launch_t<1, true, true>(sp, maps, plan, s) : launch_t<1, true, false>(sp, maps, plan, s);
+      case 2: return sp_epi ? launch_t<2, true, true>(sp, maps, plan, s) : launch_t<2, true, false>(sp, maps, plan, s);
+      default: return sp_epi ? launch_t<4, true, true>(sp, maps, plan, s) : launch_t<4, true, false>(sp, maps, plan, s);
     }
   }
   switch (plan.chunks) {
-    case 1: return launch_t<1, false>(sp, maps, plan, s);
-    case 2: return launch_t<2, false>(sp, maps, plan, s);
-    default: return launch_t<4, false>(sp, maps, plan, s);
+    case 1: return sp_epi ? launch_t<1, false, true>(sp, maps, plan, s) : launch_t<1, false, false>(sp, maps, plan, s);
+    case 2: return sp_epi ? launch_t<2, false, true>(sp, maps, plan, s) : launch_t<2, false, false>(sp, maps, plan, s);
+    default: return sp_epi ? launch_t<4, false, true>(sp, maps, plan, s) : launch_t<4, false, false>(sp, maps, plan, s);
   }
 }
 
