@@ -18,8 +18,13 @@ def test_exports_every_header_symbol():
     raw = ctypes.CDLL(bs.LIB_PATH)
     missing = [s for s in syms if not hasattr(raw, s)]
     assert not missing, missing
-    # nothing else leaks: internal symbols are hidden
-    assert not hasattr(raw, "_ZN5bspmm9make_planEiibilii iiiP12bspmm_plan_t".replace(" ", ""))
+    # nothing else leaks: every exported function is a declared bspmm_* entry point
+    import subprocess
+    dyn = subprocess.run(["nm", "-D", "--defined-only", bs.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in dyn.splitlines() if " T " in ln}
+    ours = {x for x in exported if x.startswith("bspmm_")}
+    assert ours == set(syms), (ours ^ set(syms))
+    assert not [x for x in exported if "bspmm" in x and not x.startswith("bspmm_")]
 
 
 def test_library_is_sm100a_only():
