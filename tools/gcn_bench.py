@@ -67,7 +67,7 @@ def main():
                 torch.matmul(X, W[ch], out=Us[ch])
                 Us[ch].add_(bias[ch])
                 h_.csr(ro, None, rp_d[ch], col_d, vals_d, Us[ch], Cs[ch])
-            torch.stack(Cs).sum(0, out=Y)
+            torch.sum(torch.stack(Cs), 0, out=Y)
 
         reps = [None]
         R = 20 if batch < 1000 else 3
