@@ -151,6 +151,10 @@ __global__ void __launch_bounds__(kCooThreads) coo2csr_kernel(int32_t batch, con
                                                               float* __restrict__ val_out, uint64_t* ws_keys,
                                                               uint32_t* ws_pay, int64_t ws_stride, int32_t cap) {
   extern __shared__ __align__(16) unsigned char smem[];
+  // the SpMM that consumes this CSR is launched with programmatic stream
+  // serialization: let its prologue start now (it waits for our completion
+  // before touching memory)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t i = blockIdx.x; i < batch; i += gridDim.x) {
     const int64_t g0 = row_off[i], g1 = row_off[i + 1];
     const int32_t n = sizes ? sizes[i] : (int32_t)(g1 - g0);
