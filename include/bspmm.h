@@ -93,6 +93,7 @@ typedef struct {
   int32_t threads;        /* CTA size: 1 producer warp + consumer warps                         */
   int32_t grid;           /* persistent CTAs launched                                           */
   int32_t max_rows;       /* planning assumption for max n_i (hint or default)                  */
+  int32_t sched;          /* 0: static round-robin units; 1: dynamic (global ticket counter)    */
   int64_t units;          /* batch * tiles                                                      */
 } bspmm_plan_t;
 
@@ -134,7 +135,8 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * do not store C (the result is then undefined); 2 = compute every unit from
  * global memory (no staging); 8 = consumers repeat each unit's work 4 times;
  * 16 = L2-prefetch every unit of small problems up front; 32 = always copy
- * the CSR slice with TMA.  0 (default) = normal. */
+ * the CSR slice with TMA; 64 = force the static unit schedule; 128 = force the
+ * dynamic one.  0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */

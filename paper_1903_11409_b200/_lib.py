@@ -19,7 +19,7 @@ VALIDATE = 0x1
 class Plan(ctypes.Structure):
     _fields_ = [("kt", I32), ("tiles", I32), ("lanes", I32), ("vec", I32), ("chunks", I32), ("stages", I32),
                 ("stage_b_bytes", I32), ("stage_s_bytes", I32), ("smem_bytes", I32), ("threads", I32),
-                ("grid", I32), ("max_rows", I32), ("units", I64)]
+                ("grid", I32), ("max_rows", I32), ("sched", I32), ("units", I64)]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

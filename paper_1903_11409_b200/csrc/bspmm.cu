@@ -191,11 +191,14 @@ BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* str
   h->num_sms = prop.multiProcessorCount;
   h->smem_optin = (int)prop.sharedMemPerBlockOptin;
   DeviceGuard g(device);
-  if (cudaMalloc(&h->dev_flag, sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&h->dev_flag, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&h->dev_sched, sizeof(unsigned long long)) != cudaSuccess) {
+    if (h->dev_flag) cudaFree(h->dev_flag);
     delete h;
     return BSPMM_ERROR_OUT_OF_MEMORY;
   }
   cudaMemset(h->dev_flag, 0, sizeof(int));
+  cudaMemset(h->dev_sched, 0, sizeof(unsigned long long));
   *out = h;
   return BSPMM_SUCCESS;
 }
@@ -213,6 +216,7 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (h->ws) cudaFree(h->ws);
     if (h->hbuf) cudaFree(h->hbuf);
     if (h->dev_flag) cudaFree(h->dev_flag);
+    if (h->dev_sched) cudaFree(h->dev_sched);
     if (h->scan_ws) cudaFree(h->scan_ws);
     if (h->gcn_ws) cudaFree(h->gcn_ws);
     if (h->cublas) cublasDestroy(static_cast<cublasHandle_t>(h->cublas));
@@ -252,7 +256,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 63) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 255) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -314,7 +318,11 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   bspmm_status_t st = plan_for(h, batch, k, aligned, &plan);
   if (st != BSPMM_SUCCESS) return st;
   const TmaMaps* maps = plan.vec ? tma_maps(h, B, k, ldb, plan.kt) : nullptr;
-  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias, accumulate};
+  if (h->dbg & 64) plan.sched = 0;
+  if (h->dbg & 128) plan.sched = 1;
+  h->last_plan = plan;
+  CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias, accumulate,
+            plan.sched ? h->dev_sched : nullptr};
   CK(h, launch_spmm_csr(a, plan, h->stream));
   if (plan.units > 0) h->launches++;
   return BSPMM_SUCCESS;

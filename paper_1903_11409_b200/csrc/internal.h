@@ -62,6 +62,7 @@ struct CsrArgs {
   const TmaMaps* maps;        // non-null: full k-tiles are staged with 2-D tensor TMA
   const float* bias = nullptr;  // GCN epilogue: C += rowsum(A) (x) bias (k floats), or null
   int32_t accumulate = 0;       // GCN epilogue: C += previous C
+  unsigned long long* sched = nullptr;  // dynamic-schedule ticket counter (device, zero between launches)
 };
 
 // kernels (.cu)
@@ -127,6 +128,7 @@ struct bspmm_handle_s {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int* dev_flag = nullptr;
+  unsigned long long* dev_sched = nullptr;  // dynamic-schedule ticket counter (zeroed once)
   // offsets scan state: [ticket u64][flags u32 x cap][agg i64 x cap][incl i64 x cap]
   void* scan_ws = nullptr;
   int32_t scan_cap = 0;

@@ -105,6 +105,10 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   p.units = (int64_t)batch * p.tiles;
   p.grid = (int32_t)std::min<int64_t>(p.units, (int64_t)num_sms * ctas);
   p.max_rows = R;
+  // dynamic unit schedule for small batches (a few units per CTA, where an
+  // unlucky static deal of mixed-size matrices sets the tail); large batches
+  // keep the static round-robin with batched metadata prefetch
+  p.sched = p.units <= 32LL * p.grid ? 1 : 0;
   *out = p;
   return BSPMM_SUCCESS;
 }

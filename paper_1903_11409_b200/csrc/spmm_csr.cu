@@ -53,6 +53,7 @@ struct SpmmParams {
   int32_t slice_lsu;          // 1: CSR slice by 16-byte cp.async instead of TMA bulk (small problems)
   const float* __restrict__ bias;  // GCN epilogue (NEXT-1): C += rowsum(A) (x) bias[c0..], or null
   int32_t accumulate;              // GCN epilogue: C += previous C (channel accumulation)
+  unsigned long long* sched;       // dynamic schedule ticket counter (self-resetting), or null (static)
 };
 
 // GCN epilogue (NEXT-1, PAPER.md Fig. algo:graph_conv_batched): A (U + 1 b^T)
@@ -164,8 +165,11 @@ __device__ __forceinline__ void meta_rt2(const SpmmParams& p, int64_t uu, Meta& 
   }
 }
 
+// Stage unit j of this CTA (metadata already known): wait for its ring stage,
+// TMA/cp.async the B tile and CSR slice, publish the header, arrive on "full".
 template <bool VEC>
-__device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem) {
+__device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem, int j,
+                                           int64_t g0, int32_t n, int32_t c0, int32_t kw, int32_t nz0, int32_t nnz) {
   UnitHdr* hdr = reinterpret_cast<UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
@@ -173,63 +177,6 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
   const int32_t stage_bytes = p.stage_b + p.stage_s;
   const int lane = threadIdx.x & 31;
   const uint64_t pol = policy_evict_first();
-  const int64_t G = gridDim.x;
-
-  // Metadata for 32 units per batch, one lane each, both round trips done
-  // BEFORE any copy of the batch is issued: under load the row_ptr loads
-  // would otherwise queue behind the bulk B traffic (tools/trace.py).  The
-  // next batch is prefetched while the current one is issued.
-  Meta cur, nxt;
-  meta_rt1(p, blockIdx.x + lane * G, nxt);
-  meta_rt2(p, blockIdx.x + lane * G, nxt);
-  int j = 0;
-  for (int64_t u = blockIdx.x; u < p.units; u += G, ++j) {
-    const int jj = j & 31;
-    if (jj == 0) {
-      cur = nxt;
-      meta_rt1(p, u + (32 + lane) * G, nxt);  // next batch, round trip 1
-      if (j == 0 && lane == 0) BSPMM_TRACE(p, 2);
-    }
-    if (jj == 8 || (jj == 0 && u + 8 * G >= p.units)) meta_rt2(p, u + (32 - jj + lane) * G, nxt);
-    if (jj == 0 && p.prefetch) {
-      // small problem: prefetch this lane's unit of the batch (B tile + CSR
-      // slice) into L2 now; the smem TMA loads below then hit L2 instead of
-      // queueing DRAM-latency-bound behind the SM's outstanding-copy limit
-      const int64_t uu = u + (int64_t)lane * G;
-      if (uu < p.units && cur.n > 0) {
-        const int32_t nnz_ = cur.nz1 - cur.nz0;
-        const int64_t z0 = cur.nz0 & ~3LL, z1 = (cur.nz1 + 3) & ~3LL;
-        if (nnz_ > 0 && p.sbulk) {
-          prefetch_l2(p.col + z0, (uint32_t)(z1 - z0) * 4u);
-          prefetch_l2(p.vals + z0, (uint32_t)(z1 - z0) * 4u);
-        }
-        if (VEC) {
-          const float* bsrc = p.B + cur.g0 * p.ldb + cur.c0;
-          if (cur.kw == p.ldb) {
-            prefetch_l2(bsrc, (uint32_t)cur.n * (uint32_t)cur.kw * 4u);
-          } else if (p.tma2d && cur.kw == p.kt) {
-            int32_t r0 = 0;
-            while (cur.n - r0 >= 512) {
-              prefetch_l2_2d(&maps.m[kTmaMaps - 1], cur.c0, (int32_t)(cur.g0 + r0));
-              r0 += 256;
-            }
-            for (int b = kTmaMaps - 1; b >= 0; --b)
-              if ((cur.n - r0) & (1 << b)) {
-                prefetch_l2_2d(&maps.m[b], cur.c0, (int32_t)(cur.g0 + r0));
-                r0 += 1 << b;
-              }
-          }
-        }
-      }
-    }
-    const int64_t g0 = __shfl_sync(0xffffffffu, cur.g0, jj);
-    const int32_t n = __shfl_sync(0xffffffffu, cur.n, jj);
-    const int32_t c0 = __shfl_sync(0xffffffffu, cur.c0, jj);
-    const int32_t kw = __shfl_sync(0xffffffffu, cur.kw, jj);
-    const int32_t nz0 = __shfl_sync(0xffffffffu, cur.nz0, jj);
-    const int32_t nnz = __shfl_sync(0xffffffffu, cur.nz1, jj) - nz0;
-    if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
-
     const int s = j % p.stages;
     const uint32_t phase = (uint32_t)(j / p.stages) & 1u;
     mbar_wait(&empty[s], phase ^ 1u);
@@ -341,7 +288,123 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
     if (j < 2 && lane == 0) BSPMM_TRACE(p, 11 + j);
     cp_async_arrive_noinc(&full[s]);  // 32 arrivals, each after its lane's copies land
     if (j < 2 && lane == 0) BSPMM_TRACE(p, 13 + j);
+}
+
+// After the last unit: a "done" header (flags = -1) tells the consumers to exit.
+__device__ __forceinline__ void issue_done(const SpmmParams& p, unsigned char* smem, int j) {
+  UnitHdr* hdr = reinterpret_cast<UnitHdr*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
+  uint64_t* empty = full + p.stages;
+  const int lane = threadIdx.x & 31;
+  const int s = j % p.stages;
+  mbar_wait(&empty[s], ((uint32_t)(j / p.stages) & 1u) ^ 1u);
+  if (lane == 0) {
+    hdr[s].flags = -1;
+    mbar_arrive(&full[s]);
   }
+  cp_async_arrive_noinc(&full[s]);
+}
+
+template <bool VEC>
+__device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem) {
+  const int lane = threadIdx.x & 31;
+  const int64_t G = gridDim.x;
+  int j = 0;
+  if (p.sched) {
+    // Dynamic schedule (mixed-size batches): the first unit is blockIdx.x, later
+    // ones come from a global ticket counter, so a CTA that drew small matrices
+    // keeps drawing (load balance within one unit).  The next ticket is drawn
+    // while the current unit is issued.  The counter resets itself: the draw
+    // that returns units - 1 is the last of the launch.
+    Meta m;
+    int64_t u = blockIdx.x;
+    unsigned long long t_next = 0;
+    if (lane == 0) {
+      t_next = atomicAdd(p.sched, 1ULL);
+      meta_rt1(p, u, m);
+      meta_rt2(p, u, m);
+    }
+    while (true) {
+      const int64_t g0 = __shfl_sync(0xffffffffu, m.g0, 0);
+      const int32_t n = __shfl_sync(0xffffffffu, m.n, 0);
+      const int32_t c0 = __shfl_sync(0xffffffffu, m.c0, 0);
+      const int32_t kw = __shfl_sync(0xffffffffu, m.kw, 0);
+      const int32_t nz0 = __shfl_sync(0xffffffffu, m.nz0, 0);
+      const int32_t nnz = __shfl_sync(0xffffffffu, m.nz1, 0) - nz0;
+      if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
+      issue_unit<VEC>(p, maps, smem, j, g0, n, c0, kw, nz0, nnz);
+      ++j;
+      const unsigned long long t = __shfl_sync(0xffffffffu, t_next, 0);
+      if ((int64_t)t + G >= p.units) {
+        if (lane == 0 && t == (unsigned long long)p.units - 1) atomicExch(p.sched, 0ULL);
+        break;
+      }
+      u = (int64_t)t + G;
+      if (lane == 0) {
+        t_next = atomicAdd(p.sched, 1ULL);
+        meta_rt1(p, u, m);
+        meta_rt2(p, u, m);
+      }
+    }
+  } else {
+    // Static schedule: units blockIdx.x, +grid, ...  Metadata for 32 units per
+    // batch, one lane each, both round trips done BEFORE any copy of the batch
+    // is issued: under load the row_ptr loads would otherwise queue behind the
+    // bulk B traffic (tools/trace.py).  The next batch is prefetched while the
+    // current one is issued.
+    Meta cur, nxt;
+    meta_rt1(p, blockIdx.x + lane * G, nxt);
+    meta_rt2(p, blockIdx.x + lane * G, nxt);
+    for (int64_t u = blockIdx.x; u < p.units; u += G, ++j) {
+      const int jj = j & 31;
+      if (jj == 0) {
+        cur = nxt;
+        meta_rt1(p, u + (32 + lane) * G, nxt);  // next batch, round trip 1
+        if (j == 0 && lane == 0) BSPMM_TRACE(p, 2);
+      }
+      if (jj == 8 || (jj == 0 && u + 8 * G >= p.units)) meta_rt2(p, u + (32 - jj + lane) * G, nxt);
+      if (jj == 0 && p.prefetch) {
+        // small problem: prefetch this lane's unit of the batch (B tile + CSR
+        // slice) into L2 now; the smem TMA loads below then hit L2 instead of
+        // queueing DRAM-latency-bound behind the SM's outstanding-copy limit
+        const int64_t uu = u + (int64_t)lane * G;
+        if (uu < p.units && cur.n > 0) {
+          const int32_t nnz_ = cur.nz1 - cur.nz0;
+          const int64_t z0 = cur.nz0 & ~3LL, z1 = (cur.nz1 + 3) & ~3LL;
+          if (nnz_ > 0 && p.sbulk) {
+            prefetch_l2(p.col + z0, (uint32_t)(z1 - z0) * 4u);
+            prefetch_l2(p.vals + z0, (uint32_t)(z1 - z0) * 4u);
+          }
+          if (VEC) {
+            const float* bsrc = p.B + cur.g0 * p.ldb + cur.c0;
+            if (cur.kw == p.ldb) {
+              prefetch_l2(bsrc, (uint32_t)cur.n * (uint32_t)cur.kw * 4u);
+            } else if (p.tma2d && cur.kw == p.kt) {
+              int32_t r0 = 0;
+              while (cur.n - r0 >= 512) {
+                prefetch_l2_2d(&maps.m[kTmaMaps - 1], cur.c0, (int32_t)(cur.g0 + r0));
+                r0 += 256;
+              }
+              for (int b = kTmaMaps - 1; b >= 0; --b)
+                if ((cur.n - r0) & (1 << b)) {
+                  prefetch_l2_2d(&maps.m[b], cur.c0, (int32_t)(cur.g0 + r0));
+                  r0 += 1 << b;
+                }
+            }
+          }
+        }
+      }
+      const int64_t g0 = __shfl_sync(0xffffffffu, cur.g0, jj);
+      const int32_t n = __shfl_sync(0xffffffffu, cur.n, jj);
+      const int32_t c0 = __shfl_sync(0xffffffffu, cur.c0, jj);
+      const int32_t kw = __shfl_sync(0xffffffffu, cur.kw, jj);
+      const int32_t nz0 = __shfl_sync(0xffffffffu, cur.nz0, jj);
+      const int32_t nnz = __shfl_sync(0xffffffffu, cur.nz1, jj) - nz0;
+      if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
+      issue_unit<VEC>(p, maps, smem, j, g0, n, c0, kw, nz0, nnz);
+    }
+  }
+  issue_done(p, smem, j);
   if (lane == 0) BSPMM_TRACE(p, 4);
 }
 
@@ -595,12 +658,12 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
   const int rpw = 32 / L;
   const int sub = lane / L, li = lane % L;
   const int first = cw * rpw + sub, step = W * rpw;
-  int j = 0;
-  for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+  for (int j = 0;; ++j) {
     const int s = j % p.stages;
     mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
     const UnitHdr h = hdr[s];
+    if (h.flags < 0) break;  // the producer's "done" header
     const unsigned char* st = ring + (size_t)s * stage_bytes;
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
     for (int rep = 0; rep < reps; ++rep) {
@@ -702,7 +765,8 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.slice_lsu = (plan.units <= 32LL * plan.grid && !(a.dbg & 32)) ? 1 : 0;
   sp.bias = a.bias;
   sp.accumulate = a.accumulate;
-  const bool sp_epi = a.bias != nullptr || a.accumulate != 0;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
+  const bool sp_epi = a.bias != nullptr || a.accumulate != 0;
+  sp.sched = a.sched;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {

@@ -162,6 +162,12 @@ def test_tuning_space_bitwise(h):
                     C = run_csr(h, b)
                     assert np.array_equal(C.view(np.uint32), ref.view(np.uint32)), (kt, warps, ctas, chunks)
     h.set_tuning(0, 0, 0, 0)
+    for sched_bits in (64, 128):            # static and dynamic unit schedules, same bits
+        h.set_debug(sched_bits)
+        for cid in (3, 4):
+            bb = synth.config(cid)
+            assert_parity(bb, run_csr(h, bb), f"sched {sched_bits} config {cid}")
+    h.set_debug(0)
 
 
 def test_deterministic_repeat(h):
