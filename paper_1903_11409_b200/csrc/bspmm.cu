@@ -319,7 +319,7 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   if (st != BSPMM_SUCCESS) return st;
   const TmaMaps* maps = plan.vec ? tma_maps(h, B, k, ldb, plan.kt) : nullptr;
   if (h->dbg & 64) plan.sched = 0;
-  if (h->dbg & 128) plan.sched = 1;
+  if ((h->dbg & 128) && row_off) plan.sched = 1;
   h->last_plan = plan;
   CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias, accumulate,
             plan.sched ? h->dev_sched : nullptr};
@@ -338,15 +338,15 @@ BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, c
   if ((!row_off && !sizes) || !row_ptr) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
   if (B && B == C) return fail(h, BSPMM_ERROR_INVALID_VALUE, "C must not alias B");
   DeviceGuard g(h->device);
-  if (!row_off) {
+  if (!row_off && (h->flags & BSPMM_VALIDATE)) {  // validation needs materialised offsets
     bspmm_status_t st = grow(h, &h->ws, &h->ws_bytes, al256((size_t)(batch + 1) * 8));
     if (st != BSPMM_SUCCESS) return st;
     int64_t* ro = static_cast<int64_t*>(h->ws);
     st = bspmm_build_offsets(h, batch, sizes, ro);
     if (st != BSPMM_SUCCESS) return st;
-    return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc,
-                    (h->flags & BSPMM_VALIDATE) != 0);
+    return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc, true);
   }
+  // row_off == NULL: the SpMM producer builds the packed offsets itself (fused row a-1)
   return csr_impl(h, batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc,
                   (h->flags & BSPMM_VALIDATE) != 0);
 }

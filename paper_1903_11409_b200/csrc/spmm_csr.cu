@@ -142,12 +142,42 @@ struct Meta {
   int32_t n, c0, kw, nz0, nz1;
 };
 
-// round trip 1 for unit uu: row offset, rows, tile
-__device__ __forceinline__ void meta_rt1(const SpmmParams& p, int64_t uu, Meta& m) {
+// Fused batch-offset builder (row a-1 inside the SpMM, row_off == null):
+// the prefix P(i) = sum_{m<i} sizes[m] for this lane's unit base + lane*G,
+// from a warp scan of per-lane segment sums; `carry` holds P at the batch
+// start and advances to P at the next batch's start.
+__device__ __forceinline__ int64_t fused_prefix(const SpmmParams& p, int64_t base, int64_t G, int lane,
+                                                int64_t& carry) {
+  const int64_t bmax = p.units / p.tiles;  // matrices
+  auto mat = [&](int64_t u) { return u < p.units ? u / p.tiles : bmax; };
+  const int64_t i0 = mat(base + (int64_t)lane * G), i1 = mat(base + (int64_t)(lane + 1) * G);
+  int64_t seg = 0;
+  for (int64_t m = i0; m < i1; ++m) seg += __ldg(p.sizes + m);
+  int64_t x = seg;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  const int64_t pre = carry + x - seg;
+  carry += __shfl_sync(0xffffffffu, x, 31);
+  return pre;
+}
+__device__ __forceinline__ int64_t fused_prefix_start(const SpmmParams& p, int lane) {
+  const int64_t i0 = (int64_t)blockIdx.x / p.tiles;  // matrices before this CTA's first unit
+  int64_t s = 0;
+  for (int64_t m = lane; m < i0; m += 32) s += __ldg(p.sizes + m);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+  return s;
+}
+
+// round trip 1 for unit uu: row offset (or the fused prefix g0f), rows, tile
+__device__ __forceinline__ void meta_rt1(const SpmmParams& p, int64_t uu, Meta& m, int64_t g0f = -1) {
   if (uu < p.units) {
     const int64_t i = uu / p.tiles;
     const int32_t t = (int32_t)(uu - i * p.tiles);
-    m.g0 = p.row_off[i];
+    m.g0 = p.row_off ? p.row_off[i] : g0f;
     m.n = p.sizes ? p.sizes[i] : (int32_t)(p.row_off[i + 1] - m.g0);
     m.c0 = t * p.kt;
     m.kw = min(p.kt, p.k - m.c0);
@@ -353,13 +383,15 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
     // bulk B traffic (tools/trace.py).  The next batch is prefetched while the
     // current one is issued.
     Meta cur, nxt;
-    meta_rt1(p, blockIdx.x + lane * G, nxt);
+    int64_t carry = p.row_off ? 0 : fused_prefix_start(p, lane);
+    meta_rt1(p, blockIdx.x + lane * G, nxt, p.row_off ? -1 : fused_prefix(p, blockIdx.x, G, lane, carry));
     meta_rt2(p, blockIdx.x + lane * G, nxt);
     for (int64_t u = blockIdx.x; u < p.units; u += G, ++j) {
       const int jj = j & 31;
       if (jj == 0) {
         cur = nxt;
-        meta_rt1(p, u + (32 + lane) * G, nxt);  // next batch, round trip 1
+        const int64_t nb = u + 32 * G;  // next batch, round trip 1
+        meta_rt1(p, nb + lane * G, nxt, p.row_off ? -1 : fused_prefix(p, nb, G, lane, carry));
         if (j == 0 && lane == 0) BSPMM_TRACE(p, 2);
       }
       if (jj == 8 || (jj == 0 && u + 8 * G >= p.units)) meta_rt2(p, u + (32 - jj + lane) * G, nxt);

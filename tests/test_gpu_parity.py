@@ -366,3 +366,27 @@ def test_coo_atomic_edge_cases(h):
     with pytest.raises(bs.BspmmError, match="NOT_SUPPORTED"):
         b = synth.random_batch(rng, 3, 5, nmax=5)
         h.coo_atomic(T(b.row_off), None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B))
+
+
+# ------------------------------------------------------------ a-1 fused into the SpMM (row_off == NULL)
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_fused_offsets_bitwise(h, cid):
+    b = synth.config(cid)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    C1 = h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
+    C2 = h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
+    torch.cuda.synchronize()
+    assert torch.equal(C1.view(torch.int32), C2.view(torch.int32))
+
+
+def test_fused_offsets_adversarial(h):
+    rng = np.random.default_rng(99)
+    for trial in range(8):
+        b = synth.random_batch(rng, int(rng.integers(1, 400)), 64, nmax=30, dmax=4, allow_empty_graphs=True)
+        h.set_hints(0, 0)
+        for kt in (0, 16, 32):
+            h.set_tuning(kt, 0, 0, 0)
+            C = h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)).cpu().numpy()
+            assert_parity(b, C, f"fused offsets trial {trial} kt {kt}")
+    h.set_tuning(0, 0, 0, 0)
