@@ -151,8 +151,35 @@ __device__ __forceinline__ int64_t fused_prefix(const SpmmParams& p, int64_t bas
   const int64_t bmax = p.units / p.tiles;  // matrices
   auto mat = [&](int64_t u) { return u < p.units ? u / p.tiles : bmax; };
   const int64_t i0 = mat(base + (int64_t)lane * G), i1 = mat(base + (int64_t)(lane + 1) * G);
+  // segment sum with many loads in flight: 16-byte loads, 8 per step, split partial sums
   int64_t seg = 0;
-  for (int64_t m = i0; m < i1; ++m) seg += __ldg(p.sizes + m);
+  int64_t m = i0;
+  const bool al = (reinterpret_cast<uintptr_t>(p.sizes) & 15u) == 0;
+  if (al) {
+    for (; m < i1 && (m & 3); ++m) seg += __ldg(p.sizes + m);
+    const int4* v4 = reinterpret_cast<const int4*>(p.sizes + m);
+    const int64_t nv = (i1 - m) >> 2;
+    int64_t q = 0;
+    int32_t s0 = 0, s1 = 0;
+    for (; q + 8 <= nv; q += 8) {
+      int4 t[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) t[r] = __ldg(v4 + q + r);
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) {
+        s0 += t[r].x + t[r].y + t[r].z + t[r].w;
+        s1 += t[r + 1].x + t[r + 1].y + t[r + 1].z + t[r + 1].w;
+      }
+      seg += (int64_t)s0 + s1;  // int32 partials per 32 sizes, widened (sizes < 2^31 each)
+      s0 = s1 = 0;
+    }
+    for (; q < nv; ++q) {
+      const int4 t = __ldg(v4 + q);
+      seg += (int64_t)t.x + t.y + t.z + t.w;
+    }
+    m += nv << 2;
+  }
+  for (; m < i1; ++m) seg += __ldg(p.sizes + m);
   int64_t x = seg;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
