@@ -151,8 +151,9 @@ BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h);
  *                                  vals[e] * B[(row_off[i]+col_idx[e])*ldb + c],
  *     g = row_off[i] + r, accumulated in fp32 FMA in storage order from +0.0.
  *  row_off  [batch+1] dev int64, or NULL: then `sizes` is required and the
- *           layout is packed; the SpMM kernel derives the offsets itself
- *           (warp prefix sums of sizes inside the launch: no extra kernel).
+ *           layout is packed; the library derives the offsets on the device
+ *           (small batches: warp prefix sums inside the SpMM launch itself;
+ *           large ones: the look-back scan kernel of bspmm_build_offsets).
  *  sizes    [batch]   dev int32 n_i, or NULL: n_i = row_off[i+1] - row_off[i].
  *  row_ptr  [row_off[batch]+1] dev int32: block-diagonal CSR row pointer
  *           holding ABSOLUTE positions into col_idx / vals.

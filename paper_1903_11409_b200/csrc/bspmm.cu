@@ -346,7 +346,26 @@ BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, c
     if (st != BSPMM_SUCCESS) return st;
     return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc, true);
   }
-  // row_off == NULL: the SpMM producer builds the packed offsets itself (fused row a-1)
+  if (!row_off) {
+    // row_off == NULL: small batches (every CTA's units fit one metadata batch)
+    // build the packed offsets inside the SpMM producer (fused row a-1, one
+    // launch); large ones use the look-back scan kernel first -- the fused
+    // prefix costs dependent round trips on the producer's path every 32 units
+    // (C5: 866 vs 832 us per step, tools/kbench.py)
+    const bool aligned = (k % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C);
+    bspmm_plan_t pl;
+    bspmm_status_t st = make_plan(k, batch, aligned, h->hint_rows, h->hint_nnz, h->num_sms, h->smem_optin,
+                                  h->tune_kt, h->tune_warps, h->tune_ctas, h->tune_chunks, &pl);
+    if (st != BSPMM_SUCCESS) return fail(h, st, "planner rejected the arguments");
+    if (pl.units > 32LL * pl.grid) {
+      st = grow(h, &h->ws, &h->ws_bytes, al256((size_t)(batch + 1) * 8));
+      if (st != BSPMM_SUCCESS) return st;
+      int64_t* ro = static_cast<int64_t*>(h->ws);
+      st = bspmm_build_offsets(h, batch, sizes, ro);
+      if (st != BSPMM_SUCCESS) return st;
+      return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc, false);
+    }
+  }
   return csr_impl(h, batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc,
                   (h->flags & BSPMM_VALIDATE) != 0);
 }
