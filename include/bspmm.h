@@ -182,7 +182,13 @@ BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, c
  *  csr_*_out   dev, nullable as a group: when non-NULL the built CSR is
  *              written there ([total_rows+1], [total_nnz], [total_nnz]),
  *              otherwise into handle workspace.
- * row_off may be NULL (then built from sizes); nnz_off is required. */
+ * row_off may be NULL (then built from sizes); nnz_off is required.
+ * With planner hints set (bspmm_set_hints: max_rows, max_nnz bounding every
+ * A_i), the fast path (k, ldb, ldc % 4 == 0, aligned B, C) and no csr_*_out,
+ * the conversion is FUSED into the SpMM launch: each unit's SparseTensor slice
+ * is staged and sorted into CSR in shared memory (same canonical order, same
+ * bits).  A matrix beyond the hints is then skipped and reported as
+ * BSPMM_ERROR_INVALID_VALUE by the next bspmm_sync. */
 BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
                                    const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
                                    const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc,

@@ -268,6 +268,16 @@ BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h) {
   if (h->s_h2d) CK(h, cudaStreamSynchronize(h->s_h2d));
   if (h->s_d2h) CK(h, cudaStreamSynchronize(h->s_d2h));
   CK(h, cudaGetLastError());
+  if (h->coo_fused_pending) {  // a fused bspmm_coo skipped a matrix beyond the planner hints?
+    h->coo_fused_pending = false;
+    int flag = 0;
+    CK(h, cudaMemcpy(&flag, h->dev_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag & 64) {
+      CK(h, cudaMemset(h->dev_flag, 0, sizeof(int)));
+      return fail(h, BSPMM_ERROR_INVALID_VALUE,
+                  "bspmm_coo: a matrix exceeded the max_rows / max_nnz hints; its rows were not written");
+    }
+  }
   return BSPMM_SUCCESS;
 }
 
@@ -465,6 +475,29 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
     st = bspmm_build_offsets(h, batch, sizes, w.row_off);
     if (st != BSPMM_SUCCESS) return st;
     ro = w.row_off;
+  }
+  // Fused path (one SpMM launch converts each matrix's SparseTensor slice to CSR
+  // in shared memory): needs the vectorised path, planner hints that bound every
+  // matrix (a matrix beyond them is skipped and reported by bspmm_sync), and no
+  // request for the built CSR.
+  const bool aligned = (k % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C);
+  if (!out_given && aligned && h->hint_rows > 0 && h->hint_nnz > 0 && !(h->flags & BSPMM_VALIDATE)) {
+    bspmm_plan_t plan;
+    st = make_plan(k, batch, true, h->hint_rows, h->hint_nnz, h->num_sms, h->smem_optin, h->tune_kt, h->tune_warps,
+                   h->tune_ctas, h->tune_chunks, &plan, /*coo=*/true);
+    if (st != BSPMM_SUCCESS) return fail(h, st, "planner rejected the arguments");
+    if ((int64_t)plan.stage_b_bytes >= (int64_t)h->hint_rows * plan.kt * 4) {
+      h->last_plan = plan;
+      const TmaMaps* maps = tma_maps(h, B, k, ldb, plan.kt);
+      CsrArgs a{batch, k, ro, sizes, nullptr, nullptr, vals, B, ldb, C, ldc, h->trace, h->dbg, maps};
+      a.coo_nnz_off = nnz_off;
+      a.coo_idx = idx;
+      a.err = h->dev_flag;
+      CK(h, launch_spmm_csr(a, plan, h->stream));
+      if (plan.units > 0) h->launches++;
+      h->coo_fused_pending = true;
+      return BSPMM_SUCCESS;
+    }
   }
   int32_t* rp = out_given ? csr_row_ptr_out : w.row_ptr;
   int32_t* col = out_given ? csr_col_out : w.col;

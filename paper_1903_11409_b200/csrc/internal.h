@@ -37,7 +37,7 @@ BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stag
 // planner (plan.cpp)
 bspmm_status_t make_plan(int32_t k, int32_t batch, bool aligned, int32_t max_rows, int64_t max_nnz,
                          int32_t num_sms, int32_t smem_per_cta, int32_t kt_override, int32_t warps,
-                         int32_t ctas_per_sm, int32_t chunks_pref, bspmm_plan_t* out);
+                         int32_t ctas_per_sm, int32_t chunks_pref, bspmm_plan_t* out, bool coo = false);
 
 // 2-D TMA descriptors over B [rows x k] (row pitch ldb) with box {kt, 2^b rows},
 // b = 0..8: a unit of n_i rows is staged with popcount(n_i) tensor copies
@@ -63,6 +63,9 @@ struct CsrArgs {
   const float* bias = nullptr;  // GCN epilogue: C += rowsum(A) (x) bias (k floats), or null
   int32_t accumulate = 0;       // GCN epilogue: C += previous C
   unsigned long long* sched = nullptr;  // dynamic-schedule ticket counter (device, zero between launches)
+  const int64_t* coo_nnz_off = nullptr; // fused COO mode: per-matrix entry offsets (col/vals = raw COO)
+  const int32_t* coo_idx = nullptr;     // fused COO mode: (row, col) pairs
+  int* err = nullptr;                   // device error flag (bit 64: COO unit over stage capacity)
 };
 
 // kernels (.cu)
@@ -128,6 +131,7 @@ struct bspmm_handle_s {
   void* ws = nullptr;
   size_t ws_bytes = 0;
   int* dev_flag = nullptr;
+  bool coo_fused_pending = false;  // a fused bspmm_coo ran since the last bspmm_sync
   unsigned long long* dev_sched = nullptr;  // dynamic-schedule ticket counter (zeroed once)
   // offsets scan state: [ticket u64][flags u32 x cap][agg i64 x cap][incl i64 x cap]
   void* scan_ws = nullptr;

@@ -26,7 +26,7 @@ namespace bspmm {
 
 bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, int64_t max_nnz,
                          int32_t num_sms, int32_t smem_per_cta, int32_t kt_override, int32_t warps,
-                         int32_t ctas_per_sm, int32_t chunks_pref, bspmm_plan_t* out) {
+                         int32_t ctas_per_sm, int32_t chunks_pref, bspmm_plan_t* out, bool coo) {
   if (!out || k < 1 || batch < 0 || num_sms < 1 || smem_per_cta < 1024) return BSPMM_ERROR_INVALID_VALUE;
   bspmm_plan_t p{};
   const int32_t R = max_rows > 0 ? max_rows : kDefaultRows;
@@ -56,7 +56,11 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   // (stage regions are 128-byte aligned: 2-D TMA destinations)
   // CSR slice: col, vals, row pointers, each 16 + 4*count bytes rounded to 16 (spmm_csr.cu slice_bytes)
   const int64_t Zc = std::min<int64_t>(Z, 1 << 20);
-  int64_t s_bytes64 = align_up((int32_t)(2 * ((16 + 4 * Zc + 15) / 16 * 16) + (16 + 4 * (R + 1) + 15) / 16 * 16), 128);
+  auto a16 = [](int64_t x) { return (x + 15) / 16 * 16; };
+  int64_t s_need = 2 * a16(16 + 4 * Zc) + a16(16 + 4 * (R + 1));
+  if (coo)  // fused COO mode (spmm_csr.cu coo_stage_bytes): + raw pairs, raw values, cursors, slots
+    s_need = a16(s_need) + a16(8 * (Zc + 1)) + a16(4 * (Zc + 3)) + a16(4 * (R + 1)) + a16(4 * Zc);
+  int64_t s_bytes64 = align_up((int32_t)s_need, 128);
   auto stages_in = [&](int32_t kt_, int32_t budget_) {
     int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 128);
     int64_t per = b + s_bytes64;

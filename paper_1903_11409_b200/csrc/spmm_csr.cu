@@ -54,6 +54,11 @@ struct SpmmParams {
   const float* __restrict__ bias;  // GCN epilogue (NEXT-1): C += rowsum(A) (x) bias[c0..], or null
   int32_t accumulate;              // GCN epilogue: C += previous C (channel accumulation)
   unsigned long long* sched;       // dynamic schedule ticket counter (self-resetting), or null (static)
+  // fused COO mode (bspmm_coo): the unit's SparseTensor slice is converted to
+  // CSR in shared memory by the consumers (row a-2 inside the SpMM launch)
+  const int64_t* __restrict__ nnz_off;
+  const int32_t* __restrict__ idx;   // [nnz][2] (row, col) local pairs
+  int* err;                          // device flag: bit 64 = a unit exceeded the stage (hint too small)
 };
 
 // GCN epilogue (NEXT-1, PAPER.md Fig. algo:graph_conv_batched): A (U + 1 b^T)
@@ -94,6 +99,15 @@ __device__ __forceinline__ int64_t i64min(int64_t a, int64_t b) { return a < b ?
 __host__ __device__ __forceinline__ int32_t slice_region(int64_t count) { return (int32_t)((16 + 4 * count + 15) & ~15LL); }
 __host__ __device__ __forceinline__ int64_t slice_bytes(int64_t nnz, int64_t n) {
   return 2LL * slice_region(nnz) + slice_region(n + 1);
+}
+// fused COO mode, after the CSR slice: raw (row, col) pairs (element 0 at pair
+// (first & 1)), raw values (element 0 at (first & 3)), per-row cursors, slots
+__host__ __device__ __forceinline__ int64_t al16(int64_t x) { return (x + 15) & ~15LL; }
+__host__ __device__ __forceinline__ int64_t coo_raw_off(int64_t nnz, int64_t n) { return al16(slice_bytes(nnz, n)); }
+__host__ __device__ __forceinline__ int64_t coo_pairs_bytes(int64_t nnz) { return al16(8 * (nnz + 1)); }
+__host__ __device__ __forceinline__ int64_t coo_vals_bytes(int64_t nnz) { return al16(4 * (nnz + 3)); }
+__host__ __device__ __forceinline__ int64_t coo_stage_bytes(int64_t nnz, int64_t n) {
+  return coo_raw_off(nnz, n) + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz) + al16(4 * (n + 1)) + al16(4 * nnz);
 }
 
 // trace slots per CTA (bspmm_set_trace): 0 entry, 1 after PDL wait, 2 producer has unit-0 row
@@ -208,12 +222,17 @@ __device__ __forceinline__ void meta_rt1(const SpmmParams& p, int64_t uu, Meta& 
     m.n = p.sizes ? p.sizes[i] : (int32_t)(p.row_off[i + 1] - m.g0);
     m.c0 = t * p.kt;
     m.kw = min(p.kt, p.k - m.c0);
+    if (p.nnz_off) {  // fused COO mode: the entry range comes with round trip 1
+      m.nz0 = (int32_t)p.nnz_off[i];
+      m.nz1 = (int32_t)p.nnz_off[i + 1];
+    }
   } else {
     m.g0 = 0; m.n = 0; m.c0 = 0; m.kw = 0;
   }
 }
 // round trip 2: the matrix's entry range (depends on round trip 1)
 __device__ __forceinline__ void meta_rt2(const SpmmParams& p, int64_t uu, Meta& m) {
+  if (p.nnz_off) return;  // fused COO mode: no row pointers
   if (uu < p.units) {
     m.nz0 = p.row_ptr[m.g0];
     m.nz1 = p.row_ptr[m.g0 + m.n];
@@ -239,11 +258,65 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
     mbar_wait(&empty[s], phase ^ 1u);
     if (j == 0 && lane == 0) BSPMM_TRACE(p, 9);
     unsigned char* st = ring + (size_t)s * stage_bytes;
+    const float* bsrc = p.B + g0 * p.ldb + c0;
+    unsigned char* sreg = st + p.stage_b;
+    if (p.nnz_off) {  // fused COO mode: B tile + the raw SparseTensor slice
+      const bool fits = (int64_t)n * kw * 4 <= p.stage_b && coo_stage_bytes(nnz, n) <= p.stage_s;
+      if (fits && n > 0) {
+        if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)n * (uint32_t)kw * 4u);
+        __syncwarp();
+        if (kw == p.ldb) {
+          if (lane == 3) bulk_g2s_hint(st, bsrc, (uint32_t)n * (uint32_t)kw * 4u, &full[s], pol);
+        } else if (p.tma2d && kw == p.kt) {
+          const int32_t big = n >> 8, rem = n & 255;
+          for (int32_t q = lane - 4; q >= 0 && q < big && lane < 16; q += 12)
+            tma_load_2d(st + (size_t)q * 256 * kw * 4, &maps.m[kTmaMaps - 1], c0, (int32_t)(g0 + q * 256), &full[s]);
+          const int b = lane - 16;
+          if (b >= 0 && b < 8 && (rem & (1 << b))) {
+            const int32_t r0 = big * 256 + (rem >> (b + 1) << (b + 1));
+            tma_load_2d(st + (size_t)r0 * kw * 4, &maps.m[b], c0, (int32_t)(g0 + r0), &full[s]);
+          }
+        } else {
+          for (int r = lane; r < n; r += 32)
+            bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
+        }
+        unsigned char* raw = sreg + coo_raw_off(nnz, n);
+        int32_t* dpair = reinterpret_cast<int32_t*>(raw) + 2 * (nz0 & 1);
+        int32_t* dval = reinterpret_cast<int32_t*>(raw + coo_pairs_bytes(nnz)) + (nz0 & 3);
+        const int32_t* spair = p.idx + 2 * (int64_t)nz0;
+        const int32_t* sval = reinterpret_cast<const int32_t*>(p.vals) + nz0;
+        if (p.sbulk) {  // 16-byte interiors, 8-/4-byte edges
+          const int32_t pa = min(nnz, nz0 & 1), pb = pa + ((nnz - pa) & ~1);  // pairs [pa, pb): 16-byte chunks
+          for (int32_t q = lane; q < ((pb - pa) >> 1); q += 32) cp_async16(dpair + 2 * (pa + 2 * q), spair + 2 * (pa + 2 * q));
+          if (lane == 0 && pa == 1 && nnz > 0) cp_async8(dpair, spair);
+          if (lane == 1 && pb < nnz) cp_async8(dpair + 2 * pb, spair + 2 * pb);
+          const int32_t va = (int32_t)(i64min(nnz, (4 - (nz0 & 3)) & 3)), vb = va + ((nnz - va) & ~3);
+          for (int32_t q = lane; q < ((vb - va) >> 2); q += 32) cp_async16(dval + va + 4 * q, sval + va + 4 * q);
+          if (lane >= 24 && lane < 24 + va) cp_async4(dval + (lane - 24), sval + (lane - 24));
+          if (lane >= 28 && vb + (lane - 28) < nnz) cp_async4(dval + vb + (lane - 28), sval + vb + (lane - 28));
+        } else {
+          for (int32_t e = lane; e < nnz; e += 32) {
+            cp_async4(dpair + 2 * e, spair + 2 * e);
+            cp_async4(dpair + 2 * e + 1, spair + 2 * e + 1);
+            cp_async4(dval + e, sval + e);
+          }
+        }
+      } else if (!fits && lane == 0) {
+        atomicOr(p.err, 64);  // planner hint too small: the unit is skipped, reported by bspmm_sync
+      }
+      if (lane == 0) {
+        UnitHdr h;
+        h.g0 = g0; h.n = n; h.nz0 = nz0; h.nnz = nnz; h.c0 = c0; h.kw = kw;
+        h.flags = fits ? 3 : 4;
+        hdr[s] = h;
+        mbar_arrive(&full[s]);
+      }
+      cp_async_arrive_noinc(&full[s]);
+      return;
+    }
     // a unit is staged whole (tile + structure) or not at all (read from global memory)
     const bool bst = (int64_t)n * kw * 4 <= p.stage_b && slice_bytes(nnz, n) <= p.stage_s && !(p.dbg & 2);
     const bool sst = bst;
-    const float* bsrc = p.B + g0 * p.ldb + c0;
-    unsigned char* sreg = st + p.stage_b;
     if (bst) {
       // a-4 + the CSR slice. Lane 0 announces every TMA byte of the unit once,
       // then issues the copies; the <= 3 unaligned head/tail elements of each
@@ -703,6 +776,66 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
   }
 }
 
+// Fused COO -> CSR of one staged unit (row a-2 inside the SpMM): counting
+// sort by row + rank of the unique key (col, original position) within each
+// row segment -- the same canonical order as coo2csr.cu, so the SpMM that
+// follows is bitwise identical to the two-kernel path.  Consumer warps only
+// (named barrier 1); writes the standard CSR slice layout of the stage.
+__device__ __forceinline__ void consumer_bar(int T) { asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory"); }
+
+__device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& h, unsigned char* st, int t, int T) {
+  unsigned char* sreg = st + p.stage_b;
+  const int32_t nnz = h.nnz, n = h.n, z0 = h.nz0;
+  unsigned char* raw = sreg + coo_raw_off(nnz, n);
+  const int2* pr = reinterpret_cast<const int2*>(raw) + (z0 & 1);
+  const float* rv = reinterpret_cast<const float*>(raw + coo_pairs_bytes(nnz)) + (z0 & 3);
+  int32_t* cursor = reinterpret_cast<int32_t*>(raw + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz));
+  int32_t* slot = cursor + al16(4 * (n + 1)) / 4;
+  int32_t* col = reinterpret_cast<int32_t*>(sreg) + (z0 & 3);
+  float* val = reinterpret_cast<float*>(sreg + slice_region(nnz)) + (z0 & 3);
+  int32_t* rp = reinterpret_cast<int32_t*>(sreg + 2 * slice_region(nnz)) + (h.g0 & 3);
+  for (int32_t r = t; r < n; r += T) cursor[r] = 0;
+  consumer_bar(T);
+  for (int32_t e = t; e < nnz; e += T) atomicAdd(&cursor[pr[e].x], 1);
+  consumer_bar(T);
+  if (t < 32) {  // exclusive scan of the row counts by the first consumer warp
+    int32_t carry = 0;
+    for (int32_t base = 0; base < n; base += 32) {
+      const int32_t r = base + t;
+      const int32_t v = r < n ? cursor[r] : 0;
+      int32_t x = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (t >= d) x += y;
+      }
+      if (r < n) {
+        cursor[r] = carry + x - v;
+        rp[r] = z0 + carry + x - v;
+      }
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (t == 0) rp[n] = z0 + nnz;
+  }
+  consumer_bar(T);
+  for (int32_t e = t; e < nnz; e += T) slot[atomicAdd(&cursor[pr[e].x], 1)] = e;
+  consumer_bar(T);
+  for (int32_t q = t; q < nnz; q += T) {
+    const int32_t e = slot[q];
+    const int2 rc = pr[e];
+    const int32_t s0 = rp[rc.x] - z0, s1 = rp[rc.x + 1] - z0;
+    int32_t rank = 0;
+    for (int32_t f = s0; f < s1; ++f) {
+      const int32_t fe = slot[f];
+      const int32_t cf = pr[fe].y;
+      rank += (cf < rc.y) || (cf == rc.y && fe < e);
+    }
+    col[s0 + rank] = rc.y;
+    val[s0 + rank] = rv[e];  // bitwise move
+  }
+  consumer_bar(T);
+}
+
 template <int CH, bool VEC, bool EPI>
 __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem) {
   const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
@@ -724,8 +857,10 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     const UnitHdr h = hdr[s];
     if (h.flags < 0) break;  // the producer's "done" header
     const unsigned char* st = ring + (size_t)s * stage_bytes;
+    if (p.nnz_off && h.flags == 3)  // fused COO mode: SparseTensor slice -> CSR slice in shared memory
+      coo_convert(p, h, const_cast<unsigned char*>(st), threadIdx.x - 32, W * 32);
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
-    for (int rep = 0; rep < reps; ++rep) {
+    for (int rep = 0; rep < reps && h.flags != 4; ++rep) {  // 4: COO unit over capacity (skipped, flagged)
       if (h.flags == 3) {  // the hot, staged case
         if (VEC && (h.kw >> 2) == p.lanes * CH) rows_staged_full<CH, EPI>(p, h, st, first, step, li);
         else rows<CH, VEC, true, true, EPI>(p, h, st, first, step, li);
@@ -825,7 +960,10 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.bias = a.bias;
   sp.accumulate = a.accumulate;
   const bool sp_epi = a.bias != nullptr || a.accumulate != 0;
-  sp.sched = a.sched;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
+  sp.sched = a.sched;
+  sp.nnz_off = a.coo_nnz_off;
+  sp.idx = a.coo_idx;
+  sp.err = a.err;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {

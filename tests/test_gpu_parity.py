@@ -390,3 +390,27 @@ def test_fused_offsets_adversarial(h):
             C = h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)).cpu().numpy()
             assert_parity(b, C, f"fused offsets trial {trial} kt {kt}")
     h.set_tuning(0, 0, 0, 0)
+
+
+# ------------------------------------------------------------ a-2 fused into the SpMM (bspmm_coo with hints)
+
+@pytest.mark.parametrize("seed", range(5))
+def test_coo_fused_adversarial(h, seed):
+    rng = np.random.default_rng(700 + seed)
+    k = [16, 64, 128, 256, 512][seed]
+    b = synth.random_batch(rng, int(rng.integers(1, 200)), k, nmax=60, dmax=6, duplicates=True)
+    h.set_hints(max(int(b.sizes.max()), 1), max(int(b.nnz.max()), 1))
+    C = h.coo(None, T(b.sizes), T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B)).cpu().numpy()
+    h.sync()
+    orp, ocol, ov = oracle.coo2csr(b.row_off, None, b.nnz_off, b.coo_idx, b.coo_vals)
+    C32 = oracle.spmm_f32(b.k, b.row_off, None, orp, ocol, ov, b.B)
+    assert np.array_equal(C.view(np.uint32), C32.view(np.uint32))
+
+
+def test_coo_fused_hint_too_small_is_reported(h):
+    b = synth.config(3, coo=True)
+    h.set_hints(50, 100)                      # C3 has matrices up to 300 rows / 1500 entries
+    h.coo(T(b.row_off), None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B))
+    with pytest.raises(bs.BspmmError, match="INVALID"):
+        h.sync()
+    h.sync()                                  # the flag is cleared once reported
