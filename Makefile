@@ -12,7 +12,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisi
              -ftz=false -prec-div=true -prec-sqrt=true -Iinclude -Xptxas -v
 LIB       := $(PKG)/libbspmm.so
 CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu $(CSRC)/backward.cu $(CSRC)/spmm_coo_atomic.cu
-HOST_SRCS := $(CSRC)/partition.cpp $(CSRC)/plan.cpp
+HOST_SRCS := $(CSRC)/partition.cpp $(CSRC)/plan.cpp $(CSRC)/multicast.cpp
 HDRS      := include/bspmm.h $(CSRC)/internal.h $(CSRC)/ptx.cuh
 
 all: lib oracle synth

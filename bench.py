@@ -200,6 +200,12 @@ def main():
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--chunks", type=int, default=0)
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the config's batch is sharded over the N GPUs (BASELINE config 5); "
+                         "weak: every rank runs a full batch of its own graphs")
+    ap.add_argument("--allgather", choices=["none", "nccl", "multicast"], default="none",
+                    help="optional reassembly of the full C on every GPU inside the step (off the hot path): "
+                         "NCCL broadcasts, or the multimem store fused into the SpMM (NEXT-4b)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -218,11 +224,19 @@ def main():
     c = synth.CONFIGS[cid]
     seed = synth.BASE_SEED + cid
     # a-7: every rank computes the same split from the per-graph nnz counts
-    n_all, z_all = synth.counts(c["kind"], c["params"], seed, 0, c["batch"])
-    nnz_off_all = np.zeros(c["batch"] + 1, np.int64)
+    # (weak scaling: rank r owns graphs [r*batch, (r+1)*batch) of the seeded stream)
+    gbatch = c["batch"] * (world if args.scaling == "weak" else 1)
+    n_all, z_all = synth.counts(c["kind"], c["params"], seed, 0, gbatch)
+    nnz_off_all = np.zeros(gbatch + 1, np.int64)
     np.cumsum(z_all, out=nnz_off_all[1:])
-    i0, i1 = bdist.shard_of(nnz_off_all, c["k"], rank, world)
-    b = synth.config(cid, i0=i0, i1=i1)
+    row_off_all = np.zeros(gbatch + 1, np.int64)
+    np.cumsum(n_all, out=row_off_all[1:])
+    if args.scaling == "weak":
+        split = np.arange(world + 1, dtype=np.int64) * c["batch"]
+    else:
+        split = bs.partition(nnz_off_all, c["k"], world)
+    i0, i1 = int(split[rank]), int(split[rank + 1])
+    b = synth.generate(c["kind"], c["params"], gbatch, c["k"], seed, i0=i0, i1=i1)
     k = b.k
     h = bs.Handle(dev)
     h.set_hints(int(b.sizes.max()) if b.batch else 0, int(b.nnz.max()) if b.batch else 0)
@@ -231,9 +245,19 @@ def main():
 
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     sizes, row_ptr, col, vals, B = T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)
-    C = torch.empty((b.n_rows, k), dtype=torch.float32, device=dev)
     ro = torch.empty(b.batch + 1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    bounds = bdist.row_bounds(row_off_all, split)
+    row_base = int(bounds[rank])
+    mcbuf, C_full = None, None
+    if args.allgather == "multicast":
+        mcbuf = bdist.mc_team_buffer((int(row_off_all[-1]), k), dev)
+        C = mcbuf.uc[row_base:row_base + b.n_rows]
+    elif args.allgather == "nccl":
+        C_full = torch.empty((int(row_off_all[-1]), k), dtype=torch.float32, device=dev)
+        C = C_full[row_base:row_base + b.n_rows]
+    else:
+        C = torch.empty((b.n_rows, k), dtype=torch.float32, device=dev)
 
     def step(ev=None):
         # what bspmm_csr(row_off=NULL, sizes) does for a batch this large, as two
@@ -241,9 +265,16 @@ def main():
         h.build_offsets(sizes, out=ro)                    # a-1 (look-back scan kernel)
         if ev is not None:
             ev[0].record(stream)
-        h.csr(ro, None, row_ptr, col, vals, B, C)         # a-3..a-6
+        if mcbuf is not None:                             # a-3..a-6, C stored to every GPU
+            h.csr_multicast(ro, None, row_ptr, col, vals, B, mcbuf, row_base=row_base)
+        else:
+            h.csr(ro, None, row_ptr, col, vals, B, C)     # a-3..a-6
         if ev is not None:
             ev[1].record(stream)
+        if mcbuf is not None:
+            bdist.team_barrier(dev)
+        elif C_full is not None:
+            bdist.allgather_rows(C_full, bounds)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -270,7 +301,7 @@ def main():
     NNZ_total = int(nnz_off_all[-1])
     N_total = int(n_all.sum())
     flops = 2.0 * NNZ_total * k
-    bytes_step = alg_bytes(N_total, NNZ_total, k, c["batch"]) + offsets_bytes(c["batch"])
+    bytes_step = alg_bytes(N_total, NNZ_total, k, gbatch) + offsets_bytes(gbatch)
     value = flops / (ms / 1e3) / 1e9
     hbm_gbs = bytes_step / (ms / 1e3) / 1e9
     peak, peak_src = peaks()
@@ -289,7 +320,9 @@ def main():
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         hs, hrp, hc, hv, hB = pin(b.sizes), pin(b.row_ptr), pin(b.col), pin(b.vals), pin(b.B)
         hC = torch.empty((b.n_rows, k), dtype=torch.float32).pin_memory()
-        del C, B
+        del C, B, C_full
+        if mcbuf is not None:
+            mcbuf.close()
         torch.cuda.empty_cache()
         h.csr_host(hs, hrp, hc, hv, hB, hC)              # warm-up (allocates the device mirror)
         bdist.barrier(dev)
@@ -312,10 +345,13 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-mol graphs, U[-1,1) values)",
-            "config": {"workload": synth.CONFIG_NAMES[cid], "global_batch": c["batch"], "k": k,
-                       "rows": N_total, "nnz": NNZ_total, "parallelism": f"batch-sharded x{world} (nnz*k split)",
+            "config": {"workload": synth.CONFIG_NAMES[cid], "global_batch": gbatch, "k": k,
+                       "rows": N_total, "nnz": NNZ_total,
+                       "parallelism": (f"batch-sharded x{world} (nnz*k split)" if args.scaling == "strong"
+                                       else f"x{world} independent batches"),
+                       "allgather": args.allgather,
                        "l2": "inputs larger than L2 (no flush needed)", "plan": plan},
             "hbm_gbs": hbm_gbs, "hbm_frac_of_measured": hbm_gbs / peak,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -46,12 +46,15 @@
  *    B and C (float4 lanes, TMA bulk staging).  Anything else runs the scalar
  *    path; that is not an error.
  *  - A handle is not thread-safe; distinct handles are independent.
- *  - Multi-GPU: no ABI change.  One handle per rank/device, called on the
- *    rank's contiguous sub-batch (bspmm_partition), offsets rebased to 0.
+ *  - Multi-GPU: no ABI change on the hot path.  One handle per rank/device,
+ *    called on the rank's contiguous sub-batch (bspmm_partition), offsets
+ *    rebased to 0.  Optional reassembly of the full C on every GPU is fused
+ *    into the store (bspmm_csr_multicast + the bspmm_mc_* team buffers).
  */
 #ifndef BSPMM_H_
 #define BSPMM_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -65,6 +68,7 @@ extern "C" {
 #endif
 
 typedef struct bspmm_handle_s* bspmm_handle_t;
+typedef struct bspmm_mc_s* bspmm_mc_t; /* NVSwitch multicast team buffer (NEXT-4b) */
 
 typedef enum {
   BSPMM_SUCCESS = 0,
@@ -166,6 +170,45 @@ BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h);
 BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
                                    const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
                                    const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc);
+
+/* bspmm_csr with the all-gather of C fused into the store (SURVEY §8(e)
+ * optional reassembly, §8(f) NEXT-4b; the paper is single-GPU):
+ * identical arithmetic and bits, but every C row is written with ONE
+ * multimem.st to `C_mc`, an address inside the MULTICAST range of a team
+ * buffer (bspmm_mc_bind), so it lands in the bound buffer of every GPU of the
+ * team.  Rank r passes C_mc = mc_ptr + row_base_r * ldc * 4 bytes for its
+ * shard (the shard's own offsets start at 0) and, after the call, a barrier
+ * over the team (e.g. an NCCL all_reduce on the same stream) makes the full C
+ * readable through each rank's UNICAST pointer.  The kernel ends with a
+ * system-scope fence.  Same arguments and errors as bspmm_csr; C_mc must not
+ * be an ordinary allocation (undefined behaviour). */
+BSPMM_API bspmm_status_t bspmm_csr_multicast(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                             const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
+                                             const float* vals, const float* B, int64_t ldb, float* C_mc,
+                                             int64_t ldc);
+
+/* ---- NVSwitch multicast team buffers (NEXT-4b) ------------------------ *
+ * A team of num_devices GPUs (one process per GPU, or num_devices = 1) shares
+ * one buffer of >= bytes (rounded up to the multicast granularity).
+ * Protocol: the root calls bspmm_mc_create (exportable = 1 when num_devices >
+ * 1: *fd_out receives a POSIX file descriptor the caller sends to the other
+ * ranks, e.g. SCM_RIGHTS); every other rank calls bspmm_mc_import with it.
+ * Both add the caller's `device` to the team.  After ALL members have joined
+ * (a barrier), each calls bspmm_mc_bind: it allocates `bytes` on its device,
+ * binds them and returns the unicast (own copy, ordinary loads/stores) and
+ * multicast (stores reach every member) device pointers.  Barrier again
+ * before the first multicast store.  bspmm_mc_destroy unmaps and frees (NULL
+ * ok).  Errors: INVALID_VALUE, NOT_SUPPORTED (no NVSwitch multicast on this
+ * device / driver), OUT_OF_MEMORY, CUDA.  The caller owns the fd. */
+BSPMM_API int32_t bspmm_mc_supported(int device);
+BSPMM_API bspmm_status_t bspmm_mc_create(int device, int num_devices, size_t bytes, int exportable,
+                                         bspmm_mc_t* out, int* fd_out);
+BSPMM_API bspmm_status_t bspmm_mc_import(int device, int num_devices, size_t bytes, int fd, bspmm_mc_t* out);
+BSPMM_API bspmm_status_t bspmm_mc_bind(bspmm_mc_t mc, void** uc_ptr, void** mc_ptr);
+BSPMM_API size_t bspmm_mc_bytes(bspmm_mc_t mc);
+/* Which driver call failed last in this thread (bspmm_mc_* only). */
+BSPMM_API const char* bspmm_mc_last_error(void);
+BSPMM_API bspmm_status_t bspmm_mc_destroy(bspmm_mc_t mc);
 
 /* Batched COO / SparseTensor SpMM (Fig.
  * algo:code_swa_spmm_st).  The entries of A_i are [nnz_off[i], nnz_off[i+1])

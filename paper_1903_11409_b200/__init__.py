@@ -21,8 +21,8 @@ import torch
 from . import _lib
 from ._lib import BspmmError, Plan, lib
 
-__all__ = ["Handle", "BspmmError", "Plan", "partition", "subwarp", "plan", "default_handle", "header_symbols",
-           "LIB_PATH"]
+__all__ = ["Handle", "BspmmError", "Plan", "McBuffer", "mc_supported", "mc_available", "partition", "subwarp", "plan",
+           "default_handle", "header_symbols", "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
 header_symbols = _lib.header_symbols
@@ -58,6 +58,90 @@ def _ld(t: torch.Tensor, k: int, name: str) -> int:
     if t.stride(1) != 1 and t.shape[1] > 1:
         raise ValueError(f"{name} needs unit column stride")
     return max(int(t.stride(0)), k) if t.shape[0] > 1 else max(int(t.shape[1]), k)
+
+
+def mc_supported(device: int = 0) -> bool:
+    """The device reports NVSwitch multicast (bspmm_mc_supported)."""
+    return bool(lib.bspmm_mc_supported(int(device)))
+
+
+_mc_probe: dict = {}
+
+
+def mc_available(device: int = 0):
+    """(ok, why): can a multicast team buffer actually be created here?  A
+    device may report support while the driver refuses the object (e.g. one
+    GPU of an NVSwitch box passed through to a container)."""
+    if device not in _mc_probe:
+        if not mc_supported(device):
+            _mc_probe[device] = (False, "device reports no multicast support")
+        else:
+            try:
+                McBuffer((1, 1), device).close()
+                _mc_probe[device] = (True, "")
+            except BspmmError as e:
+                _mc_probe[device] = (False, str(e))
+    return _mc_probe[device]
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of library-owned device memory (zero copy)."""
+
+    def __init__(self, ptr: int, shape, owner):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+        self._owner = owner
+
+
+class McBuffer:
+    """fp32 [rows, cols] NVSwitch multicast team buffer (bspmm_mc_*, NEXT-4b).
+
+    `uc` is this GPU's copy as a torch tensor (ordinary reads/writes);
+    `mc_ptr` is the multicast address: a store there reaches every GPU of the
+    team.  Single process: McBuffer(shape, device).  One process per GPU: use
+    dist.mc_team_buffer, which passes the exported handle between ranks."""
+
+    def __init__(self, shape, device, num_devices: int = 1, fd: Optional[int] = None, export: bool = False,
+                 bind: bool = True):
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.shape = (int(shape[0]), int(shape[1]))
+        nbytes = max(4 * self.shape[0] * self.shape[1], 4)
+        self._m = ctypes.c_void_p()
+        self.fd = None
+        if fd is None:
+            cfd = ctypes.c_int(-1)
+            st = lib.bspmm_mc_create(self.device.index, int(num_devices), nbytes, 1 if export else 0,
+                                     ctypes.byref(self._m), ctypes.byref(cfd))
+            if st != _lib.SUCCESS:
+                raise BspmmError(st, "bspmm_mc_create", lib.bspmm_mc_last_error().decode())
+            self.fd = cfd.value if export else None
+        else:
+            st = lib.bspmm_mc_import(self.device.index, int(num_devices), nbytes, int(fd), ctypes.byref(self._m))
+            if st != _lib.SUCCESS:
+                raise BspmmError(st, "bspmm_mc_import", lib.bspmm_mc_last_error().decode())
+        self.nbytes = int(lib.bspmm_mc_bytes(self._m))
+        self.uc = None
+        self.mc_ptr = 0
+        if bind:
+            self.bind()
+
+    def bind(self):
+        """Allocate and bind this GPU's memory; call after every team member joined."""
+        uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+        st = lib.bspmm_mc_bind(self._m, ctypes.byref(uc), ctypes.byref(mc))
+        if st != _lib.SUCCESS:
+            raise BspmmError(st, "bspmm_mc_bind", lib.bspmm_mc_last_error().decode())
+        self.mc_ptr = int(mc.value)
+        self.uc = torch.as_tensor(_CudaArray(int(uc.value), self.shape, self), device=self.device)
+
+    def close(self):
+        if getattr(self, "_m", None) is not None and self._m.value:
+            self.uc = None
+            lib.bspmm_mc_destroy(self._m)
+            self._m = None
+
+    def __del__(self):
+        self.close()
 
 
 class Handle:
@@ -152,6 +236,44 @@ class Handle:
                            _ptr(B), ldb, _ptr(C), ldc)
         self._raise(st, "bspmm_csr")
         return C
+
+    def csr_multicast(self, row_off: Optional[torch.Tensor], sizes: Optional[torch.Tensor], row_ptr: torch.Tensor,
+                      col: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, out, row_base: int = 0,
+                      k: Optional[int] = None, batch: Optional[int] = None) -> None:
+        """bspmm_csr with the all-gather fused into the store (NEXT-4b): this
+        shard's C rows land at global rows row_base.. of `out` (an McBuffer) on
+        EVERY GPU of the multicast team.  A team barrier must follow before
+        reading out.uc (dist.team_barrier).  `out` may also be an ordinary fp32
+        tensor: the tests' unicast emulation on boxes where the driver refuses
+        multicast objects (on sm_100a multimem.st lowers to the plain STG.E.128
+        of the same address; not a supported use)."""
+        dev = self.device
+        for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
+                            ("row_ptr", row_ptr, torch.int32), ("col", col, torch.int32),
+                            ("vals", vals, torch.float32), ("B", B, torch.float32)):
+            _check(t, name, dt, dev)
+        if isinstance(out, torch.Tensor):
+            _check(out, "out", torch.float32, dev, 2)
+            if out.stride(1) != 1 or not out.is_contiguous():
+                raise ValueError("out must be contiguous")
+            base_ptr = out.data_ptr()
+        else:
+            base_ptr = out.mc_ptr
+        if out.device != dev:
+            raise ValueError("multicast buffer is on another device")
+        if batch is None:
+            batch = (row_off.shape[0] - 1) if row_off is not None else sizes.shape[0]
+        if k is None:
+            k = B.shape[1]
+        ldc = out.shape[1]
+        rows = int(B.shape[0])
+        if ldc < k or row_base < 0 or (row_base + rows) > out.shape[0]:
+            raise ValueError("shard rows / k do not fit the multicast buffer")
+        ldb = _ld(B, k, "B")
+        self._stream()
+        st = lib.bspmm_csr_multicast(self._h, batch, k, _ptr(row_off), _ptr(sizes), _ptr(row_ptr), _ptr(col),
+                                     _ptr(vals), _ptr(B), ldb, ctypes.c_void_p(base_ptr + 4 * row_base * ldc), ldc)
+        self._raise(st, "bspmm_csr_multicast")
 
     def coo(self, row_off: Optional[torch.Tensor], sizes: Optional[torch.Tensor], nnz_off: torch.Tensor,
             idx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None,

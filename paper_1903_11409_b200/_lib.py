@@ -35,6 +35,15 @@ _SIGS = {
     "bspmm_set_trace": (I32, [P, P]),
     "bspmm_set_debug": (I32, [P, I32]),
     "bspmm_csr": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
+    "bspmm_csr_multicast": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
+    "bspmm_mc_supported": (I32, [ctypes.c_int]),
+    "bspmm_mc_create": (I32, [ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(P),
+                              ctypes.POINTER(ctypes.c_int)]),
+    "bspmm_mc_import": (I32, [ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(P)]),
+    "bspmm_mc_bind": (I32, [P, ctypes.POINTER(P), ctypes.POINTER(P)]),
+    "bspmm_mc_bytes": (ctypes.c_size_t, [P]),
+    "bspmm_mc_last_error": (ctypes.c_char_p, []),
+    "bspmm_mc_destroy": (I32, [P]),
     "bspmm_coo": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64, I64, I64, P, P, P]),
     "bspmm_coo2csr": (I32, [P, I32, P, P, P, P, P, I64, I64, P, P, P]),
     "bspmm_coo_atomic": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),

@@ -315,7 +315,8 @@ BSPMM_API bspmm_status_t bspmm_build_offsets(bspmm_handle_t h, int32_t batch, co
 static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
                                const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
                                const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc,
-                               bool validate, const float* bias = nullptr, int32_t accumulate = 0) {
+                               bool validate, const float* bias = nullptr, int32_t accumulate = 0,
+                               int32_t mc = 0) {
   if (validate) {
     CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
     CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr, col_idx, h->dev_flag, h->stream));
@@ -333,14 +334,15 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   h->last_plan = plan;
   CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias, accumulate,
             plan.sched ? h->dev_sched : nullptr};
+  a.mc = mc;
   CK(h, launch_spmm_csr(a, plan, h->stream));
   if (plan.units > 0) h->launches++;
   return BSPMM_SUCCESS;
 }
 
-BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
-                                   const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
-                                   const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc) {
+static bspmm_status_t csr_entry(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
+                                const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc, int32_t mc) {
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
   if (batch < 0 || k < 1 || ldb < k || ldc < k) return fail(h, BSPMM_ERROR_INVALID_VALUE, "batch<0, k<1 or ld<k");
   if (batch == 0) return BSPMM_SUCCESS;
@@ -354,7 +356,7 @@ BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, c
     int64_t* ro = static_cast<int64_t*>(h->ws);
     st = bspmm_build_offsets(h, batch, sizes, ro);
     if (st != BSPMM_SUCCESS) return st;
-    return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc, true);
+    return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc, true, nullptr, 0, mc);
   }
   if (!row_off) {
     // row_off == NULL: small batches (every CTA's units fit one metadata batch)
@@ -373,11 +375,24 @@ BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, c
       int64_t* ro = static_cast<int64_t*>(h->ws);
       st = bspmm_build_offsets(h, batch, sizes, ro);
       if (st != BSPMM_SUCCESS) return st;
-      return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc, false);
+      return csr_impl(h, batch, k, ro, nullptr, row_ptr, col_idx, vals, B, ldb, C, ldc, false, nullptr, 0, mc);
     }
   }
   return csr_impl(h, batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc,
-                  (h->flags & BSPMM_VALIDATE) != 0);
+                  (h->flags & BSPMM_VALIDATE) != 0, nullptr, 0, mc);
+}
+
+BSPMM_API bspmm_status_t bspmm_csr(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                   const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
+                                   const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc) {
+  return csr_entry(h, batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, 0);
+}
+
+BSPMM_API bspmm_status_t bspmm_csr_multicast(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
+                                             const int32_t* sizes, const int32_t* row_ptr, const int32_t* col_idx,
+                                             const float* vals, const float* B, int64_t ldb, float* C_mc,
+                                             int64_t ldc) {
+  return csr_entry(h, batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C_mc, ldc, 1);
 }
 
 // workspace layout for the COO path: [row_off][row_ptr][col][val][keys x2][pay x2]

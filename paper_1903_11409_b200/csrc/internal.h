@@ -66,6 +66,7 @@ struct CsrArgs {
   const int64_t* coo_nnz_off = nullptr; // fused COO mode: per-matrix entry offsets (col/vals = raw COO)
   const int32_t* coo_idx = nullptr;     // fused COO mode: (row, col) pairs
   int* err = nullptr;                   // device error flag (bit 64: COO unit over stage capacity)
+  int32_t mc = 0;                       // NEXT-4b: C is a multicast VA (multimem.st epilogue)
 };
 
 // kernels (.cu)

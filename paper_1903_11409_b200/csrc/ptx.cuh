@@ -120,4 +120,15 @@ __device__ __forceinline__ void stg_cs_f1(float* p, float v) {
   asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
+// NVSwitch multicast stores (NEXT-4b): `p` is an address in a multicast
+// object's VA range; the store lands in the bound buffer of every device of
+// the team (SASS: ST.E... on a multicast address, issued once).
+__device__ __forceinline__ void mm_st_f4(float* p, float4 v) {
+  asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st_f1(float* p, float v) {
+  asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 }  // namespace bspmm

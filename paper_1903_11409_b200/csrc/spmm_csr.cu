@@ -59,14 +59,15 @@ struct SpmmParams {
   const int64_t* __restrict__ nnz_off;
   const int32_t* __restrict__ idx;   // [nnz][2] (row, col) local pairs
   int* err;                          // device flag: bit 64 = a unit exceeded the stage (hint too small)
+  int32_t mc;                        // NEXT-4b: C is a multicast address (EPI == 2: multimem.st stores)
 };
 
 // GCN epilogue (NEXT-1, PAPER.md Fig. algo:graph_conv_batched): A (U + 1 b^T)
 // = A U + rowsum(A) b^T, so the bias add folds into the SpMM as rs * b after
 // the storage-order sum; channels accumulate into C.
-template <bool EPI, bool VEC>
+template <int EPI, bool VEC>
 __device__ __forceinline__ void epilogue(const SpmmParams& p, float4& acc, float rs, int64_t colf, const float* cptr) {
-  if (!EPI) return;
+  if (EPI != 1) return;
   if (p.bias) {
     if (VEC) {
       const float4 b = ldg_nc_f4(p.bias + colf);
@@ -88,6 +89,20 @@ __device__ __forceinline__ void epilogue(const SpmmParams& p, float4& acc, float
     } else {
       acc.x += *cptr;
     }
+  }
+}
+
+// a-6 store of one chunk: streaming st.global, or (EPI == 2, NEXT-4b) one
+// multimem store that writes the row of C into every GPU of the
+// multicast team -- the all-gather of the sharded C done by the store itself.
+template <int EPI, bool VEC>
+__device__ __forceinline__ void store_c(const SpmmParams& p, float* ptr, const float4& acc) {
+  if (EPI == 2) {
+    if (VEC) mm_st_f4(ptr, acc);
+    else mm_st_f1(ptr, acc.x);
+  } else {
+    if (VEC) stg_cs_f4(ptr, acc);
+    else stg_cs_f1(ptr, acc.x);
   }
 }
 
@@ -547,7 +562,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
 // then accumulated strictly in storage order, so the result is bitwise the
 // fp32 storage-order FMA sum (O3').  Per-unit address math is hoisted; the
 // row loop touches shared memory with 32-bit offsets only.
-template <int CH, bool VEC, bool BST, bool SST, bool EPI>
+template <int CH, bool VEC, bool BST, bool SST, int EPI>
 __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
                                      int step, int li) {
   constexpr int G = CH >= 4 ? 2 : 4;
@@ -616,7 +631,7 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
 #pragma unroll
       for (int q = 0; q < G; ++q) {
         if (q < cnt) {
-          if (EPI) rs += a[q];
+          if (EPI == 1) rs += a[q];
 #pragma unroll
           for (int v = 0; v < CH; ++v) {
             acc[v].x = fmaf(a[q], b[q][v].x, acc[v].x);
@@ -638,8 +653,7 @@ __device__ __forceinline__ void rows(const SpmmParams& p, const UnitHdr& h, cons
     for (int v = 0; v < CH; ++v) {
       if (ok[v]) {
         epilogue<EPI, VEC>(p, acc[v], rs, h.c0 + FW * (li + v * L), crow + FW * v * L);
-        if (VEC) stg_cs_f4(crow + FW * v * L, acc[v]);
-        else stg_cs_f1(crow + v * L, acc[v].x);
+        store_c<EPI, VEC>(p, crow + FW * v * L, acc[v]);
       }
     }
   }
@@ -664,7 +678,7 @@ __device__ __forceinline__ void fma4(float4& acc, float a, const float4& b) {
 // (cols == lanes * CH, float4 chunks): no per-chunk predicates, 32-bit shared
 // addressing, two entries per iteration (independent loads first, FMAs in
 // storage order).  Same arithmetic as rows<> (bitwise O3').
-template <int CH, bool EPI>
+template <int CH, int EPI>
 __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const UnitHdr& h, const unsigned char* st,
                                                  int first, int step, int li) {
   const int L = p.lanes;
@@ -707,12 +721,12 @@ __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const Unit
       for (int v = 0; v < CH; ++v) fma4(acc[v], a0, x0[v]);
 #pragma unroll
       for (int v = 0; v < CH; ++v) fma4(acc[v], a1, x1[v]);
-      if (EPI) rs += a0, rs += a1;
+      if (EPI == 1) rs += a0, rs += a1;
     }
     if (e < e1) {
       const int32_t c0 = ci[e];
       const float a0 = cv[e];
-      if (EPI) rs += a0;
+      if (EPI == 1) rs += a0;
       const uint32_t p0 = sB + (uint32_t)c0 * pitch;
 #pragma unroll
       for (int v = 0; v < CH; ++v) fma4(acc[v], a0, lds128(p0 + v * vstep));
@@ -725,12 +739,12 @@ __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const Unit
 #pragma unroll
     for (int v = 0; v < CH; ++v) {
       epilogue<EPI, true>(p, acc[v], rs, h.c0 + 4 * (li + v * L), crow + 4 * v * L);
-      stg_cs_f4(crow + 4 * v * L, acc[v]);
+      store_c<EPI, true>(p, crow + 4 * v * L, acc[v]);
     }
   }
 }
 
-template <int CH, bool VEC, bool EPI>
+template <int CH, bool VEC, int EPI>
 __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& h, int first, int step, int li) {
   constexpr int FW = VEC ? 4 : 1;
   const int L = p.lanes;
@@ -747,7 +761,7 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
     for (int32_t e = e0; e < e1; ++e) {
       const int32_t c = __ldg(p.col + e);
       const float a = __ldg(p.vals + e);
-      if (EPI) rs += a;
+      if (EPI == 1) rs += a;
       const float* brow = Bt + (int64_t)c * p.ldb;
 #pragma unroll
       for (int v = 0; v < CH; ++v) {
@@ -769,8 +783,7 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
     for (int v = 0; v < CH; ++v) {
       if (li + v * L < cols) {
         epilogue<EPI, VEC>(p, acc[v], rs, h.c0 + FW * (li + v * L), crow + FW * v * L);
-        if (VEC) stg_cs_f4(crow + FW * v * L, acc[v]);
-        else stg_cs_f1(crow + v * L, acc[v].x);
+        store_c<EPI, VEC>(p, crow + FW * v * L, acc[v]);
       }
     }
   }
@@ -836,7 +849,7 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
   consumer_bar(T);
 }
 
-template <int CH, bool VEC, bool EPI>
+template <int CH, bool VEC, int EPI>
 __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem) {
   const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -872,10 +885,13 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     if (lane == 0) mbar_arrive(&empty[s]);
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 8);
   }
+  // multicast stores: make them visible system-wide before the caller's
+  // cross-GPU barrier (which follows this kernel on the stream)
+  if (EPI == 2) __threadfence_system();
   if (cw == 0 && lane == 0) BSPMM_TRACE(p, 6);
 }
 
-template <int CH, bool VEC, bool EPI>
+template <int CH, bool VEC, int EPI>
 __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -903,7 +919,7 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
   }
 }
 
-template <int CH, bool VEC, bool EPI>
+template <int CH, bool VEC, int EPI>
 static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bspmm_plan_t& plan, cudaStream_t s) {
   auto kern = spmm_csr_kernel<CH, VEC, EPI>;
   static thread_local int configured_bytes[64] = {};  // per device
@@ -925,6 +941,14 @@ static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bsp
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, sp, maps);
+}
+
+template <int CH, bool VEC>
+static cudaError_t launch_e(int epi, const SpmmParams& sp, const TmaMaps& maps, const bspmm_plan_t& plan,
+                            cudaStream_t s) {
+  if (epi == 2) return launch_t<CH, VEC, 2>(sp, maps, plan, s);
+  if (epi == 1) return launch_t<CH, VEC, 1>(sp, maps, plan, s);
+  return launch_t<CH, VEC, 0>(sp, maps, plan, s);
 }
 
 cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s) {
@@ -959,7 +983,9 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.slice_lsu = (plan.units <= 32LL * plan.grid && !(a.dbg & 32)) ? 1 : 0;
   sp.bias = a.bias;
   sp.accumulate = a.accumulate;
-  const bool sp_epi = a.bias != nullptr || a.accumulate != 0;
+  sp.mc = a.mc;
+  // epilogue variant: 0 plain store, 1 GCN (bias / accumulate), 2 multicast store
+  const int epi = a.mc ? 2 : (a.bias != nullptr || a.accumulate != 0) ? 1 : 0;
   sp.sched = a.sched;
   sp.nnz_off = a.coo_nnz_off;
   sp.idx = a.coo_idx;
@@ -968,15 +994,15 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
     switch (plan.chunks) {
-      case 1: return sp_epi ? launch_t<1, true, true>(sp, maps, plan, s) : launch_t<1, true, false>(sp, maps, plan, s);
-      case 2: return sp_epi ? launch_t<2, true, true>(sp, maps, plan, s) : launch_t<2, true, false>(sp, maps, plan, s);
-      default: return sp_epi ? launch_t<4, true, true>(sp, maps, plan, s) : launch_t<4, true, false>(sp, maps, plan, s);
+      case 1: return launch_e<1, true>(epi, sp, maps, plan, s);
+      case 2: return launch_e<2, true>(epi, sp, maps, plan, s);
+      default: return launch_e<4, true>(epi, sp, maps, plan, s);
     }
   }
   switch (plan.chunks) {
-    case 1: return sp_epi ? launch_t<1, false, true>(sp, maps, plan, s) : launch_t<1, false, false>(sp, maps, plan, s);
-    case 2: return sp_epi ? launch_t<2, false, true>(sp, maps, plan, s) : launch_t<2, false, false>(sp, maps, plan, s);
-    default: return sp_epi ? launch_t<4, false, true>(sp, maps, plan, s) : launch_t<4, false, false>(sp, maps, plan, s);
+    case 1: return launch_e<1, false>(epi, sp, maps, plan, s);
+    case 2: return launch_e<2, false>(epi, sp, maps, plan, s);
+    default: return launch_e<4, false>(epi, sp, maps, plan, s);
   }
 }
 

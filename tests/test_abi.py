@@ -3,6 +3,8 @@ include/bspmm.h declares, rejects bad arguments, and its host-only functions
 (partition, subWarp rule, planner) agree with the oracle / the paper.
 No compute call touches a GPU here."""
 import ctypes
+import os
+import re
 
 import numpy as np
 import pytest
@@ -131,3 +133,25 @@ def test_plan_paper_shapes():
     # C5: whole rows, one unit per matrix
     p = bs.plan(256, 65536, max_rows=60)
     assert p["tiles"] == 1 and p["stages"] >= 2
+
+
+def test_multimem_store_sass():
+    """The multicast-store kernel variant (EPI = 2, NEXT-4b) writes C with the
+    same 128-bit STG as the plain kernel minus the evict-first hint: on sm_100a
+    multimem.st is an ordinary store whose fan-out comes from the multicast VA
+    mapping.  This is what lets the GPU tests check that variant by unicast
+    emulation where the driver refuses multicast objects."""
+    import shutil
+    import subprocess
+    if shutil.which("cuobjdump") is None and not os.path.exists("/usr/local/cuda/bin/cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+
+    def stores(mangled):
+        out = subprocess.run([exe, "-sass", "-fun", mangled, bs.LIB_PATH], capture_output=True, text=True).stdout
+        return set(re.findall(r"\bSTG\.E[.A-Z0-9]*\.128\b", out))
+
+    mc = stores("_ZN5bspmm15spmm_csr_kernelILi2ELb1ELi2EEEvNS_10SpmmParamsENS_7TmaMapsE")
+    plain = stores("_ZN5bspmm15spmm_csr_kernelILi2ELb1ELi0EEEvNS_10SpmmParamsENS_7TmaMapsE")
+    assert mc == {"STG.E.128"}, mc
+    assert plain == {"STG.E.EF.128"}, plain
