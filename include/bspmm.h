@@ -128,17 +128,18 @@ BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t 
                                           int32_t ctas_per_sm, int32_t chunks);
 
 /* Debug: per-CTA phase timestamps (%globaltimer, ns) of subsequent SpMM
- * launches are written to dev_buf [grid x 16] uint64 (slots: entry, after the
+ * launches are written to dev_buf [grid x 32] uint64 (slots: entry, after the
  * programmatic-launch wait, producer has unit-0 offsets, producer has unit-0
  * structure, producer done, first consumer warp sees unit 0, first consumer
- * warp done, CTA exit, first consumer warp done with unit 0).  NULL disables
+ * warp done, CTA exit, first consumer warp done with unit 0; 9-15 and 16-27
+ * producer issue steps of the first units, see spmm_csr.cu).  NULL disables
  * (the default). */
 BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
 
 /* Debug: timing-experiment bits for subsequent SpMM launches.  1 = compute but
  * do not store C (the result is then undefined); 2 = compute every unit from
  * global memory (no staging); 8 = consumers repeat each unit's work 4 times;
- * 16 = L2-prefetch every unit of small problems up front; 32 = always copy
+ * 16 = (unused; was an L2 prefetch of small problems, no gain); 32 = always copy
  * the CSR slice with TMA; 64 = force the static unit schedule; 128 = force the
  * dynamic one.  0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);

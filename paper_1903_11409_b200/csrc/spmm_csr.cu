@@ -49,7 +49,6 @@ struct SpmmParams {
   int32_t dbg;                // debug bits: 1 skip C stores, 2 unit direct, 8 consumer work x4 (experiments)
   int32_t tma2d;              // 1: full k-tiles staged with 2-D tensor TMA (maps valid)
   int32_t sbulk;              // 1: col / vals / row_ptr bases are 16-byte aligned (bulk-copy the CSR slice)
-  int32_t prefetch;           // 1: L2-prefetch every unit of a batch up front (small problems)
   int32_t slice_lsu;          // 1: CSR slice by 16-byte cp.async instead of TMA bulk (small problems)
   const float* __restrict__ bias;  // GCN epilogue (NEXT-1): C += rowsum(A) (x) bias[c0..], or null
   int32_t accumulate;              // GCN epilogue: C += previous C (channel accumulation)
@@ -129,7 +128,7 @@ __host__ __device__ __forceinline__ int64_t coo_stage_bytes(int64_t nnz, int64_t
 // offsets, 3 producer has unit-0 structure offsets, 4 producer issued its last unit, 5 first
 // consumer warp saw unit 0 land, 6 first consumer warp finished its last unit, 7 CTA exit,
 // 8 first consumer warp finished unit 0
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 32;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -229,6 +228,7 @@ __device__ __forceinline__ int64_t fused_prefix_start(const SpmmParams& p, int l
 }
 
 // round trip 1 for unit uu: row offset (or the fused prefix g0f), rows, tile
+template <bool COO>
 __device__ __forceinline__ void meta_rt1(const SpmmParams& p, int64_t uu, Meta& m, int64_t g0f = -1) {
   if (uu < p.units) {
     const int64_t i = uu / p.tiles;
@@ -237,7 +237,7 @@ __device__ __forceinline__ void meta_rt1(const SpmmParams& p, int64_t uu, Meta& 
     m.n = p.sizes ? p.sizes[i] : (int32_t)(p.row_off[i + 1] - m.g0);
     m.c0 = t * p.kt;
     m.kw = min(p.kt, p.k - m.c0);
-    if (p.nnz_off) {  // fused COO mode: the entry range comes with round trip 1
+    if (COO) {  // fused COO mode: the entry range comes with round trip 1
       m.nz0 = (int32_t)p.nnz_off[i];
       m.nz1 = (int32_t)p.nnz_off[i + 1];
     }
@@ -246,8 +246,9 @@ __device__ __forceinline__ void meta_rt1(const SpmmParams& p, int64_t uu, Meta& 
   }
 }
 // round trip 2: the matrix's entry range (depends on round trip 1)
+template <bool COO>
 __device__ __forceinline__ void meta_rt2(const SpmmParams& p, int64_t uu, Meta& m) {
-  if (p.nnz_off) return;  // fused COO mode: no row pointers
+  if (COO) return;  // fused COO mode: no row pointers
   if (uu < p.units) {
     m.nz0 = p.row_ptr[m.g0];
     m.nz1 = p.row_ptr[m.g0 + m.n];
@@ -258,7 +259,7 @@ __device__ __forceinline__ void meta_rt2(const SpmmParams& p, int64_t uu, Meta& 
 
 // Stage unit j of this CTA (metadata already known): wait for its ring stage,
 // TMA/cp.async the B tile and CSR slice, publish the header, arrive on "full".
-template <bool VEC>
+template <bool VEC, bool COO>
 __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem, int j,
                                            int64_t g0, int32_t n, int32_t c0, int32_t kw, int32_t nz0, int32_t nnz) {
   UnitHdr* hdr = reinterpret_cast<UnitHdr*>(smem);
@@ -272,10 +273,11 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
     const uint32_t phase = (uint32_t)(j / p.stages) & 1u;
     mbar_wait(&empty[s], phase ^ 1u);
     if (j == 0 && lane == 0) BSPMM_TRACE(p, 9);
+    if (j < 3 && lane == 0) BSPMM_TRACE(p, 16 + 4 * j);
     unsigned char* st = ring + (size_t)s * stage_bytes;
     const float* bsrc = p.B + g0 * p.ldb + c0;
     unsigned char* sreg = st + p.stage_b;
-    if (p.nnz_off) {  // fused COO mode: B tile + the raw SparseTensor slice
+    if (COO) {  // fused COO mode: B tile + the raw SparseTensor slice
       const bool fits = (int64_t)n * kw * 4 <= p.stage_b && coo_stage_bytes(nnz, n) <= p.stage_s;
       if (fits && n > 0) {
         if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)n * (uint32_t)kw * 4u);
@@ -375,6 +377,8 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
         }
         for (int32_t q = lane; q < nrp4; q += 32) cp_async16(drp + a_rp + 4 * q, p.row_ptr + r_lo + a_rp + 4 * q);
       }
+      if (p.trace) __syncwarp();
+      if (j < 3 && lane == 0) BSPMM_TRACE(p, 17 + 4 * j);
       if (b_bulk) {  // TMA: whole contiguous B_i (1-D), a full k-tile (2-D boxes), else one bulk copy per row
         if (kw == p.ldb) {
           if (lane == 3) bulk_g2s_hint(st, bsrc, (uint32_t)n * (uint32_t)kw * 4u, &full[s], pol);
@@ -393,7 +397,9 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
             bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
         }
       }
+      if (p.trace) __syncwarp();
       if (j == 0 && lane == 0) BSPMM_TRACE(p, 10);
+      if (j < 3 && lane == 0) BSPMM_TRACE(p, 18 + 4 * j);
       if (!VEC) {
         float* dst = reinterpret_cast<float*>(st);
         const int32_t total = n * kw;
@@ -423,6 +429,8 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
         for (int32_t r = lane; r < r_cnt; r += 32) cp_async4(drp + r, p.row_ptr + r_lo + r);
       }
     }
+    if (p.trace) __syncwarp();
+    if (j < 3 && lane == 0) BSPMM_TRACE(p, 19 + 4 * j);
     if (lane == 0) {
       UnitHdr h;
       h.g0 = g0; h.n = n; h.nz0 = nz0; h.nnz = nnz; h.c0 = c0; h.kw = kw;
@@ -450,35 +458,60 @@ __device__ __forceinline__ void issue_done(const SpmmParams& p, unsigned char* s
   cp_async_arrive_noinc(&full[s]);
 }
 
-template <bool VEC>
+template <bool VEC, bool COO>
 __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem) {
   const int lane = threadIdx.x & 31;
   const int64_t G = gridDim.x;
   int j = 0;
+  // Static schedule (default): units blockIdx.x, +grid, ...  Metadata for 32
+  // units per batch, one lane each, both round trips done BEFORE any copy of
+  // the batch is issued: under load the row_ptr loads would otherwise queue
+  // behind the bulk B traffic (tools/trace.py).  The next batch is prefetched
+  // while the current one is issued.
+  // Dynamic schedule (p.sched, mixed-size batches): the first unit is
+  // blockIdx.x, later ones come from a global ticket counter, so a CTA that
+  // drew small matrices keeps drawing (load balance within one unit).  The
+  // next ticket is drawn while the current unit is issued.  The counter resets
+  // itself: the draw that returns units - 1 is the last of the launch.
+  // Both feed ONE issue_unit call site (instruction-cache footprint).
+  Meta cur, nxt;
+  int64_t carry = 0;
+  unsigned long long t_next = 0;
+  int64_t u = blockIdx.x;
   if (p.sched) {
-    // Dynamic schedule (mixed-size batches): the first unit is blockIdx.x, later
-    // ones come from a global ticket counter, so a CTA that drew small matrices
-    // keeps drawing (load balance within one unit).  The next ticket is drawn
-    // while the current unit is issued.  The counter resets itself: the draw
-    // that returns units - 1 is the last of the launch.
-    Meta m;
-    int64_t u = blockIdx.x;
-    unsigned long long t_next = 0;
     if (lane == 0) {
       t_next = atomicAdd(p.sched, 1ULL);
-      meta_rt1(p, u, m);
-      meta_rt2(p, u, m);
+      meta_rt1<COO>(p, u, cur);
+      meta_rt2<COO>(p, u, cur);
     }
-    while (true) {
-      const int64_t g0 = __shfl_sync(0xffffffffu, m.g0, 0);
-      const int32_t n = __shfl_sync(0xffffffffu, m.n, 0);
-      const int32_t c0 = __shfl_sync(0xffffffffu, m.c0, 0);
-      const int32_t kw = __shfl_sync(0xffffffffu, m.kw, 0);
-      const int32_t nz0 = __shfl_sync(0xffffffffu, m.nz0, 0);
-      const int32_t nnz = __shfl_sync(0xffffffffu, m.nz1, 0) - nz0;
-      if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
-      issue_unit<VEC>(p, maps, smem, j, g0, n, c0, kw, nz0, nnz);
-      ++j;
+  } else {
+    carry = p.row_off ? 0 : fused_prefix_start(p, lane);
+    meta_rt1<COO>(p, blockIdx.x + lane * G, nxt, p.row_off ? -1 : fused_prefix(p, blockIdx.x, G, lane, carry));
+    meta_rt2<COO>(p, blockIdx.x + lane * G, nxt);
+  }
+  while (u < p.units) {
+    int src = 0;  // lane holding this unit's metadata
+    if (!p.sched) {
+      const int jj = j & 31;
+      if (jj == 0) {
+        cur = nxt;
+        const int64_t nb = u + 32 * G;  // next batch, round trip 1
+        meta_rt1<COO>(p, nb + lane * G, nxt, p.row_off ? -1 : fused_prefix(p, nb, G, lane, carry));
+        if (j == 0 && lane == 0) BSPMM_TRACE(p, 2);
+      }
+      if (jj == 8 || (jj == 0 && u + 8 * G >= p.units)) meta_rt2<COO>(p, u + (32 - jj + lane) * G, nxt);
+      src = jj;
+    }
+    const int64_t g0 = __shfl_sync(0xffffffffu, cur.g0, src);
+    const int32_t n = __shfl_sync(0xffffffffu, cur.n, src);
+    const int32_t c0 = __shfl_sync(0xffffffffu, cur.c0, src);
+    const int32_t kw = __shfl_sync(0xffffffffu, cur.kw, src);
+    const int32_t nz0 = __shfl_sync(0xffffffffu, cur.nz0, src);
+    const int32_t nnz = __shfl_sync(0xffffffffu, cur.nz1, src) - nz0;
+    if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
+    issue_unit<VEC, COO>(p, maps, smem, j, g0, n, c0, kw, nz0, nnz);
+    ++j;
+    if (p.sched) {
       const unsigned long long t = __shfl_sync(0xffffffffu, t_next, 0);
       if ((int64_t)t + G >= p.units) {
         if (lane == 0 && t == (unsigned long long)p.units - 1) atomicExch(p.sched, 0ULL);
@@ -487,68 +520,11 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
       u = (int64_t)t + G;
       if (lane == 0) {
         t_next = atomicAdd(p.sched, 1ULL);
-        meta_rt1(p, u, m);
-        meta_rt2(p, u, m);
+        meta_rt1<COO>(p, u, cur);
+        meta_rt2<COO>(p, u, cur);
       }
-    }
-  } else {
-    // Static schedule: units blockIdx.x, +grid, ...  Metadata for 32 units per
-    // batch, one lane each, both round trips done BEFORE any copy of the batch
-    // is issued: under load the row_ptr loads would otherwise queue behind the
-    // bulk B traffic (tools/trace.py).  The next batch is prefetched while the
-    // current one is issued.
-    Meta cur, nxt;
-    int64_t carry = p.row_off ? 0 : fused_prefix_start(p, lane);
-    meta_rt1(p, blockIdx.x + lane * G, nxt, p.row_off ? -1 : fused_prefix(p, blockIdx.x, G, lane, carry));
-    meta_rt2(p, blockIdx.x + lane * G, nxt);
-    for (int64_t u = blockIdx.x; u < p.units; u += G, ++j) {
-      const int jj = j & 31;
-      if (jj == 0) {
-        cur = nxt;
-        const int64_t nb = u + 32 * G;  // next batch, round trip 1
-        meta_rt1(p, nb + lane * G, nxt, p.row_off ? -1 : fused_prefix(p, nb, G, lane, carry));
-        if (j == 0 && lane == 0) BSPMM_TRACE(p, 2);
-      }
-      if (jj == 8 || (jj == 0 && u + 8 * G >= p.units)) meta_rt2(p, u + (32 - jj + lane) * G, nxt);
-      if (jj == 0 && p.prefetch) {
-        // small problem: prefetch this lane's unit of the batch (B tile + CSR
-        // slice) into L2 now; the smem TMA loads below then hit L2 instead of
-        // queueing DRAM-latency-bound behind the SM's outstanding-copy limit
-        const int64_t uu = u + (int64_t)lane * G;
-        if (uu < p.units && cur.n > 0) {
-          const int32_t nnz_ = cur.nz1 - cur.nz0;
-          const int64_t z0 = cur.nz0 & ~3LL, z1 = (cur.nz1 + 3) & ~3LL;
-          if (nnz_ > 0 && p.sbulk) {
-            prefetch_l2(p.col + z0, (uint32_t)(z1 - z0) * 4u);
-            prefetch_l2(p.vals + z0, (uint32_t)(z1 - z0) * 4u);
-          }
-          if (VEC) {
-            const float* bsrc = p.B + cur.g0 * p.ldb + cur.c0;
-            if (cur.kw == p.ldb) {
-              prefetch_l2(bsrc, (uint32_t)cur.n * (uint32_t)cur.kw * 4u);
-            } else if (p.tma2d && cur.kw == p.kt) {
-              int32_t r0 = 0;
-              while (cur.n - r0 >= 512) {
-                prefetch_l2_2d(&maps.m[kTmaMaps - 1], cur.c0, (int32_t)(cur.g0 + r0));
-                r0 += 256;
-              }
-              for (int b = kTmaMaps - 1; b >= 0; --b)
-                if ((cur.n - r0) & (1 << b)) {
-                  prefetch_l2_2d(&maps.m[b], cur.c0, (int32_t)(cur.g0 + r0));
-                  r0 += 1 << b;
-                }
-            }
-          }
-        }
-      }
-      const int64_t g0 = __shfl_sync(0xffffffffu, cur.g0, jj);
-      const int32_t n = __shfl_sync(0xffffffffu, cur.n, jj);
-      const int32_t c0 = __shfl_sync(0xffffffffu, cur.c0, jj);
-      const int32_t kw = __shfl_sync(0xffffffffu, cur.kw, jj);
-      const int32_t nz0 = __shfl_sync(0xffffffffu, cur.nz0, jj);
-      const int32_t nnz = __shfl_sync(0xffffffffu, cur.nz1, jj) - nz0;
-      if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
-      issue_unit<VEC>(p, maps, smem, j, g0, n, c0, kw, nz0, nnz);
+    } else {
+      u += G;
     }
   }
   issue_done(p, smem, j);
@@ -849,7 +825,7 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
   consumer_bar(T);
 }
 
-template <int CH, bool VEC, int EPI>
+template <int CH, bool VEC, int EPI, bool COO>
 __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem) {
   const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -870,7 +846,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
     const UnitHdr h = hdr[s];
     if (h.flags < 0) break;  // the producer's "done" header
     const unsigned char* st = ring + (size_t)s * stage_bytes;
-    if (p.nnz_off && h.flags == 3)  // fused COO mode: SparseTensor slice -> CSR slice in shared memory
+    if (COO && h.flags == 3)  // fused COO mode: SparseTensor slice -> CSR slice in shared memory
       coo_convert(p, h, const_cast<unsigned char*>(st), threadIdx.x - 32, W * 32);
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
     for (int rep = 0; rep < reps && h.flags != 4; ++rep) {  // 4: COO unit over capacity (skipped, flagged)
@@ -891,7 +867,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
   if (cw == 0 && lane == 0) BSPMM_TRACE(p, 6);
 }
 
-template <int CH, bool VEC, int EPI>
+template <int CH, bool VEC, int EPI, bool COO>
 __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -911,17 +887,17 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
   pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
-  if ((threadIdx.x >> 5) == 0) produce<VEC>(p, maps, smem);
-  else consume<CH, VEC, EPI>(p, smem);
+  if ((threadIdx.x >> 5) == 0) produce<VEC, COO>(p, maps, smem);
+  else consume<CH, VEC, EPI, COO>(p, smem);
   if (p.trace) {
     __syncthreads();
     if (threadIdx.x == 0) BSPMM_TRACE(p, 7);
   }
 }
 
-template <int CH, bool VEC, int EPI>
+template <int CH, bool VEC, int EPI, bool COO = false>
 static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bspmm_plan_t& plan, cudaStream_t s) {
-  auto kern = spmm_csr_kernel<CH, VEC, EPI>;
+  auto kern = spmm_csr_kernel<CH, VEC, EPI, COO>;
   static thread_local int configured_bytes[64] = {};  // per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -946,6 +922,15 @@ static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bsp
 template <int CH, bool VEC>
 static cudaError_t launch_e(int epi, const SpmmParams& sp, const TmaMaps& maps, const bspmm_plan_t& plan,
                             cudaStream_t s) {
+  // fused COO mode (row a-2 inside the launch) is planned only for the vector
+  // path with the plain epilogue: its own instantiation, so the CSR kernels
+  // carry none of its code (instruction-cache footprint of latency-bound launches)
+  if (sp.nnz_off) {
+    if constexpr (VEC) {
+      if (epi == 0) return launch_t<CH, VEC, 0, true>(sp, maps, plan, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (epi == 2) return launch_t<CH, VEC, 2>(sp, maps, plan, s);
   if (epi == 1) return launch_t<CH, VEC, 1>(sp, maps, plan, s);
   return launch_t<CH, VEC, 0>(sp, maps, plan, s);
@@ -976,10 +961,6 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.tma2d = a.maps != nullptr ? 1 : 0;
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
   sp.sbulk = (al16(a.col) && al16(a.vals) && al16(a.row_ptr)) ? 1 : 0;
-  // prefetch only when every CTA's whole share is one metadata batch (<= 32 units):
-  // the prefetched bytes then never exceed the problem (small, L2-resident)
-  // (measured: no gain on C3/C4, so off unless requested with debug bit 16)
-  sp.prefetch = (plan.units <= 32LL * plan.grid && (a.dbg & 16)) ? 1 : 0;
   sp.slice_lsu = (plan.units <= 32LL * plan.grid && !(a.dbg & 32)) ? 1 : 0;
   sp.bias = a.bias;
   sp.accumulate = a.accumulate;

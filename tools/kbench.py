@@ -23,11 +23,11 @@ from bench import alg_bytes, peaks  # noqa: E402
 L2 = 126 * 2 ** 20
 
 
-def setup(cid, dev):
+def setup(cid, dev, replicas=0):
     b = synth.config(cid, coo=True)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     per = alg_bytes(b.n_rows, b.n_nnz, b.k, b.batch)
-    M = max(1, min(64, int(np.ceil(2 * L2 / per))))
+    M = replicas if replicas > 0 else max(1, min(64, int(np.ceil(2 * L2 / per))))
     reps = []
     for _ in range(M):
         reps.append(dict(ro=T(b.row_off), rp=T(b.row_ptr), col=T(b.col), vals=T(b.vals), B=T(b.B),
@@ -88,6 +88,10 @@ def fused_step(h, r):  # offsets built inside the SpMM (row_off = None)
     h.csr(None, r["sizes"], r["rp"], r["col"], r["vals"], r["B"], r["C"])
 
 
+def copy_only(h, r):  # practical floor: a device copy moving B's bytes in and C's out
+    r["C"].copy_(r["B"])
+
+
 def offsets_only(h, r):
     h.build_offsets(r["sizes"], out=r["ro"])
 
@@ -103,13 +107,15 @@ def main():
     ap.add_argument("--chunks", default="0")
     ap.add_argument("--ncu-mode", action="store_true", help="plain launches only (for ncu)")
     ap.add_argument("--dbg", default="0", help="comma list of debug bit sets to sweep (bspmm_set_debug)")
+    ap.add_argument("--replicas", type=int, default=0, help="override the replica count (1 = L2-warm)")
+    ap.add_argument("--copy-baseline", action="store_true", help="also time C.copy_(B) on the same replicas")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     peak, _ = peaks()
     h = bs.Handle(0)
     for cid in [int(c) for c in args.configs.split(",")]:
-        b, reps, per = setup(cid, dev)
+        b, reps, per = setup(cid, dev, args.replicas)
         h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
         R = args.reps if cid != 5 else max(10, args.reps // 20)
         if args.ncu_mode:
@@ -149,12 +155,17 @@ def main():
         ms_off = time_calls(h, reps, R, offsets_only)
         ms_ng = time_calls(h, reps, min(R, 50), spmm_only, graph=False)
         extra = {}
+        if args.copy_baseline:
+            ms_cp = time_calls(h, reps, R, copy_only)
+            extra["copy_us"] = ms_cp * 1e3
+            extra["copy_GBs"] = 8 * b.n_rows * b.k / (ms_cp / 1e3) / 1e9
         if b.k % 4 == 0 and cid != 5:
             extra["coo_convert_csr_us"] = time_calls(h, reps, R, coo_convert_csr) * 1e3
             extra["coo_atomic_us"] = time_calls(h, reps, R, coo_atomic) * 1e3
         print(json.dumps({"config": cid, "step_us": ms_step * 1e3, "fused_step_us": ms_fused * 1e3,
                           "offsets_us": ms_off * 1e3,
-                          "spmm_us_no_graph": ms_ng * 1e3, "alg_bytes": per, **extra}), flush=True)
+                          "spmm_us_no_graph": ms_ng * 1e3, "alg_bytes": per, "replicas": len(reps), **extra}),
+              flush=True)
         del reps
         torch.cuda.empty_cache()
 

@@ -19,7 +19,8 @@ import synth  # noqa: E402
 
 SLOTS = ["entry", "after_pdl_wait", "prod_rowoff", "prod_struct_off", "prod_done", "cons_first_full",
          "cons_done", "exit", "cons_unit0_done", "p0_after_empty", "p0_after_tma", "p0_before_arrive",
-         "p1_before_arrive", "p0_after_arrive", "p1_after_arrive"]
+         "p1_before_arrive", "p0_after_arrive", "p1_after_arrive", "unused15"]
+SLOTS += [f"u{j}_{w}" for j in range(3) for w in ("empty_ok", "slice_issued", "tma_issued", "copies_issued")]
 
 
 def main():
@@ -31,6 +32,8 @@ def main():
     ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--launches", type=int, default=3)
     ap.add_argument("--nostore", action="store_true")
+    ap.add_argument("--dbg", type=int, default=0, help="debug bits (bspmm_set_debug)")
+    ap.add_argument("--warm", action="store_true", help="no L2 flush before the traced launch")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     b = synth.config(args.config)
@@ -42,12 +45,12 @@ def main():
     C = torch.empty((b.n_rows, b.k), device=dev)
     h.csr(ro, None, rp, col, vals, B, C)
     grid = h.last_plan()["grid"]
-    buf = torch.zeros((grid, 16), dtype=torch.int64, device=dev)
-    if args.nostore:
-        h.set_debug(1)
+    buf = torch.zeros((grid, 32), dtype=torch.int64, device=dev)
+    h.set_debug(args.dbg | (1 if args.nostore else 0))
     flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device=dev)
     for it in range(args.launches):
-        flush.fill_(float(it))
+        if not args.warm:
+            flush.fill_(float(it))
         torch.cuda.synchronize()
         h.set_trace(buf)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
