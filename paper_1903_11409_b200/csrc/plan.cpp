@@ -5,9 +5,9 @@
 // SpMM gets (subWarp * m_A for CSR, :259).  Re-derived for sm_100a:
 //  * a unit is (matrix i, k-tile t); tiles = p = ceil(k / kt);
 //  * kt starts at the whole row (capped at 512 columns on the float4 path,
-//    128 on the scalar path) and is halved while the batch yields fewer than
-//    2 units per SM (the paper's "batch 50 fails to fill the SMs", :377) or a
-//    two-stage shared-memory ring of n_max x kt tiles does not fit;
+//    128 on the scalar path) and is halved while the batch leaves more than
+//    half the SMs idle (the paper's "batch 50 fails to fill the SMs", :377)
+//    or a two-stage shared-memory ring of n_max x kt tiles does not fit;
 //  * lanes per row = the paper's subWarp rule (:150-155) applied to the
 //    tile's columns in per-lane chunks (float4 chunks on the vec path);
 //  * persistent grid = min(units, SMs x CTAs/SM); each CTA walks units
@@ -40,11 +40,13 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
     if (vec) kt = align_up(kt, 4);
     kt = std::min(kt, align_up(k, quantum));
   } else {
-    // column blocking only while the batch leaves SMs idle AND the units are
-    // big: many small units cost more (per-unit TMA + metadata) than idle SMs
-    // (measured, tools/kbench.py sweeps)
+    // column blocking only while the batch leaves more than half the SMs idle
+    // AND the units are big: a CTA's units are issued one after another by
+    // its producer (~1 us each on a cold start, tools/trace.py), so several
+    // small units per CTA cost more than idle SMs (C4: kt 512 / 100 units 8.2
+    // us, 256 / 200 8.7, 128 / 400 9.1 -- tools/kbench.py --sweep)
     kt = std::min(align_up(k, quantum), kmax);
-    while ((int64_t)batch * ceil_div(k, kt) < 2LL * num_sms && (int64_t)R * kt * 4 > 32768 && kt > 32)
+    while (2LL * batch * ceil_div(k, kt) < num_sms && (int64_t)R * kt * 4 > 32768 && kt > 32)
       kt = align_up(kt / 2, quantum);
   }
   // CTAs per SM: one by default (sweeps: 2 never won once the consumers cover
