@@ -362,23 +362,7 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
         if (tx) mbar_expect_tx(&full[s], tx);
       }
       __syncwarp();
-      if (slice_tma) {
-        if (b_col > a_col) {
-          if (lane == 0) bulk_g2s(dcol + a_col, p.col + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
-          if (lane == 1) bulk_g2s(dval + a_col, p.vals + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
-        }
-        if (lane == 2 && b_rp > a_rp)
-          bulk_g2s(drp + a_rp, p.row_ptr + r_lo + a_rp, 4u * (uint32_t)(b_rp - a_rp), &full[s]);
-      } else if (p.sbulk) {
-        const int32_t ncol4 = (b_col - a_col) >> 2, nrp4 = (b_rp - a_rp) >> 2;
-        for (int32_t q = lane; q < ncol4; q += 32) {
-          cp_async16(dcol + a_col + 4 * q, p.col + nz0 + a_col + 4 * q);
-          cp_async16(dval + a_col + 4 * q, p.vals + nz0 + a_col + 4 * q);
-        }
-        for (int32_t q = lane; q < nrp4; q += 32) cp_async16(drp + a_rp + 4 * q, p.row_ptr + r_lo + a_rp + 4 * q);
-      }
-      if (p.trace) __syncwarp();
-      if (j < 3 && lane == 0) BSPMM_TRACE(p, 17 + 4 * j);
+      auto issue_b = [&]() {
       if (b_bulk) {  // TMA: whole contiguous B_i (1-D), a full k-tile (2-D boxes), else one bulk copy per row
         if (kw == p.ldb) {
           if (lane == 3) bulk_g2s_hint(st, bsrc, (uint32_t)n * (uint32_t)kw * 4u, &full[s], pol);
@@ -397,9 +381,30 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
             bulk_g2s_hint(st + (size_t)r * kw * 4, bsrc + (int64_t)r * p.ldb, (uint32_t)kw * 4u, &full[s], pol);
         }
       }
+      };
+      // the B tile first: it is the long pole of a unit's landing (C4: 100 KB;
+      // 7.9 vs 8.2 us, C5 810 vs 817 us)
+      issue_b();
       if (p.trace) __syncwarp();
-      if (j == 0 && lane == 0) BSPMM_TRACE(p, 10);
       if (j < 3 && lane == 0) BSPMM_TRACE(p, 18 + 4 * j);
+      if (slice_tma) {
+        if (b_col > a_col) {
+          if (lane == 0) bulk_g2s(dcol + a_col, p.col + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+          if (lane == 1) bulk_g2s(dval + a_col, p.vals + nz0 + a_col, 4u * (uint32_t)(b_col - a_col), &full[s]);
+        }
+        if (lane == 2 && b_rp > a_rp)
+          bulk_g2s(drp + a_rp, p.row_ptr + r_lo + a_rp, 4u * (uint32_t)(b_rp - a_rp), &full[s]);
+      } else if (p.sbulk) {
+        const int32_t ncol4 = (b_col - a_col) >> 2, nrp4 = (b_rp - a_rp) >> 2;
+        for (int32_t q = lane; q < ncol4; q += 32) {
+          cp_async16(dcol + a_col + 4 * q, p.col + nz0 + a_col + 4 * q);
+          cp_async16(dval + a_col + 4 * q, p.vals + nz0 + a_col + 4 * q);
+        }
+        for (int32_t q = lane; q < nrp4; q += 32) cp_async16(drp + a_rp + 4 * q, p.row_ptr + r_lo + a_rp + 4 * q);
+      }
+      if (p.trace) __syncwarp();
+      if (j < 3 && lane == 0) BSPMM_TRACE(p, 17 + 4 * j);
+      if (j == 0 && lane == 0) BSPMM_TRACE(p, 10);
       if (!VEC) {
         float* dst = reinterpret_cast<float*>(st);
         const int32_t total = n * kw;
@@ -408,7 +413,11 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
           cp_async4(dst + q, bsrc + (int64_t)r * p.ldb + c);
         }
       }
-      if (p.sbulk) {  // <= 3 head and <= 3 tail elements per array, on lanes not issuing TMA
+      if (p.sbulk) {
+        // <= 3 head and <= 3 tail elements per array, on lanes 24..31 (they
+        // issue no TMA).  A branch-free variant on lanes 0..17 (addresses by
+        // selects) measured slower on C5 (840 vs 810 us): lanes 0..2 have just
+        // issued the slice's bulk copies
         if (lane >= 24 && lane < 27 && lane - 24 < a_col) {
           cp_async4(dcol + (lane - 24), p.col + nz0 + (lane - 24));
           cp_async4(dval + (lane - 24), p.vals + nz0 + (lane - 24));
