@@ -33,8 +33,25 @@ def main():
         rp, col, v = h.coo2csr(ro, None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), b.n_rows)
         rt, ct, vt = h.csr_transpose(ro, None, T(b.row_ptr), T(b.col), T(b.vals))
         gB, gv = h.csr_backward(ro, None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), C)
+        Cf = h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B))        # fused offsets
+        Cm = torch.empty_like(C)
+        h.csr_multicast(ro, None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cm)        # multimem variant (unicast)
+        Ca = h.coo_atomic(ro, None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B))
         torch.cuda.synchronize()
-        assert torch.equal(C, C2)
+        assert torch.equal(C, C2) and torch.equal(C, Cf) and torch.equal(C, Cm)
+    # C4: whole-row units (1-D bulk B tiles of 100 KB), and the GCN layer
+    b = synth.config(4)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    C4 = h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
+    b = synth.config(2)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    X = torch.randn((b.n_rows, 32), device=dev)
+    W = torch.randn((2, 32, b.k), device=dev)
+    bias = torch.randn((2, b.k), device=dev)
+    rps = torch.stack([T(b.row_ptr), T(b.row_ptr)])
+    h.gcn_layer(T(b.row_off), None, rps, T(b.col), T(b.vals), X, W, bias)
+    torch.cuda.synchronize()
+    del C4
     # direct path (tiny stage capacity) and scalar path (k % 4 != 0)
     if len(sys.argv) > 1:  # the TMA-only variant: C1-C3 vectorised paths only
         h.sync()
