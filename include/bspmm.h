@@ -138,7 +138,8 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
 
 /* Debug: timing-experiment bits for subsequent SpMM launches.  1 = compute but
  * do not store C (the result is then undefined); 2 = compute every unit from
- * global memory (no staging); 8 = consumers repeat each unit's work 4 times;
+ * global memory (no staging); 4 = no early B tile for the first unit of a
+ * CTA; 8 = consumers repeat each unit's work 4 times;
  * 16 = (unused; was an L2 prefetch of small problems, no gain); 32 = always copy
  * the CSR slice with TMA; 64 = force the static unit schedule; 128 = force the
  * dynamic one.  0 (default) = normal. */

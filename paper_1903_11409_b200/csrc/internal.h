@@ -32,7 +32,9 @@ inline int32_t pow2_ceil(int32_t x) {
 BSPMM_HD inline int32_t align_up(int32_t x, int32_t a) { return (x + a - 1) / a * a; }
 
 // smem carve-up shared by planner and kernel: [hdr S*32][full S*8][empty S*8] pad 128, then stages
-BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stages * (kHdrBytes + 16), 128); }
+// per stage: header + "full" + "empty" barriers; then one barrier for the
+// first unit's early B tile (spmm_csr.cu early_b)
+BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stages * (kHdrBytes + 16) + 8, 128); }
 
 // planner (plan.cpp)
 bspmm_status_t make_plan(int32_t k, int32_t batch, bool aligned, int32_t max_rows, int64_t max_nnz,

@@ -257,11 +257,30 @@ __device__ __forceinline__ void meta_rt2(const SpmmParams& p, int64_t uu, Meta& 
   }
 }
 
+// Early B tile of a CTA's FIRST unit (latency-bound launches): consumer warp
+// 0 -- idle until the first unit lands -- loads the unit's row range itself
+// and issues its B tile at once, on a barrier of its own (bfull), while the
+// producer is still on the structure round trip (row_ptr) and the CSR slice.
+// The B tile is the long pole of a unit's landing (C4: 100 KB per CTA).
+// Conditions are evaluated identically by the producer (which then skips the
+// tile) and by consumer warp 0.
+__device__ __forceinline__ uint64_t* early_bar(const SpmmParams& p, unsigned char* smem) {
+  return reinterpret_cast<uint64_t*>(smem + p.stages * (kHdrBytes + 16));
+}
+template <bool VEC, bool COO>
+__device__ __forceinline__ bool early_b_ok(const SpmmParams& p, int32_t n, int32_t kw) {
+  // whole contiguous B_i only (one 1-D bulk copy): with k-tiles (2-D boxes) it
+  // measured slower (C3 12.45 vs 12.16 us), whole rows faster (C4 7.9 -> 7.05 us)
+  return VEC && !COO && !p.sched && p.row_off != nullptr && !(p.dbg & (2 | 4)) && n > 0 &&
+         (int64_t)n * kw * 4 <= p.stage_b && kw == p.ldb;
+}
+
 // Stage unit j of this CTA (metadata already known): wait for its ring stage,
 // TMA/cp.async the B tile and CSR slice, publish the header, arrive on "full".
 template <bool VEC, bool COO>
 __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem, int j,
-                                           int64_t g0, int32_t n, int32_t c0, int32_t kw, int32_t nz0, int32_t nnz) {
+                                           int64_t g0, int32_t n, int32_t c0, int32_t kw, int32_t nz0, int32_t nnz,
+                                           bool b_early = false) {
   UnitHdr* hdr = reinterpret_cast<UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
@@ -346,7 +365,7 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
       int32_t* dcol = reinterpret_cast<int32_t*>(sreg) + (nz0 & 3);
       int32_t* dval = reinterpret_cast<int32_t*>(sreg + slice_region(nnz)) + (nz0 & 3);
       int32_t* drp = reinterpret_cast<int32_t*>(sreg + 2 * slice_region(nnz)) + (r_lo & 3);
-      const bool b_bulk = VEC && n > 0;
+      const bool b_bulk = VEC && n > 0 && !b_early;  // (an early tile is already in flight)
       // lane 0 announces every TMA byte of the unit, then each copy is issued
       // by its own lane: on a cold start every issue stalls its thread ~0.1 us
       // (measured with tools/trace.py), so serial issue from one lane cost
@@ -443,7 +462,7 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
     if (lane == 0) {
       UnitHdr h;
       h.g0 = g0; h.n = n; h.nz0 = nz0; h.nnz = nnz; h.c0 = c0; h.kw = kw;
-      h.flags = (bst ? 1 : 0) | (sst ? 2 : 0);
+      h.flags = (bst ? 1 : 0) | (sst ? 2 : 0) | (b_early ? 8 : 0);
       hdr[s] = h;
       mbar_arrive(&full[s]);  // release: header visible to consumers
     }
@@ -518,7 +537,7 @@ __device__ __forceinline__ void produce(const SpmmParams& p, const TmaMaps& maps
     const int32_t nz0 = __shfl_sync(0xffffffffu, cur.nz0, src);
     const int32_t nnz = __shfl_sync(0xffffffffu, cur.nz1, src) - nz0;
     if (j == 0 && lane == 0) BSPMM_TRACE(p, 3);
-    issue_unit<VEC, COO>(p, maps, smem, j, g0, n, c0, kw, nz0, nnz);
+    issue_unit<VEC, COO>(p, maps, smem, j, g0, n, c0, kw, nz0, nnz, j == 0 && early_b_ok<VEC, COO>(p, n, kw));
     ++j;
     if (p.sched) {
       const unsigned long long t = __shfl_sync(0xffffffffu, t_next, 0);
@@ -835,7 +854,7 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
 }
 
 template <int CH, bool VEC, int EPI, bool COO>
-__device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem) {
+__device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem) {
   const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
@@ -848,18 +867,40 @@ __device__ __forceinline__ void consume(const SpmmParams& p, unsigned char* smem
   const int rpw = 32 / L;
   const int sub = lane / L, li = lane % L;
   const int first = cw * rpw + sub, step = W * rpw;
+  if (cw == 0 && !p.sched && !COO && VEC) {
+    // the first unit's row range (round trip 1 of unit blockIdx.x), then its B tile
+    const int64_t i = (int64_t)blockIdx.x / p.tiles;
+    const int32_t t = (int32_t)((int64_t)blockIdx.x - i * p.tiles);
+    int64_t g0 = 0;
+    int32_t n = 0;
+    if (p.row_off) {
+      g0 = p.row_off[i];
+      n = p.sizes ? p.sizes[i] : (int32_t)(p.row_off[i + 1] - g0);
+    }
+    const int32_t c0 = t * p.kt, kw = min(p.kt, p.k - c0);
+    if (early_b_ok<VEC, COO>(p, n, kw)) {
+      uint64_t* eb = early_bar(p, const_cast<unsigned char*>(smem));
+      unsigned char* st = const_cast<unsigned char*>(ring);  // stage 0
+      if (lane == 0) mbar_arrive_expect_tx(eb, (uint32_t)n * (uint32_t)kw * 4u);
+      __syncwarp();
+      if (lane == 0)
+        bulk_g2s_hint(st, p.B + g0 * p.ldb + c0, (uint32_t)n * (uint32_t)kw * 4u, eb, policy_evict_first());
+      if (lane == 0) BSPMM_TRACE(p, 15);
+    }
+  }
   for (int j = 0;; ++j) {
     const int s = j % p.stages;
     mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
     const UnitHdr h = hdr[s];
     if (h.flags < 0) break;  // the producer's "done" header
+    if (j == 0 && (h.flags & 8)) mbar_wait(early_bar(p, const_cast<unsigned char*>(smem)), 0u);  // early B tile
     const unsigned char* st = ring + (size_t)s * stage_bytes;
-    if (COO && h.flags == 3)  // fused COO mode: SparseTensor slice -> CSR slice in shared memory
+    if (COO && (h.flags & 3) == 3)  // fused COO mode: SparseTensor slice -> CSR slice in shared memory
       coo_convert(p, h, const_cast<unsigned char*>(st), threadIdx.x - 32, W * 32);
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
-    for (int rep = 0; rep < reps && h.flags != 4; ++rep) {  // 4: COO unit over capacity (skipped, flagged)
-      if (h.flags == 3) {  // the hot, staged case
+    for (int rep = 0; rep < reps && (h.flags & 4) == 0; ++rep) {  // 4: COO unit over capacity (skipped, flagged)
+      if ((h.flags & 3) == 3) {  // the hot, staged case
         if (VEC && (h.kw >> 2) == p.lanes * CH) rows_staged_full<CH, EPI>(p, h, st, first, step, li);
         else rows<CH, VEC, true, true, EPI>(p, h, st, first, step, li);
       } else {
@@ -888,6 +929,7 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
       mbar_init(&full[s], 1 + 32);  // producer lane-0 arrive + 32 cp.async arrivals
       mbar_init(&empty[s], W);      // one arrival per consumer warp
     }
+    mbar_init(early_bar(p, smem), 1);  // the first unit's early B tile
     fence_mbar_init();
   }
   __syncthreads();
@@ -897,7 +939,7 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
   pdl_launch_dependents();
   if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
   if ((threadIdx.x >> 5) == 0) produce<VEC, COO>(p, maps, smem);
-  else consume<CH, VEC, EPI, COO>(p, smem);
+  else consume<CH, VEC, EPI, COO>(p, maps, smem);
   if (p.trace) {
     __syncthreads();
     if (threadIdx.x == 0) BSPMM_TRACE(p, 7);
