@@ -271,8 +271,30 @@ template <bool VEC, bool COO>
 __device__ __forceinline__ bool early_b_ok(const SpmmParams& p, int32_t n, int32_t kw) {
   // whole contiguous B_i only (one 1-D bulk copy): with k-tiles (2-D boxes) it
   // measured slower (C3 12.45 vs 12.16 us), whole rows faster (C4 7.9 -> 7.05 us)
+  // (not in fused COO mode: its consumer kernel spills with the extra path, C3 19.8 -> 25 us)
   return VEC && !COO && !p.sched && p.row_off != nullptr && !(p.dbg & (2 | 4)) && n > 0 &&
          (int64_t)n * kw * 4 <= p.stage_b && kw == p.ldb;
+}
+
+// consumer warp 0's side of the early B tile, out of line so that it does not
+// add to the consumer loop's register allocation (arguments by value: no
+// local copy of the parameter block).  Must agree with early_b_ok.
+__device__ __noinline__ void early_b_issue(const int64_t* __restrict__ row_off, const int32_t* __restrict__ sizes,
+                                           const float* __restrict__ B, int64_t ldb, int32_t tiles, int32_t kt,
+                                           int32_t k, int32_t stage_b, unsigned long long* trace, uint64_t* eb,
+                                           unsigned char* st) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x / tiles;
+  const int32_t t = (int32_t)((int64_t)blockIdx.x - i * tiles);
+  const int64_t g0 = row_off[i];
+  const int32_t n = sizes ? sizes[i] : (int32_t)(row_off[i + 1] - g0);
+  const int32_t c0 = t * kt, kw = min(kt, k - c0);
+  if (!(n > 0 && (int64_t)n * kw * 4 <= stage_b && kw == ldb)) return;
+  if (lane == 0) {
+    mbar_arrive_expect_tx(eb, (uint32_t)n * (uint32_t)kw * 4u);
+    bulk_g2s_hint(st, B + g0 * ldb + c0, (uint32_t)n * (uint32_t)kw * 4u, eb, policy_evict_first());
+    if (trace) trace[(size_t)blockIdx.x * kTraceSlots + 15] = gtime();
+  }
 }
 
 // Stage unit j of this CTA (metadata already known): wait for its ring stage,
@@ -867,27 +889,9 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
   const int rpw = 32 / L;
   const int sub = lane / L, li = lane % L;
   const int first = cw * rpw + sub, step = W * rpw;
-  if (cw == 0 && !p.sched && !COO && VEC) {
-    // the first unit's row range (round trip 1 of unit blockIdx.x), then its B tile
-    const int64_t i = (int64_t)blockIdx.x / p.tiles;
-    const int32_t t = (int32_t)((int64_t)blockIdx.x - i * p.tiles);
-    int64_t g0 = 0;
-    int32_t n = 0;
-    if (p.row_off) {
-      g0 = p.row_off[i];
-      n = p.sizes ? p.sizes[i] : (int32_t)(p.row_off[i + 1] - g0);
-    }
-    const int32_t c0 = t * p.kt, kw = min(p.kt, p.k - c0);
-    if (early_b_ok<VEC, COO>(p, n, kw)) {
-      uint64_t* eb = early_bar(p, const_cast<unsigned char*>(smem));
-      unsigned char* st = const_cast<unsigned char*>(ring);  // stage 0
-      if (lane == 0) mbar_arrive_expect_tx(eb, (uint32_t)n * (uint32_t)kw * 4u);
-      __syncwarp();
-      if (lane == 0)
-        bulk_g2s_hint(st, p.B + g0 * p.ldb + c0, (uint32_t)n * (uint32_t)kw * 4u, eb, policy_evict_first());
-      if (lane == 0) BSPMM_TRACE(p, 15);
-    }
-  }
+  if (VEC && !COO && cw == 0 && !p.sched && p.row_off && !(p.dbg & (2 | 4)))
+    early_b_issue(p.row_off, p.sizes, p.B, p.ldb, p.tiles, p.kt, p.k, p.stage_b, p.trace,
+                  early_bar(p, const_cast<unsigned char*>(smem)), const_cast<unsigned char*>(ring));
   for (int j = 0;; ++j) {
     const int s = j % p.stages;
     mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
