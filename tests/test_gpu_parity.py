@@ -414,3 +414,40 @@ def test_coo_fused_hint_too_small_is_reported(h):
     with pytest.raises(bs.BspmmError, match="INVALID"):
         h.sync()
     h.sync()                                  # the flag is cleared once reported
+
+
+# ------------------------------------------------------------ early first tile (whole-row plans)
+
+@pytest.mark.parametrize("k,nlo,nhi,batch", [(512, 20, 120, 40), (384, 5, 90, 30), (256, 1, 60, 70),
+                                             (512, 200, 300, 6), (128, 10, 40, 50)])
+def test_early_first_tile_shapes(h, k, nlo, nhi, batch):
+    """Whole-row plans issue each CTA's first B tile early, from consumer warp 0
+    (one bulk copy on a barrier of its own) while the producer does the
+    structure round trip.  Mixed sizes (incl. tiles that do not fit a stage and
+    k-tiled plans, where the path is off) and empty matrices; bitwise O3'
+    either way, also with the early path disabled (debug bit 4) and with sizes
+    only (fused offsets: path off)."""
+    b = synth.generate(synth.MIX, (nlo, nhi, 1, 5), batch, k, seed=k + nhi)
+    ref = None
+    for dbg in (0, 4):
+        h.set_debug(dbg)
+        for sizes in (False, True):
+            C = run_csr(h, b, sizes=sizes)
+            assert_parity(b, C, f"k={k} dbg={dbg} sizes={sizes}")
+            if ref is None:
+                ref = C
+            assert np.array_equal(C.view(np.uint32), ref.view(np.uint32))
+    h.set_debug(0)
+
+
+def test_early_first_tile_empty_first_matrices(h):
+    """Empty matrices at CTA-first positions: no early tile is issued for them
+    (producer and consumer warp 0 agree), the CTA's later units run normally."""
+    for seed in range(400):
+        b = synth.random_batch(np.random.default_rng(seed), 9, 512, nmax=40, dmax=4)
+        if b.sizes[0] == 0 and (b.sizes == 0).sum() >= 2 and b.sizes.max() > 0:
+            break
+    else:
+        pytest.fail("no seed with empty leading matrices")
+    C = run_csr(h, b)
+    assert_parity(b, C, "empty first matrices")
