@@ -23,8 +23,13 @@ from bench import alg_bytes, peaks  # noqa: E402
 L2 = 126 * 2 ** 20
 
 
-def setup(cid, dev, replicas=0):
-    b = synth.config(cid, coo=True)
+def setup(cid, dev, replicas=0, shard=1):
+    if shard > 1:  # rank 0's contiguous nnz*k shard of a `shard`-way split (scaling prediction)
+        full = synth.config(cid)
+        split = bs.partition(full.nnz_off, full.k, shard)
+        b = synth.config(cid, i0=0, i1=int(split[1]), coo=True)
+    else:
+        b = synth.config(cid, coo=True)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     per = alg_bytes(b.n_rows, b.n_nnz, b.k, b.batch)
     M = replicas if replicas > 0 else max(1, min(64, int(np.ceil(2 * L2 / per))))
@@ -109,13 +114,14 @@ def main():
     ap.add_argument("--dbg", default="0", help="comma list of debug bit sets to sweep (bspmm_set_debug)")
     ap.add_argument("--replicas", type=int, default=0, help="override the replica count (1 = L2-warm)")
     ap.add_argument("--copy-baseline", action="store_true", help="also time C.copy_(B) on the same replicas")
+    ap.add_argument("--shard", type=int, default=1, help="time rank 0's shard of an N-way split (1 GPU)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     peak, _ = peaks()
     h = bs.Handle(0)
     for cid in [int(c) for c in args.configs.split(",")]:
-        b, reps, per = setup(cid, dev, args.replicas)
+        b, reps, per = setup(cid, dev, args.replicas, args.shard)
         h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
         R = args.reps if cid != 5 else max(10, args.reps // 20)
         if args.ncu_mode:
@@ -147,7 +153,7 @@ def main():
             gbs = per / (ms / 1e3) / 1e9
             print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "chunks": ch, "dbg": dbg, "us": ms * 1e3, "GBs": gbs,
                               "frac": gbs / peak, "GFLOPs": 2 * b.n_nnz * b.k / (ms / 1e3) / 1e9,
-                              "replicas": len(reps), "plan": plan}), flush=True)
+                              "replicas": len(reps), "shard": args.shard, "plan": plan}), flush=True)
         h.set_tuning(0, 0, 0)
         h.set_debug(0)
         ms_step = time_calls(h, reps, R, full_step)
