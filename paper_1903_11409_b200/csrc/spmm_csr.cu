@@ -178,7 +178,12 @@ __device__ __forceinline__ int64_t fused_prefix(const SpmmParams& p, int64_t bas
                                                 int64_t& carry) {
   const int64_t bmax = p.units / p.tiles;  // matrices
   auto mat = [&](int64_t u) { return u < p.units ? u / p.tiles : bmax; };
-  const int64_t i0 = mat(base + (int64_t)lane * G), i1 = mat(base + (int64_t)(lane + 1) * G);
+  const int64_t i0 = mat(base + (int64_t)lane * G);
+  int64_t i1 = mat(base + (int64_t)(lane + 1) * G);
+  // a lane's segment feeds only the lanes after it (exclusive scan) and the
+  // next batch's carry: in the CTA's last batch, segments from the last valid
+  // unit on are not needed (C4: one unit per CTA -> no loads at all)
+  if (base + 32 * G >= p.units && (base + (int64_t)(lane + 1) * G) >= p.units) i1 = i0;
   // segment sum with many loads in flight: 16-byte loads, 8 per step, split partial sums
   int64_t seg = 0;
   int64_t m = i0;
@@ -218,13 +223,25 @@ __device__ __forceinline__ int64_t fused_prefix(const SpmmParams& p, int64_t bas
   carry += __shfl_sync(0xffffffffu, x, 31);
   return pre;
 }
-__device__ __forceinline__ int64_t fused_prefix_start(const SpmmParams& p, int lane) {
-  const int64_t i0 = (int64_t)blockIdx.x / p.tiles;  // matrices before this CTA's first unit
+// sum of sizes[0 .. i0) over the warp (i0 < grid: a handful per lane): the
+// first 8 loads per lane are all in flight before any add (one round trip)
+__device__ __forceinline__ int64_t warp_sizes_sum(const int32_t* __restrict__ sizes, int64_t i0, int lane) {
+  int32_t v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int64_t m = lane + 32 * q;
+    v[q] = m < i0 ? __ldg(sizes + m) : 0;
+  }
   int64_t s = 0;
-  for (int64_t m = lane; m < i0; m += 32) s += __ldg(p.sizes + m);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += v[q];
+  for (int64_t m = lane + 256; m < i0; m += 32) s += __ldg(sizes + m);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
   return s;
+}
+__device__ __forceinline__ int64_t fused_prefix_start(const SpmmParams& p, int lane) {
+  return warp_sizes_sum(p.sizes, (int64_t)blockIdx.x / p.tiles, lane);  // matrices before this CTA's first unit
 }
 
 // round trip 1 for unit uu: row offset (or the fused prefix g0f), rows, tile
@@ -272,7 +289,7 @@ __device__ __forceinline__ bool early_b_ok(const SpmmParams& p, int32_t n, int32
   // whole contiguous B_i only (one 1-D bulk copy): with k-tiles (2-D boxes) it
   // measured slower (C3 12.45 vs 12.16 us), whole rows faster (C4 7.9 -> 7.05 us)
   // (not in fused COO mode: its consumer kernel spills with the extra path, C3 19.8 -> 25 us)
-  return VEC && !COO && !p.sched && p.row_off != nullptr && !(p.dbg & (2 | 4)) && n > 0 &&
+  return VEC && !COO && !p.sched && !(p.dbg & (2 | 4)) && n > 0 &&
          (int64_t)n * kw * 4 <= p.stage_b && kw == p.ldb;
 }
 
@@ -286,8 +303,10 @@ __device__ __noinline__ void early_b_issue(const int64_t* __restrict__ row_off, 
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x / tiles;
   const int32_t t = (int32_t)((int64_t)blockIdx.x - i * tiles);
-  const int64_t g0 = row_off[i];
-  const int32_t n = sizes ? sizes[i] : (int32_t)(row_off[i + 1] - g0);
+  // packed layout with offsets fused: g0 = sum of the sizes before matrix i
+  const int32_t ni = sizes ? __ldg(sizes + i) : 0;
+  const int64_t g0 = row_off ? row_off[i] : warp_sizes_sum(sizes, i, lane);
+  const int32_t n = sizes ? ni : (int32_t)(row_off[i + 1] - g0);
   const int32_t c0 = t * kt, kw = min(kt, k - c0);
   if (!(n > 0 && (int64_t)n * kw * 4 <= stage_b && kw == ldb)) return;
   if (lane == 0) {
@@ -889,7 +908,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
   const int rpw = 32 / L;
   const int sub = lane / L, li = lane % L;
   const int first = cw * rpw + sub, step = W * rpw;
-  if (VEC && !COO && cw == 0 && !p.sched && p.row_off && !(p.dbg & (2 | 4)))
+  if (VEC && !COO && cw == 0 && !p.sched && !(p.dbg & (2 | 4)))
     early_b_issue(p.row_off, p.sizes, p.B, p.ldb, p.tiles, p.kt, p.k, p.stage_b, p.trace,
                   early_bar(p, const_cast<unsigned char*>(smem)), const_cast<unsigned char*>(ring));
   for (int j = 0;; ++j) {

@@ -426,7 +426,7 @@ def test_early_first_tile_shapes(h, k, nlo, nhi, batch):
     structure round trip.  Mixed sizes (incl. tiles that do not fit a stage and
     k-tiled plans, where the path is off) and empty matrices; bitwise O3'
     either way, also with the early path disabled (debug bit 4) and with sizes
-    only (fused offsets: path off)."""
+    only (row offsets summed from sizes by consumer warp 0)."""
     b = synth.generate(synth.MIX, (nlo, nhi, 1, 5), batch, k, seed=k + nhi)
     ref = None
     for dbg in (0, 4):
@@ -437,6 +437,12 @@ def test_early_first_tile_shapes(h, k, nlo, nhi, batch):
             if ref is None:
                 ref = C
             assert np.array_equal(C.view(np.uint32), ref.view(np.uint32))
+        # sizes only (row_off = NULL): offsets fused into the launch, the early
+        # tile's row offset summed from sizes by consumer warp 0
+        Cd = torch.full((b.n_rows, k), float("nan"), device=DEV)
+        h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cd)
+        torch.cuda.synchronize()
+        assert np.array_equal(Cd.cpu().numpy().view(np.uint32), ref.view(np.uint32))
     h.set_debug(0)
 
 

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--nostore", action="store_true")
     ap.add_argument("--dbg", type=int, default=0, help="debug bits (bspmm_set_debug)")
     ap.add_argument("--warm", action="store_true", help="no L2 flush before the traced launch")
+    ap.add_argument("--sizes", action="store_true", help="row_off = None (offsets fused into the launch)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     b = synth.config(args.config)
@@ -42,6 +43,7 @@ def main():
     h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
     h.set_tuning(args.kt, args.warps, args.ctas, args.chunks)
     ro, rp, col, vals, B = T(b.row_off), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)
+    sz = T(b.sizes)
     C = torch.empty((b.n_rows, b.k), device=dev)
     h.csr(ro, None, rp, col, vals, B, C)
     grid = h.last_plan()["grid"]
@@ -55,7 +57,10 @@ def main():
         h.set_trace(buf)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        h.csr(ro, None, rp, col, vals, B, C)
+        if args.sizes:
+            h.csr(None, sz, rp, col, vals, B, C)
+        else:
+            h.csr(ro, None, rp, col, vals, B, C)
         e1.record()
         h.set_trace(None)
         torch.cuda.synchronize()
