@@ -240,6 +240,19 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
                                    int64_t total_rows, int64_t total_nnz, int32_t* csr_row_ptr_out,
                                    int32_t* csr_col_out, float* csr_val_out);
 
+/* Arithmetic of the dense X W_ch GEMM in bspmm_gcn_layer (the SpMM part is
+ * always fp32):
+ *  BSPMM_GCN_FP32 (default) fp32-accurate (BF16x9 tensor-core emulation when
+ *                 the loaded cuBLAS offers it, else CUDA-core fp32);
+ *  BSPMM_GCN_TF32 tensor cores, inputs rounded to TF32 (10-bit mantissa);
+ *  BSPMM_GCN_BF16 tensor cores, inputs rounded to BF16 (7-bit mantissa).
+ * Errors: INVALID_VALUE (unknown mode); a rejected mode surfaces as
+ * NOT_SUPPORTED from bspmm_gcn_layer. */
+#define BSPMM_GCN_FP32 0
+#define BSPMM_GCN_TF32 1
+#define BSPMM_GCN_BF16 2
+BSPMM_API bspmm_status_t bspmm_set_gcn_math(bspmm_handle_t h, int32_t mode);
+
 /* Fused batched graph-convolution layer (PAPER.md Fig. algo:graph_conv_batched,
  * :304-321; Eq. (2) :66-68):  Y = sum_ch A_ch (X W_ch + 1 bias_ch^T).
  *  X      [total_rows x ldx] dev fp32 (node features, stacked graphs; n_x used)

@@ -190,6 +190,11 @@ class Handle:
         """Debug bits for timing experiments (1 = skip C stores; results undefined)."""
         self._raise(lib.bspmm_set_debug(self._h, int(bits)), "bspmm_set_debug")
 
+    def set_gcn_math(self, mode: str = "fp32"):
+        """GEMM arithmetic of gcn_layer: "fp32" (default), "tf32" or "bf16" tensor cores."""
+        code = {"fp32": 0, "tf32": 1, "bf16": 2}[mode]
+        self._raise(lib.bspmm_set_gcn_math(self._h, code), "bspmm_set_gcn_math")
+
     def sync(self):
         self._raise(lib.bspmm_sync(self._h), "bspmm_sync")
 

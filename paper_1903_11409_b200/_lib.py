@@ -34,6 +34,7 @@ _SIGS = {
     "bspmm_sync": (I32, [P]),
     "bspmm_set_trace": (I32, [P, P]),
     "bspmm_set_debug": (I32, [P, I32]),
+    "bspmm_set_gcn_math": (I32, [P, I32]),
     "bspmm_csr": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
     "bspmm_csr_multicast": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
     "bspmm_mc_supported": (I32, [ctypes.c_int]),

@@ -261,6 +261,12 @@ BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
   return BSPMM_SUCCESS;
 }
 
+BSPMM_API bspmm_status_t bspmm_set_gcn_math(bspmm_handle_t h, int32_t mode) {
+  if (!h || mode < BSPMM_GCN_FP32 || mode > BSPMM_GCN_BF16) return BSPMM_ERROR_INVALID_VALUE;
+  h->gcn_math = mode;
+  return BSPMM_SUCCESS;
+}
+
 BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h) {
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
   DeviceGuard g(h->device);
@@ -554,10 +560,17 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
   cublasSetStream(cb, h->stream);
   // column-major view: U_ch^T (k x N, ld channels*k) = W_ch^T (k x n_x, ld k) * X^T (n_x x N, ld ldx)
   const float one = 1.f, zero = 0.f;
+  // fp32 (default): BF16x9 tensor-core emulation when the loaded cuBLAS has
+  // it, else CUDA-core fp32; TF32 / BF16: tensor cores at reduced input
+  // precision (bspmm_set_gcn_math; the tests bound each by its own rounding)
+  const cublasComputeType_t ct = h->gcn_math == BSPMM_GCN_TF32   ? CUBLAS_COMPUTE_32F_FAST_TF32
+                                 : h->gcn_math == BSPMM_GCN_BF16 ? CUBLAS_COMPUTE_32F_FAST_16BF
+                                                                 : CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
   cublasStatus_t cs = cublasGemmStridedBatchedEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, W, CUDA_R_32F, k,
                                                  (long long)n_x * k, X, CUDA_R_32F, (int)ldx, 0, &zero, U, CUDA_R_32F,
-                                                 (int)ldu, k, channels, CUBLAS_COMPUTE_32F_EMULATED_16BFX9,
-                                                 CUBLAS_GEMM_DEFAULT);
+                                                 (int)ldu, k, channels, ct, CUBLAS_GEMM_DEFAULT);
+  if (cs != CUBLAS_STATUS_SUCCESS && h->gcn_math != BSPMM_GCN_FP32)
+    return fail(h, BSPMM_ERROR_NOT_SUPPORTED, "cuBLAS rejected the reduced-precision GEMM");
   if (cs != CUBLAS_STATUS_SUCCESS)  // emulation unavailable in the loaded cuBLAS: plain fp32
     cs = cublasGemmStridedBatchedEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, W, CUDA_R_32F, k,
                                     (long long)n_x * k, X, CUDA_R_32F, (int)ldx, 0, &zero, U, CUDA_R_32F, (int)ldu,

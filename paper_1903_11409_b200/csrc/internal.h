@@ -127,6 +127,7 @@ struct bspmm_handle_s {
   bool maps_ok = false;
   void* cublas = nullptr;  // cublasHandle_t, created on first bspmm_gcn_layer
   void* gcn_ws = nullptr;  // U = X W_ch for all channels
+  int32_t gcn_math = 0;    // bspmm_set_gcn_math: 0 fp32, 1 TF32 tensor cores, 2 BF16 tensor cores
   size_t gcn_ws_bytes = 0;
   int64_t launches = 0;
   std::string err;

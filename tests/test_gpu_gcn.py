@@ -73,3 +73,35 @@ def test_gcn_layer_reduces_to_spmm(h):
     Cref, bound = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
     assert oracle.check_bound(Y, Cref, bound)[0]
     assert np.array_equal(Y.view(np.uint32), C32.view(np.uint32))   # X @ I is exact in fp32
+
+
+@pytest.mark.parametrize("mode,u_in", [("tf32", 2.0 ** -10), ("bf16", 2.0 ** -7)])
+@pytest.mark.parametrize("cid,channels,n_x", [(2, 3, 64), (4, 2, 128)])
+def test_gcn_layer_reduced_precision(h, mode, u_in, cid, channels, n_x):
+    """Tensor-core GEMM modes (bspmm_set_gcn_math): X and W are rounded to the
+    mode's input format (unit roundoff u_in, truncation worst case: TF32 keeps
+    10 mantissa bits, BF16 7), so each product x*w carries a relative error
+    <= 2 u_in (+u_in^2); the fp32 accumulation, the storage-order SpMM and the
+    channel sum add the fp32 terms of the default bound.  Checked against the
+    fp64 oracle; the result must also differ from the fp32 mode somewhere (the
+    mode took effect)."""
+    rng = np.random.default_rng(cid * 100 + channels + n_x)
+    b = synth.config(cid)
+    rps, col, vals = channels_of(b, channels, rng)
+    X = rng.standard_normal((b.n_rows, n_x)).astype(np.float32)
+    W = (rng.standard_normal((channels, n_x, b.k)) / np.sqrt(n_x)).astype(np.float32)
+    bias = rng.standard_normal((channels, b.k)).astype(np.float32)
+    h.set_hints(int(b.sizes.max()), 0)
+    args = (T(b.row_off), None, T(rps), T(col), T(vals), T(X), T(W), T(bias))
+    try:
+        h.set_gcn_math(mode)
+        Y = h.gcn_layer(*args).cpu().numpy()
+    finally:
+        h.set_gcn_math("fp32")
+    Y32 = h.gcn_layer(*args).cpu().numpy()
+    ref, mag = oracle.gcn_layer(b.row_off, rps, col, vals, X, W, bias)
+    dmax = int(max(np.diff(rp).max() for rp in rps))
+    tol = 2 * u_in + u_in * u_in + (n_x + dmax + channels + 4) * 2.0 ** -23
+    err = np.abs(Y.astype(np.float64) - ref)
+    assert np.all(err <= tol * mag + 1e-30), float((err / np.maximum(mag, 1e-300)).max())
+    assert not np.array_equal(Y.view(np.uint32), Y32.view(np.uint32))

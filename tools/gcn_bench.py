@@ -71,6 +71,11 @@ def main():
 
         reps = [None]
         R = 20 if batch < 1000 else 3
+        t_modes = {}
+        for mode in ("tf32", "bf16"):
+            h.set_gcn_math(mode)
+            t_modes[mode] = time_calls(h, reps, R, fused) * 1e3
+        h.set_gcn_math("fp32")
         t_fused = time_calls(h, reps, R, fused) * 1e3
         t_unf = time_calls(h, reps, R, unfused) * 1e3
         gemm_flops = 2.0 * b.n_rows * width * width * channels
@@ -78,6 +83,8 @@ def main():
         print(json.dumps({"shape": name, "batch": batch, "rows": b.n_rows, "width": width, "channels": channels,
                           "fused_us": t_fused, "unfused_us": t_unf, "speedup_vs_unfused": t_unf / t_fused,
                           "fused_TFLOPs": (gemm_flops + spmm_flops) / t_fused / 1e6,
+                          "fused_tf32_us": t_modes["tf32"], "fused_bf16_us": t_modes["bf16"],
+                          "fused_tf32_TFLOPs": (gemm_flops + spmm_flops) / t_modes["tf32"] / 1e6,
                           "launches_fused": 1 + channels, "launches_unfused": 3 * channels + 2}), flush=True)
 
 
