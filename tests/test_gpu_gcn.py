@@ -105,3 +105,21 @@ def test_gcn_layer_reduced_precision(h, mode, u_in, cid, channels, n_x):
     err = np.abs(Y.astype(np.float64) - ref)
     assert np.all(err <= tol * mag + 1e-30), float((err / np.maximum(mag, 1e-300)).max())
     assert not np.array_equal(Y.view(np.uint32), Y32.view(np.uint32))
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_gcn_accumulate_writes_each_element_once(h, cid):
+    """Write-count check (SURVEY §4 tier 4): with W = I, no bias and C channels
+    sharing one integer-valued adjacency, the layer is Y = C * (A X) exactly --
+    channel ch > 0 adds its SpMM onto Y in the epilogue, so an element written
+    twice by one launch (or skipped) would be off by a whole A X term.  Every
+    row's tile is covered by the kernel's store pattern exactly once."""
+    channels = 3
+    b = synth.config(cid, int_valued=True)
+    X = b.B
+    rps = np.stack([b.row_ptr] * channels)
+    h.set_hints(int(b.sizes.max()), 0)
+    Y = h.gcn_layer(T(b.row_off), None, T(rps), T(b.col), T(b.vals), T(X),
+                    T(np.stack([np.eye(b.k, dtype=np.float32)] * channels))).cpu().numpy()
+    AX = oracle.spmm_f32(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, X)
+    assert np.array_equal(Y, channels * AX)

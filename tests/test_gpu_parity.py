@@ -457,3 +457,22 @@ def test_early_first_tile_empty_first_matrices(h):
         pytest.fail("no seed with empty leading matrices")
     C = run_csr(h, b)
     assert_parity(b, C, "empty first matrices")
+
+
+# ------------------------------------------------------------ library cross-check (SURVEY §4 tier 6)
+
+@pytest.mark.parametrize("cid", [2, 3, 4])
+def test_cusparse_cross_check(h, cid):
+    """Independent of both our kernel and the oracle: cuSPARSE (torch.sparse CSR)
+    on the block-diagonal matrix with global column ids, within the north_star
+    bound of the fp64 oracle -- and our C within the same bound of it."""
+    b = synth.config(cid)
+    # global column of every entry: local col + row offset of its matrix
+    mat_of_entry = np.repeat(np.arange(b.batch), b.nnz)
+    gcol = b.col.astype(np.int64) + b.row_off[mat_of_entry]
+    A = torch.sparse_csr_tensor(T(b.row_ptr.astype(np.int64)), T(gcol), T(b.vals), size=(b.n_rows, b.n_rows))
+    Cs = torch.sparse.mm(A, T(b.B)).cpu().numpy()
+    Cref, bound = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+    assert oracle.check_bound(Cs, Cref, bound)[0]
+    C = run_csr(h, b)
+    assert np.all(np.abs(C.astype(np.float64) - Cs) <= 2 * bound + 1e-30)
