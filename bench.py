@@ -44,6 +44,30 @@ def offsets_bytes(batch: int) -> int:
     return 4 * batch + 8 * (batch + 1)
 
 
+def pcie_roofline_ms(bytes_in: int, bytes_out: int, dev) -> float:
+    """Best of 3: one pinned H2D copy of bytes_in and one D2H of bytes_out on two
+    streams at once (the floor for an end-to-end step moving those bytes)."""
+    import torch
+    hin = torch.empty(bytes_in // 4 + 1, dtype=torch.float32).pin_memory()
+    hout = torch.empty(bytes_out // 4 + 1, dtype=torch.float32).pin_memory()
+    din = torch.empty_like(hin, device=dev)
+    dout = torch.empty_like(hout, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = float("inf")
+    for _ in range(3):
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        with torch.cuda.stream(s1):
+            din.copy_(hin, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hout.copy_(dout, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        best = min(best, time.perf_counter() - t)
+    del hin, hout, din, dout
+    torch.cuda.empty_cache()
+    return best * 1e3
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -337,6 +361,11 @@ def main():
         e2e = {"value": flops / e2e_s / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
                "path": "bspmm_csr_host (pinned host buffers, chunked H2D/compute/D2H overlap)"}
+        # PCIe roofline of this leg: the same bytes as raw pinned copies, both directions at once
+        pc = pcie_roofline_ms(hs.numel() * 4 + hrp.numel() * 4 + hc.numel() * 4 + hv.numel() * 4 + hB.numel() * 4,
+                              hC.numel() * 4, dev)
+        e2e["pcie_roofline_ms"] = pc
+        e2e["frac_of_pcie_roofline"] = pc / (e2e_s * 1e3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
