@@ -712,7 +712,8 @@ BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k,
     bspmm_status_t st = check_validate_flag(h);
     if (st != BSPMM_SUCCESS) return st;
   }
-  CK(h, launch_sddmm(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, h->stream));
+  CK(h, launch_sddmm(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, h->hint_rows, h->num_sms,
+                     h->stream));
   h->launches++;
   return BSPMM_SUCCESS;
 }

@@ -93,6 +93,10 @@ def fused_step(h, r):  # offsets built inside the SpMM (row_off = None)
     h.csr(None, r["sizes"], r["rp"], r["col"], r["vals"], r["B"], r["C"])
 
 
+def backward(h, r):  # NEXT-2: grad_B = A^T grad_C (transpose + SpMM) and grad_vals (SDDMM)
+    h.csr_backward(r["ro"], None, r["rp"], r["col"], r["vals"], r["B"], r["C"])
+
+
 def copy_only(h, r):  # practical floor: a device copy moving B's bytes in and C's out
     r["C"].copy_(r["B"])
 
@@ -115,6 +119,7 @@ def main():
     ap.add_argument("--replicas", type=int, default=0, help="override the replica count (1 = L2-warm)")
     ap.add_argument("--copy-baseline", action="store_true", help="also time C.copy_(B) on the same replicas")
     ap.add_argument("--shard", type=int, default=1, help="time rank 0's shard of an N-way split (1 GPU)")
+    ap.add_argument("--backward", action="store_true", help="also time csr_backward (grad_B and grad_vals)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -161,6 +166,8 @@ def main():
         ms_off = time_calls(h, reps, R, offsets_only)
         ms_ng = time_calls(h, reps, min(R, 50), spmm_only, graph=False)
         extra = {}
+        if args.backward:
+            extra["backward_us"] = time_calls(h, reps, max(3, R // 4), backward) * 1e3
         if args.copy_baseline:
             ms_cp = time_calls(h, reps, R, copy_only)
             extra["copy_us"] = ms_cp * 1e3
