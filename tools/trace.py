@@ -19,7 +19,7 @@ import synth  # noqa: E402
 
 SLOTS = ["entry", "after_pdl_wait", "prod_rowoff", "prod_struct_off", "prod_done", "cons_first_full",
          "cons_done", "exit", "cons_unit0_done", "p0_after_empty", "p0_after_tma", "p0_before_arrive",
-         "p1_before_arrive", "p0_after_arrive", "p1_after_arrive", "unused15"]
+         "p1_before_arrive", "p0_after_arrive", "p1_after_arrive", "early_b_issued"]
 SLOTS += [f"u{j}_{w}" for j in range(3) for w in ("empty_ok", "slice_issued", "tma_issued", "copies_issued")]
 
 
