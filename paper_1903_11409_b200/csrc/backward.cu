@@ -6,10 +6,12 @@
 //   dL/dval_e = <G[row_e], B[col_e]> (SDDMM at A's sparsity pattern)
 // (the standard adjoints).
 //
-// * transpose: one CTA per matrix expands its entries to (col, row) pairs
-//   (position = storage position), and the stable device COO->CSR
-//   (coo2csr.cu) sorts them, so A^T comes out in canonical (row, col,
-//   original position) order, bit-exact against the oracle.
+// * transpose: one warp per matrix, a stable counting sort of its entries by
+//   column in shared memory (counts, warp scan, then a scatter in storage
+//   order in which equal columns rank by __match_any_sync), so A^T comes out
+//   in canonical (row, col, original position) order, bit-exact against the
+//   oracle.  Columns are counted in windows of WIN, so any n_i works.
+//   (Replaces an expand-to-COO + general device COO->CSR pair: C5 440 us.)
 // * SDDMM: one CTA per matrix, a warp per row; each lane holds 128-bit
 //   chunks of G's row, multiplies B's row chunks for every entry and the warp
 //   reduces with shuffles (fixed butterfly order: deterministic).
@@ -23,36 +25,152 @@ namespace bspmm {
 
 constexpr int kBwdThreads = 256;
 
-// A_i entries -> (col, row) pairs at the same storage positions; nnz_off[i] = row_ptr[row_off[i]]
-__global__ void __launch_bounds__(kBwdThreads) transpose_expand_kernel(int32_t batch, const int64_t* __restrict__ row_off,
-                                                                       const int32_t* __restrict__ sizes,
-                                                                       const int32_t* __restrict__ row_ptr,
-                                                                       const int32_t* __restrict__ col,
-                                                                       int32_t* __restrict__ idx,
-                                                                       int64_t* __restrict__ nnz_off) {
-  for (int64_t i = blockIdx.x; i < batch; i += gridDim.x) {
-    const int64_t g0 = row_off[i];
-    const int32_t n = sizes ? sizes[i] : (int32_t)(row_off[i + 1] - g0);
-    if (threadIdx.x == 0) {
-      nnz_off[i] = row_ptr[g0];
-      if (i == batch - 1) nnz_off[batch] = row_ptr[g0 + n];
+// CSR -> per-matrix transposed CSR, one warp per matrix (see the header).
+// Entries of A_i are visited in storage order = (row, position) order, so a
+// stable counting sort by column yields A^T's canonical (row, col, position)
+// order: rowT[g0 + c] = z0 + #entries with column < c, and an entry of column
+// c goes to slot start[c] + #earlier entries of column c.
+// Latency: a warp's global loads are issued together, never as a dependent
+// chain -- the row-pointer slice lands in shared memory in one round trip (an
+// entry's row is then a binary search there), and each block of 256 entries'
+// columns and values land in registers (8 per lane) in one round trip, kept
+// for the scatter when the matrix has <= 256 entries.
+// Shared memory per warp: WIN column cursors + kTrRp row pointers.
+constexpr int kTrWarps = 8;
+constexpr int kTrRp = 516;  // row-pointer slice capacity (n_i <= 515; larger: search in global memory)
+constexpr int kTrE = 8;     // entries per lane per block (256-entry blocks)
+template <int WIN>          // columns counted per window (WIN / 32 per lane)
+__global__ void __launch_bounds__(kTrWarps * 32) transpose_csr_kernel(int32_t batch, const int64_t* __restrict__ row_off,
+                                                                      const int32_t* __restrict__ sizes,
+                                                                      const int32_t* __restrict__ row_ptr,
+                                                                      const int32_t* __restrict__ col,
+                                                                      const float* __restrict__ vals,
+                                                                      int32_t* __restrict__ rowT,
+                                                                      int32_t* __restrict__ colT,
+                                                                      float* __restrict__ valsT) {
+  __shared__ int32_t cnt_all[kTrWarps][WIN];
+  __shared__ int32_t rps_all[kTrWarps][kTrRp];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t* cnt = cnt_all[w];
+  int32_t* rps = rps_all[w];
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int64_t i = (int64_t)blockIdx.x * kTrWarps + w; i < batch; i += (int64_t)gridDim.x * kTrWarps) {
+    const int64_t g0 = row_off[i], g1 = row_off[i + 1];
+    const int32_t n = sizes ? sizes[i] : (int32_t)(g1 - g0);
+    const int32_t* rp = row_ptr + g0;
+    const bool rp_s = n < kTrRp;
+    if (rp_s) {
+      int32_t t[(kTrRp + 31) / 32];
+#pragma unroll
+      for (int q = 0; q < (kTrRp + 31) / 32; ++q) {
+        const int32_t r = lane + 32 * q;
+        if (r <= n) t[q] = __ldg(rp + r);
+      }
+#pragma unroll
+      for (int q = 0; q < (kTrRp + 31) / 32; ++q) {
+        const int32_t r = lane + 32 * q;
+        if (r <= n) rps[r] = t[q];
+      }
+      __syncwarp();
     }
-    for (int32_t r = threadIdx.x >> 5; r < n; r += blockDim.x >> 5) {
-      const int32_t e0 = row_ptr[g0 + r], e1 = row_ptr[g0 + r + 1];
-      for (int32_t e = e0 + (threadIdx.x & 31); e < e1; e += 32) {
-        idx[2 * (int64_t)e] = col[e];
-        idx[2 * (int64_t)e + 1] = r;
+    const int32_t z0 = rp_s ? rps[0] : __ldg(rp), z1 = rp_s ? rps[n] : __ldg(rp + n);
+    for (int64_t g = g0 + n + lane; g < g1; g += 32) rowT[g] = z1;  // padding rows: empty
+    if (i == batch - 1 && lane == 0) rowT[g1] = row_ptr[g1];
+    // one 256-entry block in registers: column ids (-1 past the end) and values
+    int32_t cq[kTrE];
+    float vq[kTrE];
+    auto load_blk = [&](int32_t blk) {
+#pragma unroll
+      for (int q = 0; q < kTrE; ++q) {
+        const int32_t e = blk + 32 * q + lane;
+        cq[q] = e < z1 ? __ldg(col + e) : -1;
+        vq[q] = e < z1 ? __ldg(vals + e) : 0.f;
+      }
+    };
+    const bool resident = z1 - z0 <= 32 * kTrE;
+    if (resident) load_blk(z0);
+    int32_t before = 0;  // entries whose column precedes the window
+    for (int32_t w0 = 0; w0 < n; w0 += WIN) {
+      const int32_t wn = min(WIN, n - w0);
+#pragma unroll
+      for (int q = 0; q < WIN / 32; ++q) cnt[lane + 32 * q] = 0;
+      __syncwarp();
+      for (int32_t blk = z0; blk < z1; blk += 32 * kTrE) {
+        if (!resident) load_blk(blk);
+#pragma unroll
+        for (int q = 0; q < kTrE; ++q) {
+          const int32_t c = cq[q] - w0;
+          if (cq[q] >= 0 && c >= 0 && c < wn) atomicAdd(&cnt[c], 1);
+        }
+      }
+      __syncwarp();
+      // exclusive scan of the window's counts: lane owns WIN/32 consecutive columns
+      int32_t v[WIN / 32], sum = 0;
+#pragma unroll
+      for (int q = 0; q < WIN / 32; ++q) {
+        v[q] = cnt[lane * (WIN / 32) + q];
+        sum += v[q];
+      }
+      int32_t x = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      int32_t run = before + x - sum;
+#pragma unroll
+      for (int q = 0; q < WIN / 32; ++q) {
+        const int32_t c = lane * (WIN / 32) + q;
+        cnt[c] = run;  // becomes the column's cursor (slot relative to z0)
+        if (c < wn) rowT[g0 + w0 + c] = z0 + run;
+        run += v[q];
+      }
+      before += __shfl_sync(0xffffffffu, x, 31);
+      __syncwarp();
+      // stable scatter, 32 entries at a time in storage order
+      for (int32_t blk = z0; blk < z1; blk += 32 * kTrE) {
+        if (!resident) load_blk(blk);
+#pragma unroll
+        for (int q = 0; q < kTrE; ++q) {
+          const int32_t e = blk + 32 * q + lane;
+          if (blk + 32 * q >= z1) break;  // warp-uniform
+          const int32_t c = cq[q] >= 0 ? cq[q] - w0 : -1;
+          const bool in = c >= 0 && c < wn;
+          const uint32_t peers = __match_any_sync(0xffffffffu, in ? c : -1);
+          if (in) {
+            const int32_t slot = cnt[c] + __popc(peers & lt);
+            // row of entry e: the last r with rp[r] <= e (empty rows share rp)
+            int32_t lo = 0, hi = n - 1;
+            while (lo < hi) {
+              const int32_t mid = (lo + hi + 1) >> 1;
+              if ((rp_s ? rps[mid] : __ldg(rp + mid)) <= e) lo = mid;
+              else hi = mid - 1;
+            }
+            colT[z0 + slot] = lo;
+            valsT[z0 + slot] = vq[q];  // bitwise move
+          }
+          __syncwarp();
+          if (in && (peers & lt) == 0) cnt[c] += __popc(peers);
+          __syncwarp();
+        }
       }
     }
   }
 }
 
-cudaError_t launch_transpose_expand(int32_t batch, const int64_t* row_off, const int32_t* sizes,
-                                    const int32_t* row_ptr, const int32_t* col, int32_t* idx, int64_t* nnz_off,
-                                    cudaStream_t s) {
+cudaError_t launch_transpose_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
+                                 const int32_t* col, const float* vals, int32_t* rowT, int32_t* colT, float* valsT,
+                                 int32_t max_rows_hint, int32_t num_sms, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  const int grid = batch < 65535 ? batch : 65535;
-  transpose_expand_kernel<<<grid, kBwdThreads, 0, s>>>(batch, row_off, sizes, row_ptr, col, idx, nnz_off);
+  const int64_t need = ((int64_t)batch + kTrWarps - 1) / kTrWarps;
+  const int grid = (int)std::min<int64_t>(need, (int64_t)num_sms * 8);
+  // window: 256 columns when the hinted rows fit, else 512 (fewer passes over big matrices)
+  if (max_rows_hint > 0 && max_rows_hint <= 256)
+    transpose_csr_kernel<256><<<grid, kTrWarps * 32, 0, s>>>(batch, row_off, sizes, row_ptr, col, vals, rowT, colT,
+                                                             valsT);
+  else
+    transpose_csr_kernel<512><<<grid, kTrWarps * 32, 0, s>>>(batch, row_off, sizes, row_ptr, col, vals, rowT, colT,
+                                                             valsT);
   return cudaGetLastError();
 }
 
@@ -139,7 +257,8 @@ template <int CH, bool STAGED>
 __device__ __forceinline__ void sddmm_rows(int32_t n, int32_t chunks, const float* __restrict__ Bsrc, int64_t bld,
                                            const float* __restrict__ Grow0, int64_t ldg,
                                            const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                           float* __restrict__ out, int lane, int warp, int nw) {
+                                           float* __restrict__ out, int lane, int warp, int nw,
+                                           uint64_t* bar = nullptr, uint32_t phase = 0) {
   // rows r = warp, warp + nw, ...; the next row's grad_C chunks and row range
   // are loaded while the current row computes (one exposed latency per matrix)
   float4 gn[CH];
@@ -157,6 +276,8 @@ __device__ __forceinline__ void sddmm_rows(int32_t n, int32_t chunks, const floa
     n1 = __ldg(rp + warp + 1);
     gload(warp, gn);
   }
+  // staged: the first row's grad_C loads are in flight while B_i lands
+  if (STAGED) mbar_wait(bar, phase);
   for (int32_t r = warp; r < n; r += nw) {
     const int32_t e0 = n0, e1 = n1;
     float4 gv[CH];
@@ -228,8 +349,9 @@ __global__ void __launch_bounds__(kBwdThreads) sddmm_staged_kernel(int32_t batch
                                                                   const int32_t* __restrict__ row_ptr,
                                                                   const int32_t* __restrict__ col,
                                                                   const float* __restrict__ B, int64_t ldb,
-                                                                  const float* __restrict__ G, int64_t ldg,
-                                                                  float* __restrict__ out, int32_t cap_bytes) {
+                                                                  const float* __restrict__ G_, int64_t ldg,
+                                                                  float* __restrict__ out, int32_t cap_bytes,
+                                                                  int32_t dbg) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   float* Bs = reinterpret_cast<float*>(smem);
@@ -241,10 +363,24 @@ __global__ void __launch_bounds__(kBwdThreads) sddmm_staged_kernel(int32_t batch
   }
   __syncthreads();
   uint32_t phase = 0;
-  for (int64_t i = blockIdx.x; i < batch; i += gridDim.x) {
-    const int64_t g0 = row_off[i];
-    const int32_t n = sizes ? sizes[i] : (int32_t)(row_off[i + 1] - g0);
+  // matrix metadata two matrices ahead (loads in flight across an iteration):
+  // matrix i's row range is known when its iteration starts, and matrix
+  // i + grid's B_i is bulk-prefetched into L2 one matrix ahead, so its TMA
+  // copy hits L2 (C5 SDDMM 1099 -> 1074 us; prefetching grad_C_i too measured
+  // slower, 1116 us, with ~1 GB of extra DRAM reads: lines evicted before use)
+  const int64_t G = gridDim.x;
+  auto meta_g = [&](int64_t m) -> int64_t { return m < batch ? row_off[m] : 0; };
+  auto meta_n = [&](int64_t m, int64_t g) -> int32_t {
+    return m < batch ? (sizes ? sizes[m] : (int32_t)(row_off[m + 1] - g)) : 0;
+  };
+  int64_t g0 = meta_g(blockIdx.x), g1m = meta_g(blockIdx.x + G);
+  int32_t n = meta_n(blockIdx.x, g0), n1m = meta_n(blockIdx.x + G, g1m);
+  for (int64_t i = blockIdx.x; i < batch; i += G) {
+    const int64_t g2m = meta_g(i + 2 * G);
+    const int32_t n2m = meta_n(i + 2 * G, g2m);
     const bool staged = n > 0 && (int64_t)n * k * 4 <= cap_bytes;
+    if (threadIdx.x == 0 && n1m > 0 && !(dbg & 512))
+      bulk_prefetch_l2(B + g1m * ldb, (uint32_t)(((int64_t)(n1m - 1) * ldb + k) * 4));
     if (staged) {
       if (threadIdx.x == 0) {
         const uint32_t bytes = (uint32_t)n * (uint32_t)k * 4u;
@@ -255,20 +391,22 @@ __global__ void __launch_bounds__(kBwdThreads) sddmm_staged_kernel(int32_t batch
           for (int32_t r = 0; r < n; ++r) bulk_g2s(Bs + (int64_t)r * k, B + (g0 + r) * ldb, (uint32_t)k * 4u, &bar);
         }
       }
-      mbar_wait(&bar, phase);
+      sddmm_rows<CH, true>(n, chunks, Bs, k, G_ + g0 * ldg, ldg, row_ptr + g0, col, out, lane, warp, nw, &bar,
+                           phase);
       phase ^= 1u;
-      sddmm_rows<CH, true>(n, chunks, Bs, k, G + g0 * ldg, ldg, row_ptr + g0, col, out, lane, warp, nw);
     } else {
-      sddmm_rows<CH, false>(n, chunks, B + g0 * ldb, ldb, G + g0 * ldg, ldg, row_ptr + g0, col, out, lane, warp,
+      sddmm_rows<CH, false>(n, chunks, B + g0 * ldb, ldb, G_ + g0 * ldg, ldg, row_ptr + g0, col, out, lane, warp,
                             nw);
     }
+    g0 = g1m, n = n1m, g1m = g2m, n1m = n2m;
     __syncthreads();  // every warp is done with Bs before the next matrix's copy
   }
 }
 
 cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
-                         int64_t ldg, float* out, int32_t max_rows_hint, int32_t num_sms, cudaStream_t s) {
+                         int64_t ldg, float* out, int32_t max_rows_hint, int32_t num_sms, int32_t dbg,
+                         cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   const bool vec = (k % 4 == 0) && (ldb % 4 == 0) && (ldg % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(G)) & 15u) == 0;
@@ -286,7 +424,7 @@ cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
         if (e != cudaSuccess) return;
       }
-      kern<<<grid, kBwdThreads, cap, s>>>(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, cap);
+      kern<<<grid, kBwdThreads, cap, s>>>(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, cap, dbg);
       e = cudaGetLastError();
     };
     if (ch <= 1) go(sddmm_staged_kernel<1>);

@@ -256,7 +256,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 255) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 1023) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -620,50 +620,32 @@ BSPMM_API bspmm_status_t bspmm_coo_atomic(bspmm_handle_t h, int32_t batch, int32
 }
 
 // ---- backward (NEXT-2) ------------------------------------------------------
-// workspace: [idx 2*NNZ i32][nnz_off (batch+1) i64][keys 2*NNZ u64][pay 2*NNZ u32]
-//            [+ rowT (N+1) i32, colT NNZ i32, valsT NNZ f32 when the transpose is internal]
+// workspace (grad_B only): rowT (N+1) i32, colT NNZ i32, valsT NNZ f32 -- the internal A^T
 struct TransWs {
-  int32_t* idx;
-  int64_t* nnz_off;
-  uint64_t* keys;
-  uint32_t* pay;
   int32_t *rowT, *colT;
   float* valsT;
 };
 
-static bspmm_status_t trans_workspace(bspmm_handle_t h, int32_t batch, int64_t N, int64_t NNZ, bool internal,
-                                      TransWs* w) {
+static bspmm_status_t trans_workspace(bspmm_handle_t h, int64_t N, int64_t NNZ, TransWs* w) {
   size_t off = 0;
-  const size_t o_idx = off;
-  off += al256((size_t)2 * NNZ * 4 + 4);
-  const size_t o_no = off;
-  off += al256((size_t)(batch + 1) * 8);
-  const size_t o_keys = off;
-  off += al256((size_t)2 * NNZ * 8 + 8);
-  const size_t o_pay = off;
-  off += al256((size_t)2 * NNZ * 4 + 4);
   const size_t o_rt = off;
-  off += internal ? al256((size_t)(N + 1) * 4) : 0;
+  off += al256((size_t)(N + 1) * 4);
   const size_t o_ct = off;
-  off += internal ? al256((size_t)NNZ * 4 + 4) : 0;
+  off += al256((size_t)NNZ * 4 + 4);
   const size_t o_vt = off;
-  off += internal ? al256((size_t)NNZ * 4 + 4) : 0;
+  off += al256((size_t)NNZ * 4 + 4);
   bspmm_status_t st = grow(h, &h->ws, &h->ws_bytes, off);
   if (st != BSPMM_SUCCESS) return st;
   char* b = static_cast<char*>(h->ws);
-  w->idx = reinterpret_cast<int32_t*>(b + o_idx);
-  w->nnz_off = reinterpret_cast<int64_t*>(b + o_no);
-  w->keys = reinterpret_cast<uint64_t*>(b + o_keys);
-  w->pay = reinterpret_cast<uint32_t*>(b + o_pay);
-  w->rowT = internal ? reinterpret_cast<int32_t*>(b + o_rt) : nullptr;
-  w->colT = internal ? reinterpret_cast<int32_t*>(b + o_ct) : nullptr;
-  w->valsT = internal ? reinterpret_cast<float*>(b + o_vt) : nullptr;
+  w->rowT = reinterpret_cast<int32_t*>(b + o_rt);
+  w->colT = reinterpret_cast<int32_t*>(b + o_ct);
+  w->valsT = reinterpret_cast<float*>(b + o_vt);
   return BSPMM_SUCCESS;
 }
 
 static bspmm_status_t transpose_impl(bspmm_handle_t h, int32_t batch, const int64_t* row_off, const int32_t* sizes,
-                                     const int32_t* row_ptr, const int32_t* col, const float* vals, int64_t NNZ,
-                                     int32_t* rowT, int32_t* colT, float* valsT, const TransWs& w) {
+                                     const int32_t* row_ptr, const int32_t* col, const float* vals, int32_t* rowT,
+                                     int32_t* colT, float* valsT) {
   if (h->flags & BSPMM_VALIDATE) {
     CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
     CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr, col, h->dev_flag, h->stream));
@@ -671,11 +653,8 @@ static bspmm_status_t transpose_impl(bspmm_handle_t h, int32_t batch, const int6
     bspmm_status_t st = check_validate_flag(h);
     if (st != BSPMM_SUCCESS) return st;
   }
-  CK(h, launch_transpose_expand(batch, row_off, sizes, row_ptr, col, w.idx, w.nnz_off, h->stream));
-  h->launches++;
-  const int32_t cap = coo_smem_cap(h->hint_nnz, h->smem_optin);
-  CK(h, launch_coo2csr(batch, row_off, sizes, w.nnz_off, w.idx, vals, rowT, colT, valsT, w.keys, w.pay, NNZ, cap,
-                       h->stream));
+  CK(h, launch_transpose_csr(batch, row_off, sizes, row_ptr, col, vals, rowT, colT, valsT, h->hint_rows, h->num_sms,
+                             h->stream));
   h->launches++;
   return BSPMM_SUCCESS;
 }
@@ -691,10 +670,7 @@ BSPMM_API bspmm_status_t bspmm_csr_transpose(bspmm_handle_t h, int32_t batch, co
   if (!row_off || !row_ptr || !rowT_out || (total_nnz > 0 && (!col || !vals || !colT_out || !valsT_out)))
     return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
   DeviceGuard g(h->device);
-  TransWs w;
-  bspmm_status_t st = trans_workspace(h, batch, total_rows, total_nnz, false, &w);
-  if (st != BSPMM_SUCCESS) return st;
-  return transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, total_nnz, rowT_out, colT_out, valsT_out, w);
+  return transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, rowT_out, colT_out, valsT_out);
 }
 
 BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
@@ -713,6 +689,7 @@ BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k,
     if (st != BSPMM_SUCCESS) return st;
   }
   CK(h, launch_sddmm(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, h->hint_rows, h->num_sms,
+                     h->dbg,
                      h->stream));
   h->launches++;
   return BSPMM_SUCCESS;
@@ -736,9 +713,9 @@ BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int
   }
   if (grad_B) {  // dL/dB_i = A_i^T grad_C_i: transpose, then the forward kernel
     TransWs w;
-    bspmm_status_t st = trans_workspace(h, batch, total_rows, total_nnz, true, &w);
+    bspmm_status_t st = trans_workspace(h, total_rows, total_nnz, &w);
     if (st != BSPMM_SUCCESS) return st;
-    st = transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, total_nnz, w.rowT, w.colT, w.valsT, w);
+    st = transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, w.rowT, w.colT, w.valsT);
     if (st != BSPMM_SUCCESS) return st;
     return csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
   }

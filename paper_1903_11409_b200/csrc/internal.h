@@ -93,12 +93,13 @@ cudaError_t launch_spmm_coo_atomic(int32_t batch, int32_t k, const int64_t* row_
                                    const int64_t* nnz_off, const int32_t* idx, const float* vals, const float* B,
                                    int64_t ldb, float* C, int64_t ldc, int32_t max_rows, int32_t smem_optin,
                                    cudaStream_t s);
-cudaError_t launch_transpose_expand(int32_t batch, const int64_t* row_off, const int32_t* sizes,
-                                    const int32_t* row_ptr, const int32_t* col, int32_t* idx, int64_t* nnz_off,
-                                    cudaStream_t s);
+cudaError_t launch_transpose_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
+                                 const int32_t* col, const float* vals, int32_t* rowT, int32_t* colT, float* valsT,
+                                 int32_t max_rows_hint, int32_t num_sms, cudaStream_t s);
 cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
-                         int64_t ldg, float* out, int32_t max_rows_hint, int32_t num_sms, cudaStream_t s);
+                         int64_t ldg, float* out, int32_t max_rows_hint, int32_t num_sms, int32_t dbg,
+                         cudaStream_t s);
 cudaError_t launch_validate_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes,
                                 const int32_t* row_ptr, const int32_t* col, int* flag, cudaStream_t s);
 cudaError_t launch_validate_coo(int32_t batch, const int64_t* row_off, const int32_t* sizes,

@@ -74,7 +74,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int32_t 
       : "memory");
 }
 
-// L2 prefetch (fire-and-forget: no completion tracking, no SM-side state)
+// L2 prefetch (fire-and-forget: no completion tracking, no SM-side state):
+// bytes at a 16-byte-aligned address, rounded down to a multiple of 16
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  bytes &= ~15u;
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // ---- cp.async (LDGSTS), 4 bytes, + arrive-on when this thread's copies land
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");

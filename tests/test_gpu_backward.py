@@ -79,3 +79,21 @@ def test_sddmm_integer_exact(h):
     out = h.sddmm(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.B), T(G)).cpu().numpy()
     ref, _ = oracle.sddmm(b.k, b.row_off, None, b.row_ptr, b.col, b.B, G)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("hints", [(0, 0), (60, 200), (300, 2000), (600, 3000)])
+def test_transpose_paths_bitexact(h, hints):
+    """Every transpose variant (256/512-column windows, shared-memory row ids or
+    binary search, several windows per matrix) gives the oracle's canonical A^T:
+    a mixed batch with small, medium (> 256 entries) and wide (> 512 rows)
+    matrices, duplicates and empty rows, under several planner hints."""
+    rng = np.random.default_rng(sum(hints) + 7)
+    parts = [synth.random_batch(rng, 20, 4, nmax=40, dmax=6, duplicates=True),
+             synth.generate(synth.MIX, (200, 300, 2, 5), 6, 4, seed=11),
+             synth.generate(synth.MIX, (520, 700, 1, 3), 2, 4, seed=12)]
+    h.set_hints(*hints)
+    try:
+        for b in parts:
+            check_transpose(h, b)
+    finally:
+        h.set_hints(0, 0)

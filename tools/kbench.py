@@ -97,6 +97,14 @@ def backward(h, r):  # NEXT-2: grad_B = A^T grad_C (transpose + SpMM) and grad_v
     h.csr_backward(r["ro"], None, r["rp"], r["col"], r["vals"], r["B"], r["C"])
 
 
+def transpose_only(h, r):  # NEXT-2 piece: A^T (expand + device COO->CSR)
+    h.csr_transpose(r["ro"], None, r["rp"], r["col"], r["vals"])
+
+
+def sddmm_only(h, r):  # NEXT-2 piece: grad_vals = <grad_C[row], B[col]> (C stands in for grad_C)
+    h.sddmm(r["ro"], None, r["rp"], r["col"], r["B"], r["C"])
+
+
 def copy_only(h, r):  # practical floor: a device copy moving B's bytes in and C's out
     r["C"].copy_(r["B"])
 
@@ -120,6 +128,7 @@ def main():
     ap.add_argument("--copy-baseline", action="store_true", help="also time C.copy_(B) on the same replicas")
     ap.add_argument("--shard", type=int, default=1, help="time rank 0's shard of an N-way split (1 GPU)")
     ap.add_argument("--backward", action="store_true", help="also time csr_backward (grad_B and grad_vals)")
+    ap.add_argument("--sddmm-dbg", default="", help="with --backward: debug bit sets for extra SDDMM timings")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -168,6 +177,12 @@ def main():
         extra = {}
         if args.backward:
             extra["backward_us"] = time_calls(h, reps, max(3, R // 4), backward) * 1e3
+            extra["transpose_us"] = time_calls(h, reps, max(3, R // 4), transpose_only) * 1e3
+            extra["sddmm_us"] = time_calls(h, reps, max(3, R // 4), sddmm_only) * 1e3
+            for d in [int(x) for x in args.sddmm_dbg.split(",") if x]:
+                h.set_debug(d)
+                extra[f"sddmm_us_dbg{d}"] = time_calls(h, reps, max(3, R // 4), sddmm_only) * 1e3
+            h.set_debug(0)
         if args.copy_baseline:
             ms_cp = time_calls(h, reps, R, copy_only)
             extra["copy_us"] = ms_cp * 1e3
