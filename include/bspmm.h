@@ -142,8 +142,9 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * CTA; 8 = consumers repeat each unit's work 4 times;
  * 16 = (unused; was an L2 prefetch of small problems, no gain); 32 = always copy
  * the CSR slice with TMA; 64 = force the static unit schedule; 128 = force the
- * dynamic one; 512 = SDDMM without the L2 prefetch of the next matrix's
- * B_i.  0 (default) = normal. */
+ * dynamic one; 256 = SDDMM by the standalone kernel instead of the SpMM
+ * pipeline's SDDMM mode; 512 = standalone SDDMM without the L2 prefetch of
+ * the next matrix's B_i.  0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */

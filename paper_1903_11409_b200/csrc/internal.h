@@ -69,6 +69,9 @@ struct CsrArgs {
   const int32_t* coo_idx = nullptr;     // fused COO mode: (row, col) pairs
   int* err = nullptr;                   // device error flag (bit 64: COO unit over stage capacity)
   int32_t mc = 0;                       // NEXT-4b: C is a multicast VA (multimem.st epilogue)
+  const float* G = nullptr;             // SDDMM mode (NEXT-2): sd_out[e] = <G[row_e], B[col_e]>
+  int64_t ldg = 0;
+  float* sd_out = nullptr;
 };
 
 // kernels (.cu)

@@ -59,6 +59,11 @@ struct SpmmParams {
   const int32_t* __restrict__ idx;   // [nnz][2] (row, col) local pairs
   int* err;                          // device flag: bit 64 = a unit exceeded the stage (hint too small)
   int32_t mc;                        // NEXT-4b: C is a multicast address (EPI == 2: multimem.st stores)
+  // SDDMM mode (EPI == 3, NEXT-2 backward): sd_out[e] = <G[row_e], B[col_e]>
+  // over the staged B_i, whole-row units (tiles == 1); C is not written
+  const float* __restrict__ G;
+  int64_t ldg;
+  float* __restrict__ sd_out;
 };
 
 // GCN epilogue (NEXT-1, PAPER.md Fig. algo:graph_conv_batched): A (U + 1 b^T)
@@ -789,6 +794,100 @@ __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const Unit
   }
 }
 
+// SDDMM rows (EPI == 3): the same sub-warp row ownership and staged B_i as
+// the SpMM, but each entry's result is a dot product: lane li holds its float4
+// chunks of the row's grad_C (loaded one row ahead from global memory), forms
+// its partial <G[r], B[col_e]> over them (fixed order), and the L lanes of the
+// sub-warp reduce it with a fixed xor butterfly (deterministic; within the
+// north_star bound of the fp64 oracle O6).  BST: B tile and CSR slice staged.
+// Used for latency-bound batches only: streaming batches keep too few grad_C
+// bytes in flight per SM this way (ld.global through the L1 left beside a
+// 190 KB ring; C5 1650 us vs 1071 us for the standalone kernel).
+template <int CH, bool BST>
+__device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
+                                           int step, int li, int sub) {
+  const int L = p.lanes;
+  const int32_t cols = h.kw >> 2;
+  bool ok[CH];
+#pragma unroll
+  for (int v = 0; v < CH; ++v) ok[v] = li + v * L < cols;
+  const unsigned char* sreg = st + p.stage_b;
+  const int32_t* rp = BST ? reinterpret_cast<const int32_t*>(sreg + 2 * slice_region(h.nnz)) + (h.g0 & 3)
+                          : p.row_ptr + h.g0;
+  const int32_t* ci = BST ? reinterpret_cast<const int32_t*>(sreg) + (h.nz0 & 3) - h.nz0 : p.col;
+  const float* Bt = BST ? reinterpret_cast<const float*>(st) + 4 * li : p.B + h.g0 * p.ldb + h.c0 + 4 * li;
+  const int64_t bstride = BST ? (int64_t)h.kw : p.ldb;
+  const float* Gt = p.G + h.g0 * p.ldg + h.c0 + 4 * li;
+  const uint32_t mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (sub * L));
+  auto gload = [&](int r_, float4* dst) {
+    const float* g = Gt + (int64_t)r_ * p.ldg;
+#pragma unroll
+    for (int v = 0; v < CH; ++v) dst[v] = ok[v] ? ldg_nc_f4(g + 4 * v * L) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto bload = [&](int32_t c, int v) -> float4 {
+    const float* b = Bt + (int64_t)c * bstride + 4 * v * L;
+    return BST ? *reinterpret_cast<const float4*>(b) : ldg_nc_f4(b);
+  };
+  auto dot = [&](const float4* g, const float4* b) {
+    float q = 0.f;
+#pragma unroll
+    for (int v = 0; v < CH; ++v) {
+      q = fmaf(g[v].x, b[v].x, q);
+      q = fmaf(g[v].y, b[v].y, q);
+      q = fmaf(g[v].z, b[v].z, q);
+      q = fmaf(g[v].w, b[v].w, q);
+    }
+    return q;
+  };
+  int r = first;
+  int32_t nx0 = 0, nx1 = 0;
+  float4 gn[CH];
+  if (r < h.n) {
+    nx0 = rp[r];
+    nx1 = rp[r + 1];
+    gload(r, gn);
+  }
+  for (; r < h.n; r += step) {
+    const int32_t e1 = nx1;
+    int32_t e = nx0;
+    float4 gv[CH];
+#pragma unroll
+    for (int v = 0; v < CH; ++v) gv[v] = gn[v];
+    if (r + step < h.n) {  // next row's range and grad_C chunks, loaded ahead
+      nx0 = rp[r + step];
+      nx1 = rp[r + step + 1];
+      gload(r + step, gn);
+    }
+    for (; e + 1 < e1; e += 2) {
+      const int32_t c0 = ci[e], c1 = ci[e + 1];
+      float4 b0[CH], b1[CH];
+#pragma unroll
+      for (int v = 0; v < CH; ++v) {
+        b0[v] = ok[v] ? bload(c0, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        b1[v] = ok[v] ? bload(c1, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float q0 = dot(gv, b0), q1 = dot(gv, b1);
+      for (int d = L >> 1; d > 0; d >>= 1) {
+        q0 += __shfl_xor_sync(mask, q0, d);
+        q1 += __shfl_xor_sync(mask, q1, d);
+      }
+      if (li == 0) {
+        p.sd_out[e] = q0;
+        p.sd_out[e + 1] = q1;
+      }
+    }
+    if (e < e1) {
+      const int32_t c0 = ci[e];
+      float4 b0[CH];
+#pragma unroll
+      for (int v = 0; v < CH; ++v) b0[v] = ok[v] ? bload(c0, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float q0 = dot(gv, b0);
+      for (int d = L >> 1; d > 0; d >>= 1) q0 += __shfl_xor_sync(mask, q0, d);
+      if (li == 0) p.sd_out[e] = q0;
+    }
+  }
+}
+
 template <int CH, bool VEC, int EPI>
 __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& h, int first, int step, int li) {
   constexpr int FW = VEC ? 4 : 1;
@@ -923,7 +1022,10 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
       coo_convert(p, h, const_cast<unsigned char*>(st), threadIdx.x - 32, W * 32);
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
     for (int rep = 0; rep < reps && (h.flags & 4) == 0; ++rep) {  // 4: COO unit over capacity (skipped, flagged)
-      if ((h.flags & 3) == 3) {  // the hot, staged case
+      if (EPI == 3) {  // SDDMM mode (NEXT-2)
+        if ((h.flags & 3) == 3) rows_sddmm<CH, true>(p, h, st, first, step, li, sub);
+        else rows_sddmm<CH, false>(p, h, st, first, step, li, sub);
+      } else if ((h.flags & 3) == 3) {  // the hot, staged case
         if (VEC && (h.kw >> 2) == p.lanes * CH) rows_staged_full<CH, EPI>(p, h, st, first, step, li);
         else rows<CH, VEC, true, true, EPI>(p, h, st, first, step, li);
       } else {
@@ -1005,6 +1107,9 @@ static cudaError_t launch_e(int epi, const SpmmParams& sp, const TmaMaps& maps, 
     }
     return cudaErrorInvalidValue;
   }
+  if constexpr (VEC) {
+    if (epi == 3) return launch_t<CH, VEC, 3>(sp, maps, plan, s);
+  }
   if (epi == 2) return launch_t<CH, VEC, 2>(sp, maps, plan, s);
   if (epi == 1) return launch_t<CH, VEC, 1>(sp, maps, plan, s);
   return launch_t<CH, VEC, 0>(sp, maps, plan, s);
@@ -1039,8 +1144,12 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.bias = a.bias;
   sp.accumulate = a.accumulate;
   sp.mc = a.mc;
-  // epilogue variant: 0 plain store, 1 GCN (bias / accumulate), 2 multicast store
-  const int epi = a.mc ? 2 : (a.bias != nullptr || a.accumulate != 0) ? 1 : 0;
+  sp.G = a.G;
+  sp.ldg = a.ldg;
+  sp.sd_out = a.sd_out;
+  // epilogue variant: 0 plain store, 1 GCN (bias / accumulate), 2 multicast store, 3 SDDMM
+  const int epi = a.sd_out ? 3 : a.mc ? 2 : (a.bias != nullptr || a.accumulate != 0) ? 1 : 0;
+  if (epi == 3 && (!plan.vec || plan.tiles != 1)) return cudaErrorInvalidValue;
   sp.sched = a.sched;
   sp.nnz_off = a.coo_nnz_off;
   sp.idx = a.coo_idx;

@@ -97,3 +97,62 @@ def test_transpose_paths_bitexact(h, hints):
             check_transpose(h, b)
     finally:
         h.set_hints(0, 0)
+
+
+def _sddmm_check(h, b, G, ld=None, exact=False):
+    k = b.k
+    ldb = k if ld is None else ld
+    Bp = np.zeros((b.n_rows, ldb), dtype=np.float32)
+    Bp[:, :k] = b.B
+    Gp = np.zeros((b.n_rows, ldb), dtype=np.float32)
+    Gp[:, :k] = G
+    out = h.sddmm(T(b.row_off), None, T(b.row_ptr), T(b.col), T(Bp), T(Gp), k=k).cpu().numpy()
+    ref, bound = oracle.sddmm(k, b.row_off, None, b.row_ptr, b.col, b.B, G)
+    if exact:
+        assert np.array_equal(out, ref)
+    ok, worst = oracle.check_bound(out, ref, bound)
+    assert ok, worst
+
+
+@pytest.mark.parametrize("dbg", [0, 256])
+@pytest.mark.parametrize("cid", [2, 3, 4])
+def test_sddmm_paths(h, cid, dbg):
+    """SDDMM through the SpMM pipeline's SDDMM mode (latency-bound batches) and
+    the standalone kernel (debug bit 256): integer-valued inputs exactly (every
+    summation order is exact), U[-1,1) inputs within 1e-5 * sum |g||b|."""
+    h.set_debug(dbg)
+    try:
+        b = synth.config(cid, int_valued=True)
+        h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+        G = np.random.default_rng(cid).integers(-4, 5, size=(b.n_rows, b.k)).astype(np.float32)
+        _sddmm_check(h, b, G, exact=True)
+        b = synth.config(cid)
+        _sddmm_check(h, b, grad(b, cid + 10))
+    finally:
+        h.set_debug(0)
+        h.set_hints(0, 0)
+
+
+@pytest.mark.parametrize("k,ld", [(64, 68), (128, 132), (512, 520), (20, 24)])
+def test_sddmm_mode_ld_and_direct_units(h, k, ld):
+    """SDDMM mode with ld > k (per-row B staging), and matrices above the
+    planner hint (the unit computes from global memory, paper case 3)."""
+    rng = np.random.default_rng(k + ld)
+    b = synth.random_batch(rng, 40, k, nmax=40, dmax=6, duplicates=True)
+    _sddmm_check(h, b, grad(b, k), ld=ld)
+    h.set_hints(8, 16)  # most matrices exceed the stage: direct units
+    try:
+        _sddmm_check(h, b, grad(b, k + 1))
+    finally:
+        h.set_hints(0, 0)
+
+
+def test_sddmm_streaming_batch(h):
+    """A batch above 8 matrices per SM takes the standalone kernel: C5's first
+    4096 graphs, bound-checked."""
+    b = synth.config(5, i0=0, i1=4096)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    try:
+        _sddmm_check(h, b, grad(b, 5))
+    finally:
+        h.set_hints(0, 0)
