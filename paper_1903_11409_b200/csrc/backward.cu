@@ -35,7 +35,9 @@ constexpr int kBwdThreads = 256;
 // entry's row is then a binary search there), and each block of 256 entries'
 // columns and values land in registers (8 per lane) in one round trip, kept
 // for the scatter when the matrix has <= 256 entries.
-// Shared memory per warp: WIN column cursors + kTrRp row pointers.
+// Shared memory per warp: WIN column cursors, kTrRp row pointers and up to
+// `ridcap` row ids (every entry's row, filled from the shared row pointers, so
+// the scatter needs no search; above the capacity: binary search).
 constexpr int kTrWarps = 8;
 constexpr int kTrRp = 516;  // row-pointer slice capacity (n_i <= 515; larger: search in global memory)
 constexpr int kTrE = 8;     // entries per lane per block (256-entry blocks)
@@ -47,12 +49,12 @@ __global__ void __launch_bounds__(kTrWarps * 32) transpose_csr_kernel(int32_t ba
                                                                       const float* __restrict__ vals,
                                                                       int32_t* __restrict__ rowT,
                                                                       int32_t* __restrict__ colT,
-                                                                      float* __restrict__ valsT) {
-  __shared__ int32_t cnt_all[kTrWarps][WIN];
-  __shared__ int32_t rps_all[kTrWarps][kTrRp];
+                                                                      float* __restrict__ valsT, int32_t ridcap) {
+  extern __shared__ __align__(16) int32_t tr_smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int32_t* cnt = cnt_all[w];
-  int32_t* rps = rps_all[w];
+  int32_t* cnt = tr_smem + (size_t)w * (WIN + kTrRp + ridcap);
+  int32_t* rps = cnt + WIN;
+  int32_t* rid = rps + kTrRp;
   const uint32_t lt = (1u << lane) - 1u;
   for (int64_t i = (int64_t)blockIdx.x * kTrWarps + w; i < batch; i += (int64_t)gridDim.x * kTrWarps) {
     const int64_t g0 = row_off[i], g1 = row_off[i + 1];
@@ -74,6 +76,12 @@ __global__ void __launch_bounds__(kTrWarps * 32) transpose_csr_kernel(int32_t ba
       __syncwarp();
     }
     const int32_t z0 = rp_s ? rps[0] : __ldg(rp), z1 = rp_s ? rps[n] : __ldg(rp + n);
+    const bool use_rid = rp_s && z1 - z0 <= ridcap;
+    if (use_rid) {
+      for (int32_t r = lane; r < n; r += 32)
+        for (int32_t e = rps[r], e1 = rps[r + 1]; e < e1; ++e) rid[e - z0] = r;
+      __syncwarp();
+    }
     for (int64_t g = g0 + n + lane; g < g1; g += 32) rowT[g] = z1;  // padding rows: empty
     if (i == batch - 1 && lane == 0) rowT[g1] = row_ptr[g1];
     // one 256-entry block in registers: column ids (-1 past the end) and values
@@ -141,6 +149,7 @@ __global__ void __launch_bounds__(kTrWarps * 32) transpose_csr_kernel(int32_t ba
             const int32_t slot = cnt[c] + __popc(peers & lt);
             // row of entry e: the last r with rp[r] <= e (empty rows share rp)
             int32_t lo = 0, hi = n - 1;
+            if (use_rid) lo = hi = rid[e - z0];
             while (lo < hi) {
               const int32_t mid = (lo + hi + 1) >> 1;
               if ((rp_s ? rps[mid] : __ldg(rp + mid)) <= e) lo = mid;
@@ -160,18 +169,27 @@ __global__ void __launch_bounds__(kTrWarps * 32) transpose_csr_kernel(int32_t ba
 
 cudaError_t launch_transpose_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
                                  const int32_t* col, const float* vals, int32_t* rowT, int32_t* colT, float* valsT,
-                                 int32_t max_rows_hint, int32_t num_sms, cudaStream_t s) {
+                                 int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   const int64_t need = ((int64_t)batch + kTrWarps - 1) / kTrWarps;
   const int grid = (int)std::min<int64_t>(need, (int64_t)num_sms * 8);
+  // row-id capacity: the hinted largest matrix up to 1536 entries (no hint: search)
+  const int32_t ridcap = max_nnz_hint > 0 ? (int32_t)std::min<int64_t>((max_nnz_hint + 3) & ~3LL, 1536) : 0;
   // window: 256 columns when the hinted rows fit, else 512 (fewer passes over big matrices)
-  if (max_rows_hint > 0 && max_rows_hint <= 256)
-    transpose_csr_kernel<256><<<grid, kTrWarps * 32, 0, s>>>(batch, row_off, sizes, row_ptr, col, vals, rowT, colT,
-                                                             valsT);
-  else
-    transpose_csr_kernel<512><<<grid, kTrWarps * 32, 0, s>>>(batch, row_off, sizes, row_ptr, col, vals, rowT, colT,
-                                                             valsT);
-  return cudaGetLastError();
+  const bool small = max_rows_hint > 0 && max_rows_hint <= 256;
+  const int smem = kTrWarps * ((small ? 256 : 512) + kTrRp + ridcap) * 4;
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return;
+    }
+    kern<<<grid, kTrWarps * 32, smem, s>>>(batch, row_off, sizes, row_ptr, col, vals, rowT, colT, valsT, ridcap);
+    e = cudaGetLastError();
+  };
+  if (small) go(transpose_csr_kernel<256>);
+  else go(transpose_csr_kernel<512>);
+  return e;
 }
 
 // out[e] = sum_c G[row_e][c] * B[col_e][c]; VEC: float4 chunks (k, ldb, ldg % 4 == 0, aligned)

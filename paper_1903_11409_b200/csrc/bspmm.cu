@@ -653,7 +653,7 @@ static bspmm_status_t transpose_impl(bspmm_handle_t h, int32_t batch, const int6
     bspmm_status_t st = check_validate_flag(h);
     if (st != BSPMM_SUCCESS) return st;
   }
-  CK(h, launch_transpose_csr(batch, row_off, sizes, row_ptr, col, vals, rowT, colT, valsT, h->hint_rows, h->num_sms,
+  CK(h, launch_transpose_csr(batch, row_off, sizes, row_ptr, col, vals, rowT, colT, valsT, h->hint_rows, h->hint_nnz, h->num_sms,
                              h->stream));
   h->launches++;
   return BSPMM_SUCCESS;

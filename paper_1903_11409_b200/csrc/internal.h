@@ -98,7 +98,7 @@ cudaError_t launch_spmm_coo_atomic(int32_t batch, int32_t k, const int64_t* row_
                                    cudaStream_t s);
 cudaError_t launch_transpose_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
                                  const int32_t* col, const float* vals, int32_t* rowT, int32_t* colT, float* valsT,
-                                 int32_t max_rows_hint, int32_t num_sms, cudaStream_t s);
+                                 int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms, cudaStream_t s);
 cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
                          int64_t ldg, float* out, int32_t max_rows_hint, int32_t num_sms, int32_t dbg,
