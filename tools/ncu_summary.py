@@ -71,18 +71,28 @@ def launches(path):
     rows = list(csv.reader(io.StringIO(text[start:])))
     hdr = rows[0]
     kn, val, unit = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    agg = {}
+    mn = hdr.index("Metric Name")
+    agg, dram = {}, {}
     for r in rows[1:]:
         if len(r) <= val:
             continue
-        t = float(r[val].replace(",", "")) * SCALE.get(r[unit], 1e-9)
         name = r[kn].split("(")[0].replace("void ", "")
+        v = float(r[val].replace(",", ""))
+        if r[mn] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):  # other metrics of the same launches
+            dram[name] = dram.get(name, 0.0) + v * SCALE.get(r[unit], 1)
+            continue
+        if r[mn] != "gpu__time_duration.sum":
+            continue
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
-        a[1] += t
+        a[1] += v * SCALE.get(r[unit], 1e-9)
     tot = sum(v[1] for v in agg.values())
-    return {"total_s": tot, "kernels": {k: {"launches": n, "total_us": s * 1e6, "mean_us": s / n * 1e6,
-                                            "share": s / tot} for k, (n, s) in agg.items()}}
+    out = {k: {"launches": n, "total_us": s * 1e6, "mean_us": s / n * 1e6, "share": s / tot}
+           for k, (n, s) in agg.items()}
+    for k, b in dram.items():
+        if k in out:
+            out[k]["dram_bytes_per_launch"] = b / out[k]["launches"]
+    return {"total_s": tot, "kernels": out}
 
 
 if __name__ == "__main__":

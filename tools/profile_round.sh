@@ -23,7 +23,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm
   -o $O/full_c4_spmm python tools/kbench.py --configs 4 --ncu-mode > $O/ncu_c4.log 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file $O/launches_c2345.csv python tools/kbench.py --configs 2,3,4,5 --ncu-mode > $O/ncu_cfg.log 2>&1
-# 5. steady-state kernel timings (CUDA graph, replicas > 2x L2) and phase traces
-timeout 300 python tools/kbench.py --configs 2,3,4,5 > $O/kbench.jsonl 2>&1
+# 5. steady-state kernel timings (CUDA graph, replicas > 2x L2; with the backward breakdown) and phase traces
+timeout 400 python tools/kbench.py --configs 2,3,4,5 --backward --copy-baseline > $O/kbench.jsonl 2>&1
+# 6. backward (NEXT-2) on C5: launch list with DRAM bytes, one full capture of the SDDMM
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  --csv --log-file $O/launches_bwd_c5.csv python tools/probe/bwd_once.py 5 > $O/ncu_bwd.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sddmm_staged_kernel -s 1 -c 1 \
+  -o $O/full_c5_sddmm python tools/probe/bwd_once.py 5 > $O/ncu_sddmm.log 2>&1
 (for c in 2 3 4 5; do timeout 60 python tools/trace.py --config $c; done) > $O/trace.jsonl 2>&1
 echo done
