@@ -97,6 +97,10 @@ class Clocks:
             pass
         self.period = period
         self._stop = threading.Event()
+        # samples are kept only while `active` is set (the timed region); the
+        # thread starts before the warm-up so NVML's first-call latency is
+        # paid outside the region
+        self.active = threading.Event()
 
     def _run(self):
         nv = self.nv
@@ -104,8 +108,11 @@ class Clocks:
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
         while not self._stop.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.dev, nv.NVML_CLOCK_SM))
-                self.reasons |= int(get_r(self.dev))
+                mhz = nv.nvmlDeviceGetClockInfo(self.dev, nv.NVML_CLOCK_SM)
+                why = int(get_r(self.dev))
+                if self.active.is_set():
+                    self.samples.append(mhz)
+                    self.reasons |= why
             except Exception:
                 pass
             time.sleep(self.period)
@@ -300,6 +307,7 @@ def main():
         elif C_full is not None:
             bdist.allgather_rows(C_full, bounds)
 
+    clk = Clocks(dev.index).__enter__()
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize(dev)
@@ -310,12 +318,14 @@ def main():
     launches0 = h.launch_count()
     bdist.barrier(dev)
     torch.cuda.synchronize(dev)
-    with Clocks(dev.index) as clk:
-        t0.record(stream)
-        for s in range(K):
-            step(kev[s])
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
+    clk.active.set()
+    t0.record(stream)
+    for s in range(K):
+        step(kev[s])
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk.active.clear()
+    clk.__exit__()
     bdist.barrier(dev)
     launches = h.launch_count() - launches0
     ms_rank = t0.elapsed_time(t1) / K
