@@ -822,7 +822,8 @@ __device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h
   auto gload = [&](int r_, float4* dst) {
     const float* g = Gt + (int64_t)r_ * p.ldg;
 #pragma unroll
-    for (int v = 0; v < CH; ++v) dst[v] = ok[v] ? ldg_nc_f4(g + 4 * v * L) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int v = 0; v < CH; ++v)  // read once: no L1 allocation (C4 10.1 -> 9.5 us)
+      dst[v] = ok[v] ? ldg_na_f4(g + 4 * v * L) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
   auto bload = [&](int32_t c, int v) -> float4 {
     const float* b = Bt + (int64_t)c * bstride + 4 * v * L;
