@@ -256,7 +256,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 1023) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 2047) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -695,7 +695,7 @@ BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k,
   // 512, unaligned or split plans: the standalone kernel below (C5: 1071 vs
   // 1650 us; also forced by debug bit 256)
   const bool aligned = (k % 4 == 0) && (ldb % 4 == 0) && (ldg % 4 == 0) && aligned16(B) && aligned16(G);
-  if (aligned && k <= kMaxVecKt && batch <= 8 * h->num_sms && !(h->dbg & 256)) {
+  if (aligned && k <= kMaxVecKt && (batch <= 8 * h->num_sms || (h->dbg & 1024)) && !(h->dbg & 256)) {
     bspmm_plan_t plan;
     bspmm_status_t st = make_plan(k, batch, true, h->hint_rows, h->hint_nnz, h->num_sms, h->smem_optin, k,
                                   h->tune_warps, h->tune_ctas, h->tune_chunks, &plan);

@@ -800,9 +800,11 @@ __device__ __forceinline__ void rows_staged_full(const SpmmParams& p, const Unit
 // its partial <G[r], B[col_e]> over them (fixed order), and the L lanes of the
 // sub-warp reduce it with a fixed xor butterfly (deterministic; within the
 // north_star bound of the fp64 oracle O6).  BST: B tile and CSR slice staged.
-// Used for latency-bound batches only: streaming batches keep too few grad_C
-// bytes in flight per SM this way (ld.global through the L1 left beside a
-// 190 KB ring; C5 1650 us vs 1071 us for the standalone kernel).
+// Used for latency-bound batches only: on streaming batches the per-row
+// grad_C loads leave too few bytes in flight per SM (C5 1200 us vs 1071 us
+// for the standalone kernel; a two-row register double buffer measured
+// slower, 1525 us, no-allocate loads changed nothing, and warp-uniform loops
+// with full-mask shuffles for sub-warp rows were slower on every config).
 template <int CH, bool BST>
 __device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h, const unsigned char* st, int first,
                                            int step, int li, int sub) {
@@ -828,6 +830,16 @@ __device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h
   auto bload = [&](int32_t c, int v) -> float4 {
     const float* b = Bt + (int64_t)c * bstride + 4 * v * L;
     return BST ? *reinterpret_cast<const float4*>(b) : ldg_nc_f4(b);
+  };
+  // all lanes of a sub-warp reduce q over the sub-warp (fixed xor butterfly)
+  auto reduce = [&](float q) {
+    if (L == 32) {  // whole-warp rows: a constant mask, no convergence checks per shuffle (C4 9.5 -> 8.0 us)
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) q += __shfl_xor_sync(0xffffffffu, q, d);
+    } else {
+      for (int d = L >> 1; d > 0; d >>= 1) q += __shfl_xor_sync(mask, q, d);
+    }
+    return q;
   };
   auto dot = [&](const float4* g, const float4* b) {
     float q = 0.f;
@@ -867,11 +879,7 @@ __device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h
         b0[v] = ok[v] ? bload(c0, v) : make_float4(0.f, 0.f, 0.f, 0.f);
         b1[v] = ok[v] ? bload(c1, v) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      float q0 = dot(gv, b0), q1 = dot(gv, b1);
-      for (int d = L >> 1; d > 0; d >>= 1) {
-        q0 += __shfl_xor_sync(mask, q0, d);
-        q1 += __shfl_xor_sync(mask, q1, d);
-      }
+      const float q0 = reduce(dot(gv, b0)), q1 = reduce(dot(gv, b1));
       if (li == 0) {
         p.sd_out[e] = q0;
         p.sd_out[e + 1] = q1;
@@ -882,8 +890,7 @@ __device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h
       float4 b0[CH];
 #pragma unroll
       for (int v = 0; v < CH; ++v) b0[v] = ok[v] ? bload(c0, v) : make_float4(0.f, 0.f, 0.f, 0.f);
-      float q0 = dot(gv, b0);
-      for (int d = L >> 1; d > 0; d >>= 1) q0 += __shfl_xor_sync(mask, q0, d);
+      const float q0 = reduce(dot(gv, b0));
       if (li == 0) p.sd_out[e] = q0;
     }
   }
