@@ -1,3 +1,4 @@
+"""Time bspmm_sddmm per config: default dispatch, the SpMM-pipeline SDDMM mode forced (debug 1024), the standalone kernel (debug 256)."""
 import json, os, sys
 import torch
 sys.path.insert(0, os.getcwd())
