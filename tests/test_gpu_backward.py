@@ -147,12 +147,16 @@ def test_sddmm_mode_ld_and_direct_units(h, k, ld):
         h.set_hints(0, 0)
 
 
-def test_sddmm_streaming_batch(h):
-    """A batch above 8 matrices per SM takes the standalone kernel: C5's first
-    4096 graphs, bound-checked."""
+@pytest.mark.parametrize("dbg", [0, 1024])
+def test_sddmm_streaming_batch(h, dbg):
+    """A batch above 8 matrices per SM takes the standalone kernel (debug bit
+    1024: the SpMM pipeline's SDDMM mode instead): C5's first 4096 graphs,
+    bound-checked."""
     b = synth.config(5, i0=0, i1=4096)
     h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    h.set_debug(dbg)
     try:
         _sddmm_check(h, b, grad(b, 5))
     finally:
+        h.set_debug(0)
         h.set_hints(0, 0)
