@@ -841,6 +841,21 @@ __device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h
     }
     return q;
   };
+  // two reductions interleaved (independent shuffle chains)
+  auto reduce2 = [&](float& q0, float& q1) {
+    if (L == 32) {
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        q0 += __shfl_xor_sync(0xffffffffu, q0, d);
+        q1 += __shfl_xor_sync(0xffffffffu, q1, d);
+      }
+    } else {
+      for (int d = L >> 1; d > 0; d >>= 1) {
+        q0 += __shfl_xor_sync(mask, q0, d);
+        q1 += __shfl_xor_sync(mask, q1, d);
+      }
+    }
+  };
   auto dot = [&](const float4* g, const float4* b) {
     float q = 0.f;
 #pragma unroll
@@ -879,7 +894,8 @@ __device__ __forceinline__ void rows_sddmm(const SpmmParams& p, const UnitHdr& h
         b0[v] = ok[v] ? bload(c0, v) : make_float4(0.f, 0.f, 0.f, 0.f);
         b1[v] = ok[v] ? bload(c1, v) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      const float q0 = reduce(dot(gv, b0)), q1 = reduce(dot(gv, b1));
+      float q0 = dot(gv, b0), q1 = dot(gv, b1);
+      reduce2(q0, q1);
       if (li == 0) {
         p.sd_out[e] = q0;
         p.sd_out[e + 1] = q1;
