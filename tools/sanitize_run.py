@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): C1-C3 through every entry point (offsets, CSR, COO,
-COO->CSR, transpose, backward, host path), plus a padded layout and the
-direct (unstaged) path.  C is pre-filled with NaN-free garbage only where the
+COO->CSR, transpose, backward incl. a streaming batch, host path), plus a
+padded layout and the direct (unstaged) path.  C is pre-filled with NaN-free garbage only where the
 kernel must write it, so initcheck sees every read of C-derived data.
 
   compute-sanitizer --tool memcheck python tools/sanitize_run.py
@@ -52,6 +52,12 @@ def main():
     h.gcn_layer(T(b.row_off), None, rps, T(b.col), T(b.vals), X, W, bias)
     torch.cuda.synchronize()
     del C4
+    # backward of a streaming batch (standalone SDDMM kernel: > 8 matrices per SM)
+    b = synth.config(5, i0=0, i1=1500)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    G = torch.randn((b.n_rows, b.k), device=dev)
+    h.csr_backward(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), G)
+    torch.cuda.synchronize()
     # direct path (tiny stage capacity) and scalar path (k % 4 != 0)
     if len(sys.argv) > 1:  # the TMA-only variant: C1-C3 vectorised paths only
         h.sync()
