@@ -1017,7 +1017,7 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
   consumer_bar(T);
 }
 
-template <int CH, bool VEC, int EPI, bool COO>
+template <int CH, bool VEC, int EPI, bool COO, bool ONE>
 __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps, unsigned char* smem) {
   const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -1034,7 +1034,36 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
   if (VEC && !COO && cw == 0 && !p.sched && !(p.dbg & (2 | 4)))
     early_b_issue(p.row_off, p.sizes, p.B, p.ldb, p.tiles, p.kt, p.k, p.stage_b, p.trace,
                   early_bar(p, const_cast<unsigned char*>(smem)), const_cast<unsigned char*>(ring));
-  for (int j = 0;; ++j) {
+  int j0 = 0;
+  if (ONE) {
+    // one whole-row unit per CTA whose rows the consumer warps cover in one
+    // round (small latency-bound batches, e.g. C2): the consumers do not wait
+    // for the producer's header and CSR slice -- every warp loads the unit's
+    // row range itself, waits only for the early B tile and reads its rows'
+    // structure from global memory (those loads overlap the B landing; the
+    // producer's slice path is the critical path otherwise, trace).  The
+    // producer still stages unit 0 as usual: its copies are waited for
+    // (full[0], phase 0) BEFORE arriving on empty[0] -- the producer cannot
+    // advance full[0] past phase 0 until every warp has arrived.
+    const int64_t i = blockIdx.x;
+    const int32_t ni = p.sizes ? __ldg(p.sizes + i) : 0;
+    const int64_t g0 = p.row_off ? p.row_off[i] : warp_sizes_sum(p.sizes, i, lane);
+    const int32_t n = p.sizes ? ni : (int32_t)(p.row_off[i + 1] - g0);
+    const int32_t kw = min(p.kt, p.k);  // as the producer and early_b_issue compute it
+    if (n <= step && early_b_ok<VEC, COO>(p, n, kw)) {
+      UnitHdr h;
+      h.g0 = g0; h.n = n; h.nz0 = 0; h.nnz = 0; h.c0 = 0; h.kw = kw; h.flags = 1;
+      mbar_wait(early_bar(p, const_cast<unsigned char*>(smem)), 0u);
+      if (cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
+      rows<CH, VEC, true, false, EPI>(p, h, ring, first, step, li);
+      mbar_wait(&full[0], 0u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[0]);
+      if (cw == 0 && lane == 0) BSPMM_TRACE(p, 8);
+      j0 = 1;
+    }
+  }
+  for (int j = j0;; ++j) {
     const int s = j % p.stages;
     mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
@@ -1066,7 +1095,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
   if (cw == 0 && lane == 0) BSPMM_TRACE(p, 6);
 }
 
-template <int CH, bool VEC, int EPI, bool COO>
+template <int CH, bool VEC, int EPI, bool COO, bool ONE = false>
 __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
@@ -1088,16 +1117,16 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
   pdl_launch_dependents();
   if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
   if ((threadIdx.x >> 5) == 0) produce<VEC, COO>(p, maps, smem);
-  else consume<CH, VEC, EPI, COO>(p, maps, smem);
+  else consume<CH, VEC, EPI, COO, ONE>(p, maps, smem);
   if (p.trace) {
     __syncthreads();
     if (threadIdx.x == 0) BSPMM_TRACE(p, 7);
   }
 }
 
-template <int CH, bool VEC, int EPI, bool COO = false>
+template <int CH, bool VEC, int EPI, bool COO = false, bool ONE = false>
 static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bspmm_plan_t& plan, cudaStream_t s) {
-  auto kern = spmm_csr_kernel<CH, VEC, EPI, COO>;
+  auto kern = spmm_csr_kernel<CH, VEC, EPI, COO, ONE>;
   static thread_local int configured_bytes[64] = {};  // per device
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1133,6 +1162,13 @@ static cudaError_t launch_e(int epi, const SpmmParams& sp, const TmaMaps& maps, 
   }
   if constexpr (VEC) {
     if (epi == 3) return launch_t<CH, VEC, 3>(sp, maps, plan, s);
+    // one whole-row unit per CTA, rows covered in one consumer round (decided
+    // per CTA on the device): the consumers start without the producer's
+    // header and slice (an instantiation of its own; plain epilogue only)
+    const int32_t rows_per_round = ((plan.threads >> 5) - 1) * (32 / plan.lanes);
+    if (epi == 0 && plan.units <= plan.grid && plan.tiles == 1 && !sp.sched && plan.max_rows <= rows_per_round &&
+        !(sp.dbg & (2 | 4 | 1024)))
+      return launch_t<CH, VEC, 0, false, true>(sp, maps, plan, s);
   }
   if (epi == 2) return launch_t<CH, VEC, 2>(sp, maps, plan, s);
   if (epi == 1) return launch_t<CH, VEC, 1>(sp, maps, plan, s);

@@ -476,3 +476,37 @@ def test_cusparse_cross_check(h, cid):
     assert oracle.check_bound(Cs, Cref, bound)[0]
     C = run_csr(h, b)
     assert np.all(np.abs(C.astype(np.float64) - Cs) <= 2 * bound + 1e-30)
+
+
+@pytest.mark.parametrize("k,nlo,nhi,batch", [(64, 20, 60, 100), (32, 1, 64, 120), (16, 0, 30, 148),
+                                             (128, 10, 60, 90), (256, 5, 30, 40)])
+def test_one_unit_consumer_path(h, k, nlo, nhi, batch):
+    """One whole-row unit per CTA with all rows covered in one consumer round
+    (C2-like): the consumers load their row range and row structure themselves
+    and wait only for the early B tile.  Mixed sizes (incl. matrices above the
+    hinted rows, which fall back per CTA), empty matrices, sizes / fused
+    offsets; bitwise O3' and bitwise equal with the path off (debug bit 1024)."""
+    rng = np.random.default_rng(k + batch)
+    b = synth.random_batch(rng, batch, k, nmax=nhi, dmax=5, duplicates=True)
+    ref = None
+    for dbg in (0, 1024):
+        h.set_debug(dbg)
+        try:
+            for sizes in (False, True):
+                C = run_csr(h, b, sizes=sizes)
+                assert_parity(b, C, f"k={k} dbg={dbg} sizes={sizes}")
+                if ref is None:
+                    ref = C
+                assert np.array_equal(C.view(np.uint32), ref.view(np.uint32))
+            Cd = torch.full((b.n_rows, k), float("nan"), device=DEV)
+            h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cd)
+            torch.cuda.synchronize()
+            assert np.array_equal(Cd.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+            h.set_hints(max(1, nhi // 2), 0)  # many matrices above the hint: per-CTA fallback
+            Cd = torch.full((b.n_rows, k), float("nan"), device=DEV)
+            h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cd)
+            torch.cuda.synchronize()
+            assert np.array_equal(Cd.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+        finally:
+            h.set_debug(0)
+            h.set_hints(0, 0)
