@@ -155,12 +155,12 @@ def test_multimem_store_sass():
     sass = subprocess.run([exe, "-sass", bs.LIB_PATH], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s*Function : ", sass)
 
-    def stores(prefix):  # 128-bit global stores of the CSR-mode kernel <CH=2, VEC, EPI=...>
+    def stores(prefix):  # 128-bit global stores of the CSR-mode kernel <CH=2, VEC, EPI=..., COO=0, ONE=0>
         body = [f for f in funcs if f.startswith(prefix)]
         assert len(body) == 1, (prefix, len(body))
         return set(re.findall(r"\bSTG\.E[.A-Z0-9]*\.128\b", body[0]))
 
-    mc = stores("_ZN5bspmm15spmm_csr_kernelILi2ELb1ELi2ELb0E")
-    plain = stores("_ZN5bspmm15spmm_csr_kernelILi2ELb1ELi0ELb0E")
+    mc = stores("_ZN5bspmm15spmm_csr_kernelILi2ELb1ELi2ELb0ELb0EE")
+    plain = stores("_ZN5bspmm15spmm_csr_kernelILi2ELb1ELi0ELb0ELb0EE")
     assert mc == {"STG.E.128"}, mc
     assert plain == {"STG.E.EF.128"}, plain
