@@ -1164,11 +1164,13 @@ static cudaError_t launch_e(int epi, const SpmmParams& sp, const TmaMaps& maps, 
     if (epi == 3) return launch_t<CH, VEC, 3>(sp, maps, plan, s);
     // one whole-row unit per CTA, rows covered in one consumer round (decided
     // per CTA on the device): the consumers start without the producer's
-    // header and slice (an instantiation of its own; plain epilogue only)
+    // header and slice (an instantiation of its own; plain and GCN epilogues)
     const int32_t rows_per_round = ((plan.threads >> 5) - 1) * (32 / plan.lanes);
-    if (epi == 0 && plan.units <= plan.grid && plan.tiles == 1 && !sp.sched && plan.max_rows <= rows_per_round &&
-        !(sp.dbg & (2 | 4 | 1024)))
+    if (epi <= 1 && plan.units <= plan.grid && plan.tiles == 1 && !sp.sched && plan.max_rows <= rows_per_round &&
+        !(sp.dbg & (2 | 4 | 1024))) {
+      if (epi == 1) return launch_t<CH, VEC, 1, false, true>(sp, maps, plan, s);
       return launch_t<CH, VEC, 0, false, true>(sp, maps, plan, s);
+    }
   }
   if (epi == 2) return launch_t<CH, VEC, 2>(sp, maps, plan, s);
   if (epi == 1) return launch_t<CH, VEC, 1>(sp, maps, plan, s);

@@ -45,8 +45,13 @@ def main():
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     h = bs.Handle(0)
     rng = np.random.default_rng(0)
-    for name, batch, width, channels in (("tox21_like", 100, 64, 4), ("reaction100_like", 100, 512, 4),
-                                         ("reaction100_like_b65536", 65536, 512, 4)):
+    # optional: --dbg BITS (bspmm_set_debug), --small (the two 100-graph shapes only)
+    if "--dbg" in sys.argv:
+        h.set_debug(int(sys.argv[sys.argv.index("--dbg") + 1]))
+    shapes = [("tox21_like", 100, 64, 4), ("reaction100_like", 100, 512, 4), ("reaction100_like_b65536", 65536, 512, 4)]
+    if "--small" in sys.argv:
+        shapes = shapes[:2]
+    for name, batch, width, channels in shapes:
         b = synth.generate(synth.MOL, (20, 60, 0, 0), batch, width, seed=1903114090 + batch, dense=False)
         rps, col, vals = channels_of(b, channels, rng)
         X = T(rng.standard_normal((b.n_rows, width)).astype(np.float32))
