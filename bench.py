@@ -397,6 +397,8 @@ def main():
             "gpu_launches": int(launches), "clocks": clk.summary(),
         }
         print(json.dumps(out), flush=True)
+    bdist.barrier(dev)
+    bdist.finalize()
 
 
 if __name__ == "__main__":

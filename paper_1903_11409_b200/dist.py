@@ -34,6 +34,12 @@ def init(backend: str = "nccl", device: torch.device | None = None) -> Tuple[int
     return rank, world
 
 
+def finalize() -> None:
+    """Tear down the process group (multi-rank runs) before exit."""
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
+
+
 def shard_of(nnz_off: np.ndarray, k: int, rank: int, world: int) -> Tuple[int, int]:
     """Contiguous graph range [i0, i1) of `rank` (identical on every rank: integer rule)."""
     split = partition(nnz_off, k, world)
