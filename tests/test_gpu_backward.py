@@ -160,3 +160,34 @@ def test_sddmm_streaming_batch(h, dbg):
     finally:
         h.set_debug(0)
         h.set_hints(0, 0)
+
+
+def test_backward_c5_full_size_window(h):
+    """The backward at BASELINE.json's full C5 size (65536 graphs, k = 256; the
+    streaming paths: warp-per-matrix transpose, grad_B SpMM, standalone SDDMM),
+    checked on a contiguous window of 1500 graphs regenerated alone: grad_B
+    rows bitwise equal to O3' over the oracle's A^T, grad_vals within the bound
+    of O6; and no NaN left anywhere (every row / entry written)."""
+    b = synth.config(5)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    rng = np.random.default_rng(5150)
+    G = (rng.integers(-(1 << 23), 1 << 23, size=(b.n_rows, b.k), dtype=np.int64) / float(1 << 23)).astype(np.float32)
+    try:
+        gB, gv = h.csr_backward(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), T(G))
+        torch.cuda.synchronize()
+    finally:
+        h.set_hints(0, 0)
+    gB, gv = gB.cpu().numpy(), gv.cpu().numpy()
+    assert not np.isnan(gB).any() and not np.isnan(gv).any()
+    i0, i1 = 31000, 32500
+    w = synth.config(5, i0=i0, i1=i1)                  # the window, laid out from row 0
+    r0, r1 = int(b.row_off[i0]), int(b.row_off[i1])
+    z0, z1 = int(b.nnz_off[i0]), int(b.nnz_off[i1])
+    Gw = G[r0:r1]
+    assert np.array_equal(w.B, b.B[r0:r1]) and np.array_equal(w.col, b.col[z0:z1])
+    ort, oct_, ovt = oracle.csr_transpose(w.row_off, None, w.row_ptr, w.col, w.vals)
+    ref32 = oracle.spmm_f32(w.k, w.row_off, None, ort, oct_, ovt, Gw)
+    assert np.array_equal(gB[r0:r1].view(np.uint32), ref32.view(np.uint32))
+    rv, bv = oracle.sddmm(w.k, w.row_off, None, w.row_ptr, w.col, w.B, Gw)
+    ok, worst = oracle.check_bound(gv[z0:z1], rv, bv)
+    assert ok, worst
