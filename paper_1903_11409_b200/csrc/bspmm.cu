@@ -199,6 +199,15 @@ BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* str
   }
   cudaMemset(h->dev_flag, 0, sizeof(int));
   cudaMemset(h->dev_sched, 0, sizeof(unsigned long long));
+  // the backward's auxiliary stream and fork/join events, created here so that
+  // a backward call may be captured into a CUDA graph on its first use
+  if (cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    bspmm_destroy(h);
+    return BSPMM_ERROR_CUDA;
+  }
   *out = h;
   return BSPMM_SUCCESS;
 }
@@ -211,6 +220,9 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (cudaStreamSynchronize(h->stream) != cudaSuccess) st = BSPMM_ERROR_CUDA;
     if (h->s_h2d) cudaStreamSynchronize(h->s_h2d), cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamSynchronize(h->s_d2h), cudaStreamDestroy(h->s_d2h);
+    if (h->s_aux) cudaStreamSynchronize(h->s_aux), cudaStreamDestroy(h->s_aux);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     for (auto& e : h->ev)
       if (e) cudaEventDestroy(e);
     if (h->ws) cudaFree(h->ws);
@@ -256,7 +268,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 2047) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 4095) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -645,7 +657,8 @@ static bspmm_status_t trans_workspace(bspmm_handle_t h, int64_t N, int64_t NNZ, 
 
 static bspmm_status_t transpose_impl(bspmm_handle_t h, int32_t batch, const int64_t* row_off, const int32_t* sizes,
                                      const int32_t* row_ptr, const int32_t* col, const float* vals, int32_t* rowT,
-                                     int32_t* colT, float* valsT) {
+                                     int32_t* colT, float* valsT, cudaStream_t stream = nullptr) {
+  if (!stream) stream = h->stream;
   if (h->flags & BSPMM_VALIDATE) {
     CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
     CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr, col, h->dev_flag, h->stream));
@@ -653,8 +666,8 @@ static bspmm_status_t transpose_impl(bspmm_handle_t h, int32_t batch, const int6
     bspmm_status_t st = check_validate_flag(h);
     if (st != BSPMM_SUCCESS) return st;
   }
-  CK(h, launch_transpose_csr(batch, row_off, sizes, row_ptr, col, vals, rowT, colT, valsT, h->hint_rows, h->hint_nnz, h->num_sms,
-                             h->stream));
+  CK(h, launch_transpose_csr(batch, row_off, sizes, row_ptr, col, vals, rowT, colT, valsT, h->hint_rows, h->hint_nnz,
+                             h->num_sms, stream));
   h->launches++;
   return BSPMM_SUCCESS;
 }
@@ -732,6 +745,23 @@ BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int
   if (batch == 0 || (!grad_B && !grad_vals)) return BSPMM_SUCCESS;
   if (!row_off || !row_ptr) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
   DeviceGuard g(h->device);
+  if (grad_B && grad_vals && !(h->flags & BSPMM_VALIDATE) && !(h->dbg & 2048)) {
+    // both adjoints: the transpose (latency-bound) runs on an auxiliary stream
+    // concurrently with the SDDMM, then grad_B = A^T grad_C once it has joined
+    // (fork / join by events: also valid inside a CUDA-graph capture)
+    TransWs w;
+    bspmm_status_t st = trans_workspace(h, total_rows, total_nnz, &w);
+    if (st != BSPMM_SUCCESS) return st;
+    CK(h, cudaEventRecord(h->ev_fork, h->stream));
+    CK(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
+    st = transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, w.rowT, w.colT, w.valsT, h->s_aux);
+    if (st != BSPMM_SUCCESS) return st;
+    CK(h, cudaEventRecord(h->ev_join, h->s_aux));
+    st = bspmm_sddmm(h, batch, k, row_off, sizes, row_ptr, col, B, ldb, grad_C, ldgc, grad_vals);
+    CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));  // joined even if the SDDMM call failed
+    if (st != BSPMM_SUCCESS) return st;
+    return csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
+  }
   if (grad_vals) {  // dL/dval_e = <grad_C[row_e], B[col_e]>
     bspmm_status_t st = bspmm_sddmm(h, batch, k, row_off, sizes, row_ptr, col, B, ldb, grad_C, ldgc, grad_vals);
     if (st != BSPMM_SUCCESS) return st;

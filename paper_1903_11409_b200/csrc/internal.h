@@ -149,5 +149,9 @@ struct bspmm_handle_s {
   void* hbuf = nullptr;
   size_t hbuf_bytes = 0;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  // backward: the transpose runs on s_aux concurrently with the SDDMM (forked
+  // from and joined back into `stream` within the call)
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev[64] = {};
 };
