@@ -146,9 +146,10 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * pipeline's SDDMM mode; 512 = standalone SDDMM without the L2 prefetch of
  * the next matrix's B_i; 1024 = the SDDMM mode also for streaming batches,
  * and no one-unit consumer fast path in the SpMM (consumers wait for the
- * producer's header and CSR slice); 2048 = backward with the transpose on
- * the caller's stream after the SDDMM (no auxiliary stream).  0 (default) =
- * normal. */
+ * producer's header and CSR slice); 2048 = backward entirely on the
+ * caller's stream (no auxiliary stream); 4096 = backward with only the
+ * transpose on the auxiliary stream (grad_B SpMM on the caller's stream).
+ * 0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */

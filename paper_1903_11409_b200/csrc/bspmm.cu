@@ -268,7 +268,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 4095) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 8191) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -756,11 +756,20 @@ BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int
     CK(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
     st = transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, w.rowT, w.colT, w.valsT, h->s_aux);
     if (st != BSPMM_SUCCESS) return st;
+    if (!(h->dbg & 4096)) {  // grad_B = A^T grad_C on the auxiliary stream too, after the transpose
+      cudaStream_t main = h->stream;
+      h->stream = h->s_aux;
+      st = csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
+      h->stream = main;
+      if (st != BSPMM_SUCCESS) return st;
+    }
     CK(h, cudaEventRecord(h->ev_join, h->s_aux));
     st = bspmm_sddmm(h, batch, k, row_off, sizes, row_ptr, col, B, ldb, grad_C, ldgc, grad_vals);
     CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));  // joined even if the SDDMM call failed
     if (st != BSPMM_SUCCESS) return st;
-    return csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
+    if (h->dbg & 4096)
+      return csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
+    return BSPMM_SUCCESS;
   }
   if (grad_vals) {  // dL/dval_e = <grad_C[row_e], B[col_e]>
     bspmm_status_t st = bspmm_sddmm(h, batch, k, row_off, sizes, row_ptr, col, B, ldb, grad_C, ldgc, grad_vals);
