@@ -148,8 +148,9 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * and no one-unit consumer fast path in the SpMM (consumers wait for the
  * producer's header and CSR slice); 2048 = backward entirely on the
  * caller's stream (no auxiliary stream); 4096 = backward with only the
- * transpose on the auxiliary stream (grad_B SpMM on the caller's stream).
- * 0 (default) = normal. */
+ * transpose on the auxiliary stream (grad_B SpMM on the caller's stream);
+ * 8192 = GCN layer with one batched GEMM before the channel SpMMs instead
+ * of channel GEMMs pipelined on the auxiliary stream.  0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */

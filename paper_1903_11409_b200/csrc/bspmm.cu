@@ -208,6 +208,13 @@ BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* str
     bspmm_destroy(h);
     return BSPMM_ERROR_CUDA;
   }
+  bool ev_ok = true;
+  for (auto& e : h->ev_ch) ev_ok = ev_ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  if (!ev_ok) {
+    cudaGetLastError();
+    bspmm_destroy(h);
+    return BSPMM_ERROR_CUDA;
+  }
   *out = h;
   return BSPMM_SUCCESS;
 }
@@ -223,6 +230,8 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (h->s_aux) cudaStreamSynchronize(h->s_aux), cudaStreamDestroy(h->s_aux);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
+    for (auto& e : h->ev_ch)
+      if (e) cudaEventDestroy(e);
     for (auto& e : h->ev)
       if (e) cudaEventDestroy(e);
     if (h->ws) cudaFree(h->ws);
@@ -268,7 +277,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 8191) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 16383) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -578,6 +587,42 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
   const cublasComputeType_t ct = h->gcn_math == BSPMM_GCN_TF32   ? CUBLAS_COMPUTE_32F_FAST_TF32
                                  : h->gcn_math == BSPMM_GCN_BF16 ? CUBLAS_COMPUTE_32F_FAST_16BF
                                                                  : CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
+  if (channels > 1 && channels <= bspmm_handle_s::kGcnEvents && !(h->flags & BSPMM_VALIDATE) && !(h->dbg & 8192)) {
+    // channel-pipelined: GEMM_ch on the auxiliary stream, SpMM_ch (which
+    // accumulates into Y, so the SpMMs stay in channel order) on the caller's
+    // stream after GEMM_ch -- GEMM_{ch+1} overlaps SpMM_ch
+    CK(h, cudaEventRecord(h->ev_fork, h->stream));
+    CK(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
+    cublasSetStream(cb, h->s_aux);
+    for (int32_t ch = 0; ch < channels; ++ch) {
+      float* Uc = U + (int64_t)ch * k;
+      const float* Wc = W + (int64_t)ch * n_x * k;
+      cublasStatus_t cs = cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, Wc, CUDA_R_32F, k, X,
+                                       CUDA_R_32F, (int)ldx, &zero, Uc, CUDA_R_32F, (int)ldu, ct, CUBLAS_GEMM_DEFAULT);
+      if (cs != CUBLAS_STATUS_SUCCESS && h->gcn_math == BSPMM_GCN_FP32)
+        cs = cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, Wc, CUDA_R_32F, k, X, CUDA_R_32F,
+                          (int)ldx, &zero, Uc, CUDA_R_32F, (int)ldu, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+      CK(h, cudaEventRecord(h->ev_ch[ch], h->s_aux));
+      if (cs != CUBLAS_STATUS_SUCCESS) {
+        cublasSetStream(cb, h->stream);
+        CK(h, cudaStreamWaitEvent(h->stream, h->ev_ch[ch], 0));
+        return fail(h, h->gcn_math != BSPMM_GCN_FP32 ? BSPMM_ERROR_NOT_SUPPORTED : BSPMM_ERROR_CUDA,
+                    "cuBLAS GEMM failed");
+      }
+      h->launches++;
+    }
+    cublasSetStream(cb, h->stream);
+    for (int32_t ch = 0; ch < channels; ++ch) {
+      CK(h, cudaStreamWaitEvent(h->stream, h->ev_ch[ch], 0));
+      st = csr_impl(h, batch, k, row_off, sizes, row_ptr + (int64_t)ch * (N + 1), col, vals, U + (int64_t)ch * k, ldu,
+                    Y, ldy, false, bias ? bias + (int64_t)ch * k : nullptr, ch > 0 ? 1 : 0);
+      if (st != BSPMM_SUCCESS) {  // join the auxiliary stream before returning
+        CK(h, cudaStreamWaitEvent(h->stream, h->ev_ch[channels - 1], 0));
+        return st;
+      }
+    }
+    return BSPMM_SUCCESS;
+  }
   cublasStatus_t cs = cublasGemmStridedBatchedEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, W, CUDA_R_32F, k,
                                                  (long long)n_x * k, X, CUDA_R_32F, (int)ldx, 0, &zero, U, CUDA_R_32F,
                                                  (int)ldu, k, channels, ct, CUBLAS_GEMM_DEFAULT);

@@ -153,5 +153,9 @@ struct bspmm_handle_s {
   // from and joined back into `stream` within the call)
   cudaStream_t s_aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // GCN layer: per-channel GEMM done-events (channel GEMMs on s_aux overlap
+  // the previous channel's SpMM on `stream`)
+  static constexpr int kGcnEvents = 16;
+  cudaEvent_t ev_ch[kGcnEvents] = {};
   cudaEvent_t ev[64] = {};
 };
