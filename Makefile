@@ -11,11 +11,11 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
              -ftz=false -prec-div=true -prec-sqrt=true -Iinclude -Xptxas -v
 LIB       := $(PKG)/libbspmm.so
-CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu $(CSRC)/backward.cu $(CSRC)/spmm_coo_atomic.cu
+CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu $(CSRC)/backward.cu $(CSRC)/spmm_coo_atomic.cu $(CSRC)/spmm_tile.cu
 HOST_SRCS := $(CSRC)/partition.cpp $(CSRC)/plan.cpp $(CSRC)/multicast.cpp
 HDRS      := include/bspmm.h $(CSRC)/internal.h $(CSRC)/ptx.cuh
 
-all: lib oracle synth
+all: lib oracle synth probes
 
 lib: $(LIB)
 
@@ -33,8 +33,13 @@ synth: synth/libsynth.so
 synth/libsynth.so: synth/synth.c
 	$(CC) -O2 -std=c11 -fPIC -shared -fopenmp -o $@ $<
 
+# measurement probes (not product code): the copy floor of tools/kbench.py --copy-baseline
+probes: tools/probe/libfloor.so
+tools/probe/libfloor.so: tools/probe/floor.cu
+	$(NVCC) $(ARCH) -O3 -lineinfo -shared -Xcompiler -fPIC -o $@ $<
+
 clean:
 	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so
 	rm -rf build
 
-.PHONY: all lib oracle synth clean
+.PHONY: all lib oracle synth probes clean

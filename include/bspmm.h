@@ -99,6 +99,8 @@ typedef struct {
   int32_t max_rows;       /* planning assumption for max n_i (hint or default)                  */
   int32_t sched;          /* 0: static round-robin units; 1: dynamic (global ticket counter)    */
   int64_t units;          /* batch * tiles                                                      */
+  int32_t kernel;         /* 0: persistent TMA-ring pipeline; 1: small-batch tile kernel (one   *
+                           * CTA per (matrix, column block); kt = 4 * block, lanes = block)     */
 } bspmm_plan_t;
 
 /* ---- lifetime -------------------------------------------------------- */
@@ -120,38 +122,6 @@ BSPMM_API bspmm_status_t bspmm_set_stream(bspmm_handle_t h, void* stream);
  * the plan's stage capacity still run correctly, reading B from global memory
  * directly (the paper's "case 3"). */
 BSPMM_API bspmm_status_t bspmm_set_hints(bspmm_handle_t h, int32_t max_rows, int64_t max_nnz);
-
-/* Tuning override for experiments: kt (multiple of 4 on the vec path, 0 =
- * auto), consumer warps per CTA (0 = auto, <= 16; 15 with 4 chunks), CTAs per SM (0 = auto,
- * <= 4), column chunks per lane (0 = auto, <= 4). */
-BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t consumer_warps,
-                                          int32_t ctas_per_sm, int32_t chunks);
-
-/* Debug: per-CTA phase timestamps (%globaltimer, ns) of subsequent SpMM
- * launches are written to dev_buf [grid x 32] uint64 (slots: entry, after the
- * programmatic-launch wait, producer has unit-0 offsets, producer has unit-0
- * structure, producer done, first consumer warp sees unit 0, first consumer
- * warp done, CTA exit, first consumer warp done with unit 0; 9-15 and 16-27
- * producer issue steps of the first units, see spmm_csr.cu).  NULL disables
- * (the default). */
-BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
-
-/* Debug: timing-experiment bits for subsequent SpMM launches.  1 = compute but
- * do not store C (the result is then undefined); 2 = compute every unit from
- * global memory (no staging); 4 = no early B tile for the first unit of a
- * CTA; 8 = consumers repeat each unit's work 4 times;
- * 16 = (unused; was an L2 prefetch of small problems, no gain); 32 = always copy
- * the CSR slice with TMA; 64 = force the static unit schedule; 128 = force the
- * dynamic one; 256 = SDDMM by the standalone kernel instead of the SpMM
- * pipeline's SDDMM mode; 512 = standalone SDDMM without the L2 prefetch of
- * the next matrix's B_i; 1024 = the SDDMM mode also for streaming batches,
- * and no one-unit consumer fast path in the SpMM (consumers wait for the
- * producer's header and CSR slice); 2048 = backward entirely on the
- * caller's stream (no auxiliary stream); 4096 = backward with only the
- * transpose on the auxiliary stream (grad_B SpMM on the caller's stream);
- * 8192 = GCN layer with one batched GEMM before the channel SpMMs instead
- * of channel GEMMs pipelined on the auxiliary stream.  0 (default) = normal. */
-BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Waits for all work enqueued by this handle; surfaces asynchronous errors. */
 BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h);

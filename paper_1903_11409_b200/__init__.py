@@ -186,6 +186,10 @@ class Handle:
             _check(buf, "trace", torch.int64, self.device)
         self._raise(lib.bspmm_set_trace(self._h, _ptr(buf)), "bspmm_set_trace")
 
+    def set_tile_cb(self, cb: int):
+        """Experiment knob (bspmm_debug.h): float4 columns per tile of the small-batch kernel, 0 = planner."""
+        self._raise(lib.bspmm_set_tile_cb(self._h, int(cb)), "bspmm_set_tile_cb")
+
     def set_debug(self, bits: int):
         """Debug bits for timing experiments (1 = skip C stores; results undefined)."""
         self._raise(lib.bspmm_set_debug(self._h, int(bits)), "bspmm_set_debug")

@@ -9,6 +9,7 @@ import re
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbspmm.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bspmm.h")
+DEBUG_HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bspmm_debug.h")
 
 P, I32, I64, U32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
 
@@ -19,7 +20,7 @@ VALIDATE = 0x1
 class Plan(ctypes.Structure):
     _fields_ = [("kt", I32), ("tiles", I32), ("lanes", I32), ("vec", I32), ("chunks", I32), ("stages", I32),
                 ("stage_b_bytes", I32), ("stage_s_bytes", I32), ("smem_bytes", I32), ("threads", I32),
-                ("grid", I32), ("max_rows", I32), ("sched", I32), ("units", I64)]
+                ("grid", I32), ("max_rows", I32), ("sched", I32), ("units", I64), ("kernel", I32)]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -34,6 +35,7 @@ _SIGS = {
     "bspmm_sync": (I32, [P]),
     "bspmm_set_trace": (I32, [P, P]),
     "bspmm_set_debug": (I32, [P, I32]),
+    "bspmm_set_tile_cb": (I32, [P, I32]),
     "bspmm_set_gcn_math": (I32, [P, I32]),
     "bspmm_csr": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
     "bspmm_csr_multicast": (I32, [P, I32, I32, P, P, P, P, P, P, I64, P, I64]),
@@ -64,9 +66,12 @@ _SIGS = {
 }
 
 
-def header_symbols(path: str = HEADER_PATH) -> list[str]:
-    """Every function the C header declares (BSPMM_API ... name(...))."""
-    src = open(path).read()
+def header_symbols(paths=(HEADER_PATH, DEBUG_HEADER_PATH)) -> list[str]:
+    """Every function the C headers declare (BSPMM_API ... name(...)): the
+    contract (bspmm.h) and the experiment knobs (bspmm_debug.h)."""
+    if isinstance(paths, str):
+        paths = (paths,)
+    src = "".join(open(p).read() for p in paths)
     return sorted(set(re.findall(r"BSPMM_API\s+[\w\s\*]+?\b(bspmm_\w+)\s*\(", src)))
 
 

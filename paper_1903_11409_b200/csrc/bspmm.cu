@@ -270,6 +270,12 @@ BSPMM_API bspmm_status_t bspmm_set_tuning(bspmm_handle_t h, int32_t kt, int32_t 
   return BSPMM_SUCCESS;
 }
 
+BSPMM_API bspmm_status_t bspmm_set_tile_cb(bspmm_handle_t h, int32_t cb) {
+  if (!h || cb < 0 || cb > 32) return BSPMM_ERROR_INVALID_VALUE;
+  h->tune_tile_cb = cb;
+  return BSPMM_SUCCESS;
+}
+
 BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
   h->trace = reinterpret_cast<unsigned long long*>(dev_buf);
@@ -277,7 +283,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 16383) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 32767) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -355,6 +361,30 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   bspmm_plan_t plan;
   bspmm_status_t st = plan_for(h, batch, k, aligned, &plan);
   if (st != BSPMM_SUCCESS) return st;
+  // small batches (every tile resident at once): the tile kernel
+  // (spmm_tile.cu); tuning overrides and the debug bits of the pipeline kernel
+  // keep the pipeline
+  TileLayout L;
+  const bool tuned = h->tune_kt || h->tune_warps || h->tune_ctas || h->tune_chunks;
+  if (plan.vec && mc == 0 && !tuned && !(h->dbg & (2 | 4 | 8 | 128 | 16384)) &&
+      plan_tile(batch, k, h->hint_rows, h->hint_nnz, h->num_sms, h->tune_tile_cb, &L)) {
+    plan.kernel = 1;
+    plan.kt = 4 * L.cb;
+    plan.tiles = L.tiles;
+    plan.lanes = L.cb;
+    plan.chunks = 1;
+    plan.stages = 1;
+    plan.units = L.units;
+    plan.grid = (int32_t)L.units;
+    plan.threads = 128;
+    plan.smem_bytes = L.smem;
+    h->last_plan = plan;
+    CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, nullptr, bias,
+              accumulate};
+    CK(h, launch_spmm_tile(a, L, h->stream));
+    h->launches++;
+    return BSPMM_SUCCESS;
+  }
   const TmaMaps* maps = plan.vec ? tma_maps(h, B, k, ldb, plan.kt) : nullptr;
   if (h->dbg & 64) plan.sched = 0;
   if ((h->dbg & 128) && row_off) plan.sched = 1;

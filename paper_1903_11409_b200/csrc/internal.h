@@ -6,6 +6,7 @@
 #include <string>
 
 #include "bspmm.h"
+#include "bspmm_debug.h"
 
 #if defined(__CUDACC__)
 #define BSPMM_HD __host__ __device__
@@ -76,6 +77,15 @@ struct CsrArgs {
 
 // kernels (.cu)
 cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s);
+// small-batch tile kernel (spmm_tile.cu): one CTA per (matrix, float4 column block)
+struct TileLayout {
+  int32_t cb, tiles, per_sm, smem;
+  int32_t cap_rows, cap_nnz, rp_off, col_off, val_off;
+  int64_t units;
+};
+bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int32_t num_sms, int32_t cb_override,
+               TileLayout* out);
+cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t s);
 // decoupled look-back scan state (persistent per handle; epoch-tagged, never reset per call)
 struct ScanState {
   uint32_t* flags;                 // [tiles] (epoch << 2) | {1: aggregate, 2: inclusive}
@@ -120,6 +130,7 @@ struct bspmm_handle_s {
   int32_t hint_rows = 0;
   int64_t hint_nnz = 0;
   int32_t tune_kt = 0, tune_warps = 0, tune_ctas = 0, tune_chunks = 0;
+  int32_t tune_tile_cb = 0;  // bspmm_set_tile_cb: tile kernel column block (0 = planner)
   bspmm_plan_t last_plan{};
   unsigned long long* trace = nullptr;  // debug: per-CTA phase timestamps
   int32_t dbg = 0;                      // debug bits: 1 = skip C stores

@@ -1,0 +1,370 @@
+// spmm_tile.cu — the batched CSR SpMM for small batches (hot-path rows a-4,
+// a-5, a-6 for the latency-bound configs, BASELINE.json configs 1-4): one
+// short-lived CTA per TILE = (matrix i, block of cb float4 columns).
+//
+// What it computes is exactly spmm_csr.cu's operation (PAPER.md Fig.
+// algo:code_swa_spmm_csr, lines 196-207, batched as in §IV-C): for every
+// matrix i, row r < n_i and column c < k
+//     C[g][c] = sum_{e in row g} vals[e] * B[row_off[i] + col[e]][c],
+// g = row_off[i] + r, fp32 FMA in CSR storage order from +0 (bitwise O3').
+//
+// Why a second kernel.  A batch of 100 graphs is 100 units of work for 148
+// SMs; the persistent pipeline of spmm_csr.cu stages each B_i whole in one
+// CTA, so a third of the SMs idle and every CTA serialises landing (100 KB
+// per SM on config 4) and its row pass.  Here the paper's column cache
+// blocking (p column blocks per SpMM) is used
+// to cut the batch into MANY small independent tiles instead: B_i[:, block]
+// and C_i[:, block] depend on nothing else (a C column needs only the same B
+// column), so a tile is a complete little SpMM.  With cb chosen so that the
+// batch makes ~8-16 tiles per SM, every SM holds many CTAs at once and they
+// overlap: one tile's loads land while another computes and a third stores --
+// the same overlap a plain copy kernel gets, with no producer/consumer
+// barrier spanning a whole SM.
+//
+// Per CTA (128 threads, several per SM):
+//   RT1  the matrix's row offset and size (fused offsets: a block sum of the
+//        sizes before it when row_off == NULL);
+//   B    the tile B_i[:, c0 .. c0+cw) (n_i x cw float4) into shared memory by
+//        16-byte cp.async, issued at once;
+//   RT2  the matrix's row pointers (and its first/last entry), RT3 its (col,
+//        val) run -> shared memory, while B lands;
+//   row pass: thread (row slot, column) -- cb lanes per row, the paper's
+//        subWarp lanes on lane-strided columns in
+//        float4 chunks -- storage-order FMA over the row's entries, one
+//        128-bit streaming store per (row, chunk); empty rows store +0.
+// A matrix whose tile or structure does not fit the planned capacity reads
+// them from global memory instead (the paper's case 3),
+// decided per CTA: correct for any size, fast for the planned ones.
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace bspmm {
+
+constexpr int kTileThreads = 128;
+
+struct TileParams {
+  int32_t batch, k4, tiles;
+  int32_t cap_rows, cap_nnz;           // staging capacity: rows of a tile, entries of a matrix
+  int32_t rp_off, col_off, val_off;    // shared-memory carve-up (bytes) after the B tile
+  const int64_t* __restrict__ row_off;
+  const int32_t* __restrict__ sizes;
+  const int32_t* __restrict__ row_ptr;
+  const int32_t* __restrict__ col;
+  const float* __restrict__ vals;
+  const float4* __restrict__ B;
+  int64_t ldb4;
+  float4* __restrict__ C;
+  int64_t ldc4;
+  const float4* __restrict__ bias;  // GCN epilogue (EPI 1): C += rowsum(A) (x) bias
+  int32_t accumulate;               // GCN epilogue: C += previous C
+  unsigned long long* trace;        // debug: per-CTA phase timestamps (globaltimer ns), or null
+};
+
+__device__ __forceinline__ void tile_trace(const TileParams& p, int slot) {
+  if (p.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    p.trace[(size_t)blockIdx.x * 32 + slot] = t;
+  }
+}
+
+// sum of sizes[0 .. i) over the CTA (fused offsets builder, packed layout):
+// every load of a thread in flight before any add (one round trip)
+__device__ __forceinline__ int64_t tile_sizes_prefix(const int32_t* __restrict__ sizes, int32_t i) {
+  __shared__ int64_t part[kTileThreads / 32];
+  int64_t s = 0;
+  for (int32_t m0 = 0; m0 < i; m0 += 8 * kTileThreads) {
+    int32_t v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int32_t m = m0 + threadIdx.x + q * kTileThreads;
+      v[q] = m < i ? __ldg(sizes + m) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += v[q];
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  int64_t tot = 0;
+#pragma unroll
+  for (int w = 0; w < kTileThreads / 32; ++w) tot += part[w];
+  return tot;
+}
+
+__device__ __forceinline__ void fma4(float4& acc, float a, const float4& b) {
+  acc.x = fmaf(a, b.x, acc.x);
+  acc.y = fmaf(a, b.y, acc.y);
+  acc.z = fmaf(a, b.z, acc.z);
+  acc.w = fmaf(a, b.w, acc.w);
+}
+
+template <int EPI>
+__device__ __forceinline__ void tile_store(const TileParams& p, float4* dst, int32_t colf4, float4 acc, float rs) {
+  if (EPI == 1) {
+    if (p.bias) {
+      const float4 b = __ldg(p.bias + colf4);
+      acc.x = fmaf(rs, b.x, acc.x);
+      acc.y = fmaf(rs, b.y, acc.y);
+      acc.z = fmaf(rs, b.z, acc.z);
+      acc.w = fmaf(rs, b.w, acc.w);
+    }
+    if (p.accumulate) {
+      const float4 o = *dst;
+      acc.x += o.x;
+      acc.y += o.y;
+      acc.z += o.z;
+      acc.w += o.w;
+    }
+  }
+  stg_cs_f4(reinterpret_cast<float*>(dst), acc);
+}
+
+// The row pass.  SST: (col, val) and row pointers (relative to the matrix's
+// first entry) in shared memory; BST: the B tile in shared memory (row pitch
+// CB float4).  Entries two at a time: loads first, FMAs in storage order.
+template <int CB, int EPI, bool BST, bool SST>
+__device__ __forceinline__ void tile_rows(const TileParams& p, const float4* Bs, const int32_t* rp_s,
+                                          const int32_t* col_s, const float* val_s, int64_t g0, int32_t n,
+                                          int32_t c0, int32_t cw) {
+  const int c = threadIdx.x % CB;
+  if (c >= cw) return;
+  constexpr int RP = kTileThreads / CB;  // rows per pass
+  const float4* Bp = BST ? Bs + c : p.B + g0 * p.ldb4 + c0 + c;
+  const int64_t bstride = BST ? CB : p.ldb4;
+  float4* Cp = p.C + g0 * p.ldc4 + c0 + c;
+  for (int32_t r = threadIdx.x / CB; r < n; r += RP) {
+    int32_t e, e1;
+    if (SST) {
+      e = rp_s[r];
+      e1 = rp_s[r + 1];
+    } else {
+      e = __ldg(p.row_ptr + g0 + r);
+      e1 = __ldg(p.row_ptr + g0 + r + 1);
+    }
+    const int32_t* ci = SST ? col_s : p.col;
+    const float* cv = SST ? val_s : p.vals;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float rs = 0.f;
+    for (; e + 1 < e1; e += 2) {
+      const int32_t k0 = SST ? ci[e] : __ldg(ci + e), k1 = SST ? ci[e + 1] : __ldg(ci + e + 1);
+      const float a0 = SST ? cv[e] : __ldg(cv + e), a1 = SST ? cv[e + 1] : __ldg(cv + e + 1);
+      const float4 b0 = BST ? Bp[k0 * CB] : __ldg(Bp + k0 * bstride);
+      const float4 b1 = BST ? Bp[k1 * CB] : __ldg(Bp + k1 * bstride);
+      fma4(acc, a0, b0);
+      fma4(acc, a1, b1);
+      if (EPI == 1) rs += a0, rs += a1;
+    }
+    if (e < e1) {
+      const int32_t k0 = SST ? ci[e] : __ldg(ci + e);
+      const float a0 = SST ? cv[e] : __ldg(cv + e);
+      const float4 b0 = BST ? Bp[k0 * CB] : __ldg(Bp + k0 * bstride);
+      fma4(acc, a0, b0);
+      if (EPI == 1) rs += a0;
+    }
+    tile_store<EPI>(p, Cp + (int64_t)r * p.ldc4, c0 + c, acc, rs);
+  }
+}
+
+template <int CB, int EPI>
+__global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float4* Bs = reinterpret_cast<float4*>(smem);
+  int32_t* rp_s = reinterpret_cast<int32_t*>(smem + p.rp_off);
+  int32_t* col_s = reinterpret_cast<int32_t*>(smem + p.col_off);
+  float* val_s = reinterpret_cast<float*>(smem + p.val_off);
+  const int t = threadIdx.x;
+  const int32_t i = (int32_t)(blockIdx.x / (uint32_t)p.tiles);
+  const int32_t c0 = (int32_t)(blockIdx.x - (uint32_t)i * (uint32_t)p.tiles) * CB;
+  const int32_t cw = min(CB, p.k4 - c0);
+  tile_trace(p, 0);
+  // programmatic dependent launch: global memory only after the wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  tile_trace(p, 1);
+
+  // ---- RT1: where the matrix lives
+  int64_t g0;
+  int32_t n;
+  if (p.row_off) {
+    g0 = p.row_off[i];
+    n = p.sizes ? __ldg(p.sizes + i) : (int32_t)(p.row_off[i + 1] - g0);
+  } else {  // packed layout, offsets fused into the launch
+    n = __ldg(p.sizes + i);
+    g0 = tile_sizes_prefix(p.sizes, i);
+  }
+  if (n <= 0) return;
+  tile_trace(p, 2);
+
+  // ---- B tile: n x cw float4 by 16-byte cp.async (row pitch CB in shared memory)
+  const bool bst = n <= p.cap_rows;
+  if (bst) {
+    const float4* src = p.B + g0 * p.ldb4 + c0;
+    const int32_t cells = n * cw;
+    if (cw == CB) {
+      for (int32_t q = t; q < cells; q += kTileThreads)
+        cp_async16(Bs + q, src + (int64_t)(q / CB) * p.ldb4 + (q % CB));
+    } else {
+      for (int32_t q = t; q < cells; q += kTileThreads) {
+        const int32_t j = q / cw, c = q - j * cw;
+        cp_async16(Bs + j * CB + c, src + (int64_t)j * p.ldb4 + c);
+      }
+    }
+    cp_async_commit();
+  }
+  tile_trace(p, 3);
+
+  // ---- RT2 / RT3: row pointers, then the matrix's (col, val) run
+  const int32_t z0 = __ldg(p.row_ptr + g0), z1 = __ldg(p.row_ptr + g0 + n);
+  const int32_t nz = z1 - z0;
+  const bool sst = bst && nz <= p.cap_nnz;
+  if (sst) {
+    for (int32_t r = t; r <= n; r += kTileThreads) rp_s[r] = __ldg(p.row_ptr + g0 + r) - z0;
+    constexpr int U = 4;
+    for (int32_t e = t; e < nz; e += U * kTileThreads) {
+      int32_t cv[U];
+      float vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t ee = e + u * kTileThreads;
+        cv[u] = ee < nz ? __ldg(p.col + z0 + ee) : 0;
+        vv[u] = ee < nz ? __ldg(p.vals + z0 + ee) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t ee = e + u * kTileThreads;
+        if (ee < nz) {
+          col_s[ee] = cv[u];
+          val_s[ee] = vv[u];
+        }
+      }
+    }
+  }
+  tile_trace(p, 4);
+  if (bst) cp_async_wait_all();
+  __syncthreads();
+  tile_trace(p, 5);
+
+  // ---- row pass
+  if (sst) tile_rows<CB, EPI, true, true>(p, Bs, rp_s, col_s, val_s, g0, n, c0, cw);
+  else if (bst) tile_rows<CB, EPI, true, false>(p, Bs, rp_s, col_s, val_s, g0, n, c0, cw);
+  else tile_rows<CB, EPI, false, false>(p, Bs, rp_s, col_s, val_s, g0, n, c0, cw);
+  tile_trace(p, 6);
+}
+
+// Launch geometry for a batch; false when the batch is better served by the
+// persistent pipeline (more tiles than the GPU holds at once).
+bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int32_t num_sms, int32_t cb_override,
+               TileLayout* out) {
+  if (batch < 1 || k % 4 != 0) return false;
+  const int32_t k4 = k / 4;
+  const int64_t R = max_rows > 0 ? max_rows : kDefaultRows;
+  const int64_t Z = max_nnz > 0 ? max_nnz : 8 * R;
+  auto a16 = [](int64_t x) { return (x + 15) / 16 * 16; };
+  auto layout = [&](int32_t cb, TileLayout& L) {
+    L.cb = cb;
+    L.tiles = (int32_t)ceil_div(k4, cb);
+    L.units = (int64_t)batch * L.tiles;
+    L.cap_rows = (int32_t)std::min<int64_t>(R, 1 << 20);
+    L.cap_nnz = (int32_t)std::min<int64_t>(Z, 1 << 20);
+    L.rp_off = (int32_t)a16((int64_t)L.cap_rows * cb * 16);
+    L.col_off = (int32_t)(L.rp_off + a16(4LL * (L.cap_rows + 1)));
+    L.val_off = (int32_t)(L.col_off + a16(4LL * L.cap_nnz));
+    L.smem = (int32_t)(L.val_off + a16(4LL * L.cap_nnz));
+    // resident CTAs per SM: 16 by threads (2048 / 128), fewer by shared memory
+    // (228 KB per SM, 1 KB reserved per CTA)
+    L.per_sm = (int32_t)std::min<int64_t>(16, 233472 / (L.smem + 1024 + 64));
+  };
+  TileLayout L{};
+  if (cb_override > 0) {
+    int32_t cb = 1;
+    while (cb < cb_override && cb < 32) cb <<= 1;
+    layout(cb, L);
+  } else {
+    // widest tiles that still give >= 8 tiles per SM (overlap between the CTAs
+    // of an SM), and a B tile of at most 32 KB
+    int32_t cb = 1;
+    while (cb < 32 && cb < k4) cb <<= 1;
+    layout(cb, L);
+    while (cb > 1 && (L.units < 8LL * num_sms || R * cb * 16 > 32768)) {
+      cb >>= 1;
+      layout(cb, L);
+    }
+  }
+  if (L.smem > 200 * 1024 || L.per_sm < 1) return false;
+  // one wave: every tile resident at once (beyond that the persistent
+  // pipeline streams better, e.g. config 5)
+  if (cb_override <= 0 && L.units > (int64_t)L.per_sm * num_sms) return false;
+  *out = L;
+  return true;
+}
+
+template <int CB, int EPI>
+static cudaError_t launch_tile_t(const TileParams& tp, const TileLayout& L, cudaStream_t s) {
+  auto kern = spmm_tile_kernel<CB, EPI>;
+  static thread_local int configured[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (L.smem > 48 * 1024 && configured[dev & 63] < L.smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
+    if (e != cudaSuccess) return e;
+    configured[dev & 63] = L.smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)L.units);
+  cfg.blockDim = dim3(kTileThreads);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tp);
+}
+
+template <int EPI>
+static cudaError_t launch_tile_e(const TileParams& tp, const TileLayout& L, cudaStream_t s) {
+  switch (L.cb) {
+    case 1: return launch_tile_t<1, EPI>(tp, L, s);
+    case 2: return launch_tile_t<2, EPI>(tp, L, s);
+    case 4: return launch_tile_t<4, EPI>(tp, L, s);
+    case 8: return launch_tile_t<8, EPI>(tp, L, s);
+    case 16: return launch_tile_t<16, EPI>(tp, L, s);
+    default: return launch_tile_t<32, EPI>(tp, L, s);
+  }
+}
+
+cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t s) {
+  if (L.units == 0) return cudaSuccess;
+  if (L.units > 0x7fffffffLL) return cudaErrorInvalidValue;
+  TileParams tp;
+  tp.batch = a.batch;
+  tp.k4 = a.k / 4;
+  tp.tiles = L.tiles;
+  tp.cap_rows = L.cap_rows;
+  tp.cap_nnz = L.cap_nnz;
+  tp.rp_off = L.rp_off;
+  tp.col_off = L.col_off;
+  tp.val_off = L.val_off;
+  tp.row_off = a.row_off;
+  tp.sizes = a.sizes;
+  tp.row_ptr = a.row_ptr;
+  tp.col = a.col;
+  tp.vals = a.vals;
+  tp.B = reinterpret_cast<const float4*>(a.B);
+  tp.ldb4 = a.ldb / 4;
+  tp.C = reinterpret_cast<float4*>(a.C);
+  tp.ldc4 = a.ldc / 4;
+  tp.bias = reinterpret_cast<const float4*>(a.bias);
+  tp.accumulate = a.accumulate;
+  tp.trace = a.trace;
+  const int epi = (a.bias != nullptr || a.accumulate != 0) ? 1 : 0;
+  return epi ? launch_tile_e<1>(tp, L, s) : launch_tile_e<0>(tp, L, s);
+}
+
+}  // namespace bspmm

@@ -195,10 +195,15 @@ def config(cid: int, *, i0: int = 0, i1: Optional[int] = None, int_valued: bool 
 
 def random_batch(rng: np.random.Generator, batch: int, k: int, *, nmax: int = 12, dmax: int = 4,
                  int_valued: bool = False, empty_rows: bool = True, allow_empty_graphs: bool = True,
-                 duplicates: bool = False) -> Batch:
+                 duplicates: bool = False, sizes: Optional[np.ndarray] = None) -> Batch:
     """Small adversarial batches for tests (numpy Generator, seeded by the caller):
-    empty graphs, empty rows, unsorted rows and (optionally) duplicate entries."""
-    sizes = rng.integers(0 if allow_empty_graphs else 1, nmax + 1, size=batch).astype(np.int32)
+    empty graphs, empty rows, unsorted rows and (optionally) duplicate entries.
+    ``sizes`` fixes n_i (length ``batch``) instead of drawing them."""
+    if sizes is None:
+        sizes = rng.integers(0 if allow_empty_graphs else 1, nmax + 1, size=batch).astype(np.int32)
+    else:
+        sizes = np.ascontiguousarray(sizes, dtype=np.int32)
+        assert sizes.shape == (batch,)
     rows_cols, per_graph_nnz = [], []
     for n in sizes:
         cols_g = []

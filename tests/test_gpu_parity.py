@@ -56,6 +56,15 @@ def assert_parity(b, C, what=""):
     assert diff[0].size == 0, f"{what}: {diff[0].size} elements differ bitwise from O3', first {diff[0][:5]}"
 
 
+# debug bit 16384 keeps small batches on the pipeline kernel (spmm_csr.cu);
+# 0 lets the planner pick the small-batch tile kernel (spmm_tile.cu)
+KERNELS = {"auto": 0, "pipeline": 16384}
+
+
+def use_kernel(h, kern):
+    h.set_debug(KERNELS[kern])
+
+
 # ------------------------------------------------------------ a-1 offsets
 
 @pytest.mark.parametrize("batch", [0, 1, 5, 1023, 1024, 1025, 4095, 4096, 4097, 65536, 100003])
@@ -76,11 +85,18 @@ def test_offsets_int64_no_wrap(h):
 
 # ------------------------------------------------------------ a-3..a-6 CSR SpMM
 
+@pytest.mark.parametrize("kern", ["auto", "pipeline"])
 @pytest.mark.parametrize("cid", [1, 2, 3, 4])
 @pytest.mark.parametrize("int_valued", [False, True])
-def test_configs_csr(h, cid, int_valued):
+def test_configs_csr(h, cid, int_valued, kern):
     b = synth.config(cid, int_valued=int_valued)
-    C = run_csr(h, b)
+    use_kernel(h, kern)
+    try:
+        C = run_csr(h, b)
+        if kern == "auto":
+            assert h.last_plan()["kernel"] == 1, "configs 1-4 fit one wave: tile kernel expected"
+    finally:
+        h.set_debug(0)
     assert_parity(b, C, f"config {cid}")
     if int_valued:
         Cref, _ = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
@@ -92,19 +108,30 @@ def test_k_sweep_adversarial(h, k):
     rng = np.random.default_rng(1000 + k)
     for trial in range(4):
         b = synth.random_batch(rng, int(rng.integers(1, 40)), k, nmax=70, dmax=6, duplicates=trial % 2 == 1)
-        assert_parity(b, run_csr(h, b), f"k={k} trial={trial}")
-        assert_parity(b, run_csr(h, b, sizes=True, hints=False), f"k={k} trial={trial} no hints")
+        for kern in KERNELS:
+            use_kernel(h, kern)
+            try:
+                assert_parity(b, run_csr(h, b), f"k={k} trial={trial} {kern}")
+                assert_parity(b, run_csr(h, b, sizes=True, hints=False), f"k={k} trial={trial} no hints {kern}")
+            finally:
+                h.set_debug(0)
 
 
 @pytest.mark.parametrize("k,ld", [(16, 20), (64, 68), (5, 7), (128, 129), (256, 260)])
-def test_leading_dimension(h, k, ld):
+@pytest.mark.parametrize("kern", ["auto", "pipeline"])
+def test_leading_dimension(h, k, ld, kern):
     rng = np.random.default_rng(k * ld)
     b = synth.random_batch(rng, 30, k, nmax=40, dmax=5)
-    C = run_csr(h, b, ld=ld)
+    use_kernel(h, kern)
+    try:
+        C = run_csr(h, b, ld=ld)
+    finally:
+        h.set_debug(0)
     assert_parity(b, C, f"k={k} ld={ld}")
 
 
-def test_padded_layout_untouched(h):
+@pytest.mark.parametrize("kern", ["auto", "pipeline"])
+def test_padded_layout_untouched(h, kern):
     """row_off with gaps + sizes: only matrix rows are written (padding stays NaN)."""
     rng = np.random.default_rng(42)
     b = synth.random_batch(rng, 20, 64, nmax=30, allow_empty_graphs=False)
@@ -121,8 +148,12 @@ def test_padded_layout_untouched(h):
     rp[Np] = b.row_ptr[-1]
     Cd = torch.full((Np, 64), float("nan"), device=DEV)
     h.set_hints(0, 0)
-    h.csr(T(ro), T(b.sizes), T(rp), T(b.col), T(b.vals), T(Bp), Cd)
-    C = Cd.cpu().numpy()
+    use_kernel(h, kern)
+    try:
+        h.csr(T(ro), T(b.sizes), T(rp), T(b.col), T(b.vals), T(Bp), Cd)
+        C = Cd.cpu().numpy()
+    finally:
+        h.set_debug(0)
     Cref = oracle.spmm_f32(64, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
     for i in range(b.batch):
         n = int(b.sizes[i])
@@ -130,15 +161,20 @@ def test_padded_layout_untouched(h):
         assert np.all(np.isnan(C[ro[i] + n:ro[i + 1]]))
 
 
-def test_large_matrices_direct_path(h):
+@pytest.mark.parametrize("kern", ["auto", "pipeline"])
+def test_large_matrices_direct_path(h, kern):
     """Matrices beyond the stage capacity (paper case 3) run from global memory."""
-    for k in (256, 7):
-        b = synth.generate(synth.MIX, (1500, 3000, 1, 8), 3, k, seed=77)
-        h.set_hints(64, 512)  # deliberately too small: forces the direct path
-        C = run_csr(h, b, hints=False)
-        assert_parity(b, C, f"direct k={k}")
-        # and with hints large enough that some units stage, mixed with direct ones
-        assert_parity(b, run_csr(h, b, hints=True), f"mixed k={k}")
+    use_kernel(h, kern)
+    try:
+        for k in (256, 7):
+            b = synth.generate(synth.MIX, (1500, 3000, 1, 8), 3, k, seed=77)
+            h.set_hints(64, 512)  # deliberately too small: forces the direct path
+            C = run_csr(h, b, hints=False)
+            assert_parity(b, C, f"direct k={k}")
+            # and with hints large enough that some units stage, mixed with direct ones
+            assert_parity(b, run_csr(h, b, hints=True), f"mixed k={k}")
+    finally:
+        h.set_debug(0)
 
 
 def test_empty_batch_and_empty_graphs(h):
@@ -315,7 +351,21 @@ def test_invalid_arguments_rejected(h):
 
 # ------------------------------------------------------------ full size (BASELINE.json c5, bench launch config)
 
-def test_c5_full_size_sampled(h):
+def window(b, i0, i1):
+    """Graphs [i0, i1) of batch b rebased to row / entry 0 (slices of b's arrays,
+    no regeneration): (row_off, row_ptr, col, vals, B, r0, r1, z0, z1)."""
+    r0, r1 = int(b.row_off[i0]), int(b.row_off[i1])
+    z0, z1 = int(b.row_ptr[r0]), int(b.row_ptr[r1])
+    return (b.row_off[i0:i1 + 1] - r0, b.row_ptr[r0:r1 + 1] - z0, b.col[z0:z1], b.vals[z0:z1], b.B[r0:r1],
+            r0, r1, z0, z1)
+
+
+def test_c5_full_size_exhaustive(h):
+    """BASELINE.json configs[4] at full size (65536 graphs, k = 256) in the bench's
+    launch configuration (device offsets builder + SpMM): the offsets bit-exact
+    against oracle.offsets, EVERY row bitwise equal to O3' and EVERY element
+    within the north_star bound of O3 (checked in windows of 8192 graphs to
+    bound host memory), and no element left unwritten."""
     b = synth.config(5)
     h.set_hints(60, int(b.nnz.max()))
     Bd, Cd = T(b.B), torch.full((b.n_rows, b.k), float("nan"), device=DEV)
@@ -323,23 +373,40 @@ def test_c5_full_size_sampled(h):
     ro = h.build_offsets(sizes)                        # the bench step: offsets + SpMM
     h.csr(ro, None, T(b.row_ptr), T(b.col), T(b.vals), Bd, Cd)
     torch.cuda.synchronize()
-    assert np.array_equal(ro.cpu().numpy(), b.row_off)
+    assert np.array_equal(ro.cpu().numpy(), oracle.offsets(b.sizes))
     C = Cd.cpu().numpy()
-    rng = np.random.default_rng(2024)
-    mats = np.unique(rng.integers(0, b.batch, 600))
-    # whole sampled matrices: bound + bitwise against O3'
-    for i in mats[:150]:
-        g0, g1 = int(b.row_off[i]), int(b.row_off[i + 1])
-        z0, z1 = int(b.row_ptr[g0]), int(b.row_ptr[g1])
-        ro1 = np.array([0, g1 - g0], np.int64)
-        rp1 = b.row_ptr[g0:g1 + 1] - z0
-        ref32 = oracle.spmm_f32(b.k, ro1, None, rp1, b.col[z0:z1], b.vals[z0:z1], b.B[g0:g1])
-        assert np.array_equal(C[g0:g1].view(np.uint32), ref32.view(np.uint32)), i
-    rl = np.array([rng.integers(0, b.sizes[i]) for i in mats], np.int32)
-    ref, bound = oracle.spmm_rows(mats, rl, b.k, b.row_off, b.row_ptr, b.col, b.vals, b.B)
-    assert oracle.check_bound(C[b.row_off[mats] + rl], ref, bound)[0]
-    # property at any size: every row written (no NaN left), empty rows exact zero
+    del Bd, Cd
     assert not np.isnan(C).any()
+    W = 8192
+    for i0 in range(0, b.batch, W):
+        i1 = min(b.batch, i0 + W)
+        ro1, rp1, col1, v1, B1, r0, r1, _, _ = window(b, i0, i1)
+        ref32 = oracle.spmm_f32(b.k, ro1, None, rp1, col1, v1, B1)
+        diff = np.count_nonzero(C[r0:r1].view(np.uint32) != ref32.view(np.uint32))
+        assert diff == 0, f"graphs [{i0}, {i1}): {diff} elements differ bitwise from O3'"
+        ref, bound = oracle.spmm(b.k, ro1, None, rp1, col1, v1, B1)
+        ok, worst = oracle.check_bound(C[r0:r1], ref, bound)
+        assert ok, f"graphs [{i0}, {i1}): worst |d|/bound = {worst}"
+
+
+def test_fmaf_single_rounding_pin(h):
+    """The kernel accumulates with fused multiply-add, as O3' does (SURVEY §8(c)
+    O3'): row (v = -(1+2^-11), b = 1), then (v = 1+2^-12, b = 1+2^-12) gives
+    exactly 2^-24 with one rounding per FMA; multiply-then-add gives 0."""
+    n, k = 2, 4                                        # a 2-node graph: row 0 has entries at cols 0, 1
+    ro = np.array([0, 2], np.int64)
+    rp = np.array([0, 2, 2], np.int32)
+    col = np.array([0, 1], np.int32)
+    vals = np.array([-(1 + 2.0 ** -11), 1 + 2.0 ** -12], np.float32)
+    B = np.zeros((n, k), np.float32)
+    B[0, :] = 1.0
+    B[1, :] = 1 + 2.0 ** -12
+    h.set_hints(2, 2)
+    C = h.csr(T(ro), None, T(rp), T(col), T(vals), T(B)).cpu().numpy()
+    assert np.all(C[0] == np.float32(2.0 ** -24)), C[0]
+    assert np.all(C[1] == 0.0)
+    ref32 = oracle.spmm_f32(k, ro, None, rp, col, vals, B)
+    assert np.array_equal(C.view(np.uint32), ref32.view(np.uint32))
 
 
 # ------------------------------------------------------------ NEXT-3: the paper's atomic SWA-ST kernel
@@ -429,7 +496,7 @@ def test_early_first_tile_shapes(h, k, nlo, nhi, batch):
     only (row offsets summed from sizes by consumer warp 0)."""
     b = synth.generate(synth.MIX, (nlo, nhi, 1, 5), batch, k, seed=k + nhi)
     ref = None
-    for dbg in (0, 4):
+    for dbg in (16384, 16384 | 4):              # the pipeline kernel: early tile on / off
         h.set_debug(dbg)
         for sizes in (False, True):
             C = run_csr(h, b, sizes=sizes)
@@ -455,8 +522,13 @@ def test_early_first_tile_empty_first_matrices(h):
             break
     else:
         pytest.fail("no seed with empty leading matrices")
-    C = run_csr(h, b)
-    assert_parity(b, C, "empty first matrices")
+    for kern in KERNELS:
+        use_kernel(h, kern)
+        try:
+            C = run_csr(h, b)
+        finally:
+            h.set_debug(0)
+        assert_parity(b, C, f"empty first matrices {kern}")
 
 
 # ------------------------------------------------------------ library cross-check (SURVEY §4 tier 6)
@@ -489,7 +561,7 @@ def test_one_unit_consumer_path(h, k, nlo, nhi, batch):
     rng = np.random.default_rng(k + batch)
     b = synth.random_batch(rng, batch, k, nmax=nhi, dmax=5, duplicates=True)
     ref = None
-    for dbg in (0, 1024):
+    for dbg in (16384, 16384 | 1024):           # the pipeline kernel: one-unit path on / off
         h.set_debug(dbg)
         try:
             for sizes in (False, True):
@@ -510,3 +582,65 @@ def test_one_unit_consumer_path(h, k, nlo, nhi, batch):
         finally:
             h.set_debug(0)
             h.set_hints(0, 0)
+
+
+# ------------------------------------------------------------ small-batch tile kernel (spmm_tile.cu)
+
+def run_both(h, b, **kw):
+    out = {}
+    for kern in KERNELS:
+        use_kernel(h, kern)
+        try:
+            out[kern] = run_csr(h, b, **kw)
+            out[kern + "_plan"] = h.last_plan()
+        finally:
+            h.set_debug(0)
+    return out
+
+
+@pytest.mark.parametrize("k,nlo,nhi,batch", [(512, 50, 50, 100), (4, 1, 3, 2048), (8, 0, 9, 1500), (256, 1, 300, 64),
+                                             (1024, 2, 40, 7), (64, 20, 60, 100), (128, 10, 300, 200),
+                                             (300, 5, 40, 50), (36, 1, 20, 300)])
+def test_tile_shapes(h, k, nlo, nhi, batch):
+    """The tile kernel over mixed shapes: tiny matrices, empty ones, wide and
+    ragged k, large batches; bitwise O3' and bitwise equal to the pipeline
+    kernel, with row_off, sizes only (fused offsets) and both; and every
+    column-block width (bspmm_set_tile_cb) gives the same bits."""
+    b = synth.generate(synth.MIX, (max(nlo, 1), nhi, 1, 5), batch, k, seed=k * 7 + batch)
+    out = run_both(h, b)
+    assert_parity(b, out["auto"], f"tile k={k} plan={out['auto_plan']}")
+    assert np.array_equal(out["auto"].view(np.uint32), out["pipeline"].view(np.uint32))
+    out2 = run_both(h, b, sizes=True)                   # row_off + sizes
+    assert np.array_equal(out2["auto"].view(np.uint32), out["pipeline"].view(np.uint32))
+    Cd = torch.full((b.n_rows, k), float("nan"), device=DEV)
+    h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cd)   # fused offsets
+    torch.cuda.synchronize()
+    assert np.array_equal(Cd.cpu().numpy().view(np.uint32), out["pipeline"].view(np.uint32))
+    for cb in (1, 2, 4, 8, 16, 32):
+        h.set_tile_cb(cb)
+        try:
+            C = run_csr(h, b)
+            assert h.last_plan()["kernel"] == 1 and h.last_plan()["lanes"] == cb
+        finally:
+            h.set_tile_cb(0)
+        assert np.array_equal(C.view(np.uint32), out["pipeline"].view(np.uint32)), cb
+
+
+def test_tile_fallbacks(h):
+    """Tiles whose matrix exceeds the planned capacity (hints far too small)
+    read B and / or the structure from global memory: still bitwise O3'.
+    (1) one 20000-row matrix, k = 512; (2) mostly-empty matrices; (3) rows
+    and entries beyond the capacity."""
+    cases = [synth.generate(synth.MIX, (20000, 20000, 1, 3), 1, 512, seed=5)]
+    rng = np.random.default_rng(11)
+    sizes = np.where(np.arange(2048) % 50 == 0, 1, 0).astype(np.int32)
+    cases.append(synth.random_batch(rng, 2048, 512, dmax=1, sizes=sizes))
+    cases.append(synth.generate(synth.MIX, (1500, 3000, 1, 8), 3, 256, seed=77))
+    for b in cases:
+        h.set_hints(8, 16)                               # deliberately too small
+        try:
+            out = run_both(h, b, hints=False)
+        finally:
+            h.set_hints(0, 0)
+        assert_parity(b, out["auto"], "tile fallback")
+        assert np.array_equal(out["auto"].view(np.uint32), out["pipeline"].view(np.uint32))

@@ -110,6 +110,30 @@ def test_golden_spmm(golden):
         assert np.array_equal(C32, want), ex["cite"]
 
 
+def test_golden_fmaf_storage_order(golden):
+    """O3' is fmaf in storage order, not multiply-then-add: the worked example
+    separates the two (one rounding per FMA gives 2^-24, a rounded product
+    gives 0).  O3 (fp64) is exactly 2^-24 as well."""
+    for ex in golden["spmm_f32"]:
+        n, k = ex["n"], ex["k"]
+        ent = ex["entries"]                            # already in storage order (row 0: cols 0, 1)
+        rp = np.zeros(n + 1, dtype=np.int32)
+        for r, _, _ in ent:
+            rp[r + 1] += 1
+        rp = np.cumsum(rp).astype(np.int32)
+        col = np.array([c for _, c, _ in ent], dtype=np.int32)
+        vals = np.array([v for _, _, v in ent], dtype=np.float32)
+        B = np.array(ex["B"], dtype=np.float32).reshape(n, k)
+        ro = np.array([0, n], dtype=np.int64)
+        C32 = oracle.spmm_f32(k, ro, None, rp, col, vals, B)
+        C, _ = oracle.spmm(k, ro, None, rp, col, vals, B)
+        assert np.array_equal(C32, np.array(ex["C_f32"], dtype=np.float32)), ex["cite"]
+        assert np.array_equal(C, np.array(ex["C_f64"], dtype=np.float32)), ex["cite"]
+        # the alternative the pin rules out, evaluated in numpy fp32 (product rounded, then added)
+        mta = np.float32(np.float32(vals[0] * B[0, 0]) + np.float32(vals[1] * B[1, 0]))
+        assert mta == np.float32(ex["C_mul_then_add"][0][0]) and mta != C32[0, 0]
+
+
 def test_identity_gives_B():
     rng = np.random.default_rng(1)
     sizes = np.array([5, 0, 1, 17, 3], dtype=np.int32)

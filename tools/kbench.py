@@ -16,6 +16,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import paper_1903_11409_b200 as bs  # noqa: E402
 import synth  # noqa: E402
 from bench import alg_bytes, peaks  # noqa: E402
@@ -72,6 +73,24 @@ def time_calls(h, reps, R, fn, graph=True):
     return e0.elapsed_time(e1) / R
 
 
+def trace_in_graph(h, reps, R):
+    """Phase trace of the LAST launch of a graph of R back-to-back SpMM launches
+    (steady state: the trace pointer is captured into every launch, each
+    overwrites the buffer)."""
+    from trace import summarize
+    spmm_only(h, reps[0])
+    torch.cuda.synchronize()
+    plan = h.last_plan()
+    buf = torch.zeros((plan["grid"], 32), dtype=torch.int64, device=reps[0]["B"].device)
+    buf.fill_(-1)
+    h.set_trace(buf)
+    try:
+        time_calls(h, reps, R, spmm_only)
+    finally:
+        h.set_trace(None)
+    return summarize(buf.cpu().numpy().astype(np.int64), plan)
+
+
 def spmm_only(h, r):
     h.csr(r["ro"], None, r["rp"], r["col"], r["vals"], r["B"], r["C"])
 
@@ -105,8 +124,36 @@ def sddmm_only(h, r):  # NEXT-2 piece: grad_vals = <grad_C[row], B[col]> (C stan
     h.sddmm(r["ro"], None, r["rp"], r["col"], r["B"], r["C"])
 
 
-def copy_only(h, r):  # practical floor: a device copy moving B's bytes in and C's out
+def copy_only(h, r):  # torch's device copy moving B's bytes in and C's out
     r["C"].copy_(r["B"])
+
+
+_floor = None
+
+
+def floor_lib():
+    """tools/probe/libfloor.so: hand-written one-CTA-per-SM copies of B into C,
+    launched like the SpMM kernels (PDL, same graph)."""
+    global _floor
+    if _floor is None:
+        import ctypes
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "probe", "libfloor.so")
+        _floor = ctypes.CDLL(path)
+        _floor.floor_copy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+        _floor.floor_copy.restype = ctypes.c_int
+    return _floor
+
+
+def floor_copy(mode, groups=4):
+    def fn(h, r):
+        n4 = r["B"].numel() // 4
+        grid = torch.cuda.get_device_properties(r["B"].device).multi_processor_count
+        rc = floor_lib().floor_copy(r["B"].data_ptr(), r["C"].data_ptr(), n4, mode, groups, grid,
+                                    torch.cuda.current_stream().cuda_stream, r["dep"].data_ptr())
+        if rc != 0:
+            raise RuntimeError(f"floor_copy rc={rc}")
+    return fn
 
 
 def offsets_only(h, r):
@@ -129,6 +176,7 @@ def main():
     ap.add_argument("--shard", type=int, default=1, help="time rank 0's shard of an N-way split (1 GPU)")
     ap.add_argument("--backward", action="store_true", help="also time csr_backward (grad_B and grad_vals)")
     ap.add_argument("--sddmm-dbg", default="", help="with --backward: debug bit sets for extra SDDMM timings")
+    ap.add_argument("--trace", action="store_true", help="phase trace of the last launch of the graph (per dbg)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -165,9 +213,10 @@ def main():
                 continue
             plan = h.last_plan()
             gbs = per / (ms / 1e3) / 1e9
+            tr = {"trace": trace_in_graph(h, reps, R)} if args.trace else {}
             print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "chunks": ch, "dbg": dbg, "us": ms * 1e3, "GBs": gbs,
                               "frac": gbs / peak, "GFLOPs": 2 * b.n_nnz * b.k / (ms / 1e3) / 1e9,
-                              "replicas": len(reps), "shard": args.shard, "plan": plan}), flush=True)
+                              "replicas": len(reps), "shard": args.shard, "plan": plan, **tr}), flush=True)
         h.set_tuning(0, 0, 0)
         h.set_debug(0)
         ms_step = time_calls(h, reps, R, full_step)
@@ -187,6 +236,17 @@ def main():
             ms_cp = time_calls(h, reps, R, copy_only)
             extra["copy_us"] = ms_cp * 1e3
             extra["copy_GBs"] = 8 * b.n_rows * b.k / (ms_cp / 1e3) / 1e9
+            if cid != 5:  # one-wave configs: hand-written 148-CTA copies (floor.cu modes)
+                for r in reps:
+                    r["dep"] = torch.zeros(64, dtype=torch.int64, device=dev)
+                for mode, name in ((0, "floor_cpasync"), (1, "floor_regs"), (2, "floor_tma_stg"), (3, "floor_tma_tma"),
+                                   (1 | 4, "floor_regs_rt1"), (1 | 12, "floor_regs_rt1_evl"), (2 | 4, "floor_tma_stg_rt1")):
+                    for g in ((1, 2, 4, 8) if mode & 3 in (0, 2, 3) else (1,)):
+                        try:
+                            ms_f = time_calls(h, reps, R, floor_copy(mode, g))
+                            extra[f"{name}_g{g}_us"] = ms_f * 1e3
+                        except Exception as e:  # noqa: BLE001
+                            extra[f"{name}_g{g}_err"] = str(e)
         if b.k % 4 == 0 and cid != 5:
             extra["coo_convert_csr_us"] = time_calls(h, reps, R, coo_convert_csr) * 1e3
             extra["coo_atomic_us"] = time_calls(h, reps, R, coo_atomic) * 1e3

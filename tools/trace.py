@@ -21,6 +21,24 @@ SLOTS = ["entry", "after_pdl_wait", "prod_rowoff", "prod_struct_off", "prod_done
          "cons_done", "exit", "cons_unit0_done", "p0_after_empty", "p0_after_tma", "p0_before_arrive",
          "p1_before_arrive", "p0_after_arrive", "p1_after_arrive", "early_b_issued"]
 SLOTS += [f"u{j}_{w}" for j in range(3) for w in ("empty_ok", "slice_issued", "tma_issued", "copies_issued")]
+# the small-batch tile kernel (spmm_tile.cu, plan kernel == 1)
+TILE_SLOTS = ["entry", "after_pdl_wait", "rt1_done", "b_issued", "struct_staged", "b_landed", "done"]
+
+
+def summarize(t, plan):
+    """Per-slot [min, median, max] over CTAs (us, relative to the earliest CTA
+    entry) of one launch's trace rows t [grid x 32] (unwritten slots < 0)."""
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3
+    tile = plan.get("kernel", 0) == 1
+    names, last = (TILE_SLOTS, 6) if tile else (SLOTS, 7)
+    out = {"span_us": float((t[:, last].max() - t0) / 1e3)}
+    for k, name in enumerate(names):
+        col_ = rel[:, k][t[:, k] > 0]
+        if col_.size == 0:
+            continue
+        out[name] = [round(float(col_.min()), 2), round(float(np.median(col_)), 2), round(float(col_.max()), 2)]
+    return out
 
 
 def main():
@@ -46,14 +64,16 @@ def main():
     sz = T(b.sizes)
     C = torch.empty((b.n_rows, b.k), device=dev)
     h.csr(ro, None, rp, col, vals, B, C)
+    h.set_debug(args.dbg | (1 if args.nostore else 0))
+    h.csr(ro, None, rp, col, vals, B, C)
     grid = h.last_plan()["grid"]
     buf = torch.zeros((grid, 32), dtype=torch.int64, device=dev)
-    h.set_debug(args.dbg | (1 if args.nostore else 0))
     flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device=dev)
     for it in range(args.launches):
         if not args.warm:
             flush.fill_(float(it))
         torch.cuda.synchronize()
+        buf.fill_(-(1 << 62))
         h.set_trace(buf)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -65,13 +85,8 @@ def main():
         h.set_trace(None)
         torch.cuda.synchronize()
         t = buf.cpu().numpy().astype(np.int64)
-        t0 = t[:, 0].min()
-        rel = (t - t0) / 1e3  # us
-        out = {"config": args.config, "launch": it, "nostore": args.nostore, "event_us": e0.elapsed_time(e1) * 1e3, "plan": h.last_plan(),
-               "span_us": float((t[:, 7].max() - t0) / 1e3)}
-        for k, name in enumerate(SLOTS):
-            col_ = rel[:, k]
-            out[name] = [round(float(col_.min()), 2), round(float(np.median(col_)), 2), round(float(col_.max()), 2)]
+        out = {"config": args.config, "launch": it, "nostore": args.nostore, "event_us": e0.elapsed_time(e1) * 1e3,
+               "plan": h.last_plan(), **summarize(t, h.last_plan())}
         print(json.dumps(out), flush=True)
 
 
