@@ -159,7 +159,53 @@ def cpu_baseline(b, budget_s: float = 12.0):
         reps += 1
     return {"value": fl_tot / tot / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
             "sample": f"first {nb} of {b.batch} graphs of the rank-0 shard (config 5) x {reps} runs, "
-                      f"fp64 oracle.spmm (OpenMP over matrices), {tot:.1f} s"}
+                      f"fp64 oracle.spmm (OpenMP over matrices), {tot:.1f} s",
+            "cpu_model": cpu_model(), "runs": reps,
+            "one_thread_configs_1_4": oracle_one_thread()}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+_ONE_THREAD = r"""
+import json, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle, synth
+out = {}
+for cid in (1, 2, 3, 4):
+    b = synth.config(cid)
+    ts = []
+    for _ in range(int(sys.argv[2])):
+        t = time.perf_counter()
+        oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
+        ts.append(time.perf_counter() - t)
+    fl = 2.0 * b.n_nnz * b.k
+    out["c%d" % cid] = {"mean_ms": 1e3 * float(np.mean(ts)), "median_ms": 1e3 * float(np.median(ts)),
+                        "runs": len(ts), "gflops_mean": fl / float(np.mean(ts)) / 1e9}
+print(json.dumps(out))
+"""
+
+
+def oracle_one_thread(runs: int = 10) -> dict:
+    """The oracle on ONE host thread (OMP_NUM_THREADS=1, a fresh process) over the
+    full configs 1-4: mean and median of `runs` executions each (the paper's
+    protocol is the mean of 10)."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    try:
+        r = subprocess.run([sys.executable, "-c", _ONE_THREAD, ROOT, str(runs)], env=env, capture_output=True,
+                           text=True, timeout=300)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # reported, never fatal for the bench line
+        return {"error": f"{type(e).__name__}: {e}"}
 
 
 def run_reference(args):
@@ -199,7 +245,8 @@ def run_reference(args):
            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": synth.CONFIG_NAMES[cid], "global_batch": c["batch"], "k": c["k"],
                       "parallelism": "cpu-oracle"},
-           "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
+                            "cpu_model": cpu_model()},
            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -215,6 +262,73 @@ def load_traffic(cid: int):
         except Exception:
             pass
     return None, None
+
+
+class ShardPlan:
+    """Row a-7 for one rank: the job's graphs, their split and this rank's range.
+
+    strong scaling: the config's batch is split into contiguous nnz*k-balanced
+    ranges (bspmm_partition, identical on every rank); weak: rank r owns graphs
+    [r*batch, (r+1)*batch) of the seeded stream (the job has world*batch graphs)."""
+
+    def __init__(self, cid: int, world: int, rank: int, scaling: str, partition_fn):
+        c = synth.CONFIGS[cid]
+        self.cid, self.world, self.rank, self.scaling = cid, world, rank, scaling
+        self.kind, self.params, self.k = c["kind"], c["params"], c["k"]
+        self.seed = synth.BASE_SEED + cid
+        self.gbatch = c["batch"] * (world if scaling == "weak" else 1)
+        n_all, z_all = synth.counts(self.kind, self.params, self.seed, 0, self.gbatch)
+        self.nnz_off_all = np.zeros(self.gbatch + 1, np.int64)
+        np.cumsum(z_all, out=self.nnz_off_all[1:])
+        self.row_off_all = np.zeros(self.gbatch + 1, np.int64)
+        np.cumsum(n_all, out=self.row_off_all[1:])
+        if scaling == "weak":
+            self.split = np.arange(world + 1, dtype=np.int64) * c["batch"]
+        else:
+            self.split = np.asarray(partition_fn(self.nnz_off_all, self.k, world), dtype=np.int64)
+        self.i0, self.i1 = int(self.split[rank]), int(self.split[rank + 1])
+        self.n_total = int(self.row_off_all[-1])
+        self.nnz_total = int(self.nnz_off_all[-1])
+
+    def rank_batch(self):
+        """This rank's graphs, regenerated alone from their per-graph seeds."""
+        return synth.generate(self.kind, self.params, self.gbatch, self.k, self.seed, i0=self.i0, i1=self.i1)
+
+    def row_bounds(self) -> np.ndarray:
+        return self.row_off_all[self.split]
+
+    def flops(self) -> float:
+        return 2.0 * self.nnz_total * self.k
+
+    def step_bytes(self) -> int:
+        return alg_bytes(self.n_total, self.nnz_total, self.k, self.gbatch) + offsets_bytes(self.gbatch)
+
+
+def job_timing(ms_rank: float, spmm_ms_rank: float, max_fn):
+    """Whole-job step time and SpMM time: the max over ranks (the slowest rank
+    finishes the job)."""
+    return max_fn(ms_rank), max_fn(spmm_ms_rank)
+
+
+def make_report(sp: ShardPlan, ms: float, steps: int, warmup: int, peak: float, **extra) -> dict:
+    """The bench JSON line (rank 0): whole-job GFLOP/s over all ranks' graphs."""
+    value = sp.flops() / (ms / 1e3) / 1e9
+    hbm_gbs = sp.step_bytes() / (ms / 1e3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": sp.world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": sp.scaling,
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-mol graphs, U[-1,1) values)",
+        "config": {"workload": synth.CONFIG_NAMES[sp.cid], "global_batch": sp.gbatch, "k": sp.k,
+                   "rows": sp.n_total, "nnz": sp.nnz_total,
+                   "parallelism": (f"batch-sharded x{sp.world} (nnz*k split)" if sp.scaling == "strong"
+                                   else f"x{sp.world} independent batches"),
+                   "l2": "inputs larger than L2 (no flush needed)"},
+        "hbm_gbs": hbm_gbs, "hbm_frac_of_measured": hbm_gbs / peak,
+    }
+    cfg_extra = extra.pop("config_extra", {})
+    out["config"].update(cfg_extra)
+    out.update(extra)
+    return out
 
 
 def main():
@@ -252,23 +366,11 @@ def main():
     assert world == args.gpus or world == 1, "--gpus must match WORLD_SIZE"
 
     cid = args.config
-    c = synth.CONFIGS[cid]
-    seed = synth.BASE_SEED + cid
     # a-7: every rank computes the same split from the per-graph nnz counts
-    # (weak scaling: rank r owns graphs [r*batch, (r+1)*batch) of the seeded stream)
-    gbatch = c["batch"] * (world if args.scaling == "weak" else 1)
-    n_all, z_all = synth.counts(c["kind"], c["params"], seed, 0, gbatch)
-    nnz_off_all = np.zeros(gbatch + 1, np.int64)
-    np.cumsum(z_all, out=nnz_off_all[1:])
-    row_off_all = np.zeros(gbatch + 1, np.int64)
-    np.cumsum(n_all, out=row_off_all[1:])
-    if args.scaling == "weak":
-        split = np.arange(world + 1, dtype=np.int64) * c["batch"]
-    else:
-        split = bs.partition(nnz_off_all, c["k"], world)
-    i0, i1 = int(split[rank]), int(split[rank + 1])
-    b = synth.generate(c["kind"], c["params"], gbatch, c["k"], seed, i0=i0, i1=i1)
+    sp = ShardPlan(cid, world, rank, args.scaling, bs.partition)
+    b = sp.rank_batch()
     k = b.k
+    gbatch = sp.gbatch
     h = bs.Handle(dev)
     h.set_hints(int(b.sizes.max()) if b.batch else 0, int(b.nnz.max()) if b.batch else 0)
     if args.kt or args.warps or args.ctas or args.chunks:
@@ -278,14 +380,14 @@ def main():
     sizes, row_ptr, col, vals, B = T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)
     ro = torch.empty(b.batch + 1, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    bounds = bdist.row_bounds(row_off_all, split)
+    bounds = sp.row_bounds()
     row_base = int(bounds[rank])
     mcbuf, C_full = None, None
     if args.allgather == "multicast":
-        mcbuf = bdist.mc_team_buffer((int(row_off_all[-1]), k), dev)
+        mcbuf = bdist.mc_team_buffer((sp.n_total, k), dev)
         C = mcbuf.uc[row_base:row_base + b.n_rows]
     elif args.allgather == "nccl":
-        C_full = torch.empty((int(row_off_all[-1]), k), dtype=torch.float32, device=dev)
+        C_full = torch.empty((sp.n_total, k), dtype=torch.float32, device=dev)
         C = C_full[row_base:row_base + b.n_rows]
     else:
         C = torch.empty((b.n_rows, k), dtype=torch.float32, device=dev)
@@ -330,14 +432,8 @@ def main():
     launches = h.launch_count() - launches0
     ms_rank = t0.elapsed_time(t1) / K
     spmm_ms_rank = float(np.mean([a.elapsed_time(e) for a, e in kev]))
-    ms = bdist.max_over_ranks(ms_rank, dev)
-    spmm_ms = bdist.max_over_ranks(spmm_ms_rank, dev)
-    NNZ_total = int(nnz_off_all[-1])
-    N_total = int(n_all.sum())
-    flops = 2.0 * NNZ_total * k
-    bytes_step = alg_bytes(N_total, NNZ_total, k, gbatch) + offsets_bytes(gbatch)
-    value = flops / (ms / 1e3) / 1e9
-    hbm_gbs = bytes_step / (ms / 1e3) / 1e9
+    ms, spmm_ms = job_timing(ms_rank, spmm_ms_rank, lambda x: bdist.max_over_ranks(x, dev))
+    flops = sp.flops()
     peak, peak_src = peaks()
     # roofline of the dominant kernel on this rank (the SpMM), per launch
     spmm_bytes = alg_bytes(b.n_rows, b.n_nnz, k, b.batch)
@@ -382,20 +478,9 @@ def main():
         cpu = cpu_baseline(b)
 
     if rank == 0:
-        out = {
-            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded G-mol graphs, U[-1,1) values)",
-            "config": {"workload": synth.CONFIG_NAMES[cid], "global_batch": gbatch, "k": k,
-                       "rows": N_total, "nnz": NNZ_total,
-                       "parallelism": (f"batch-sharded x{world} (nnz*k split)" if args.scaling == "strong"
-                                       else f"x{world} independent batches"),
-                       "allgather": args.allgather,
-                       "l2": "inputs larger than L2 (no flush needed)", "plan": plan},
-            "hbm_gbs": hbm_gbs, "hbm_frac_of_measured": hbm_gbs / peak,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clk.summary(),
-        }
+        out = make_report(sp, ms, K, args.warmup, peak, roofline=roof, cpu_baseline=cpu, e2e=e2e,
+                          gpu_launches=int(launches), clocks=clk.summary(),
+                          config_extra={"allgather": args.allgather, "plan": plan})
         print(json.dumps(out), flush=True)
     bdist.barrier(dev)
     bdist.finalize()

@@ -24,9 +24,18 @@
  *  - All functions return bspmm_status_t; nothing is thrown across the ABI.
  *  - Pointers marked "dev" are device pointers on the handle's device, owned
  *    by the caller (typically torch tensors); "host" pointers are host memory.
- *    The library never frees caller memory.  The handle owns only its
- *    workspace (grown on demand, freed by bspmm_destroy) and BORROWS the
- *    stream given to bspmm_create / bspmm_set_stream.
+ *    The library never frees caller memory.  The handle owns its device
+ *    workspace (grown on demand, freed by bspmm_destroy), one internal
+ *    non-blocking auxiliary stream and its events (created with the handle, so
+ *    calls can be captured into a CUDA graph on first use), and BORROWS the
+ *    stream given to bspmm_create / bspmm_set_stream.  bspmm_csr_backward and
+ *    bspmm_gcn_layer fork work onto the auxiliary stream and join it back into
+ *    the caller's stream before returning (also on error), so to the caller
+ *    every call is ordered on its stream.
+ *  - Handle state (workspace, scan state, error flag) is shared by the calls
+ *    of a handle: when bspmm_set_stream changes the stream, the new stream is
+ *    made to wait for all work enqueued so far on the previous one (the
+ *    previous stream must still exist at that point).
  *  - Calls on device pointers are asynchronous on the handle's stream: they
  *    enqueue kernels and return.  Inputs must stay alive and unmodified until
  *    the stream reaches that point.  Device faults surface from a later call,
@@ -114,7 +123,11 @@ BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* str
 /* Synchronises the handle's stream, frees the workspace.  NULL is a no-op. */
 BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h);
 
-/* Re-targets the borrowed stream (e.g. torch's current stream per call). */
+/* Re-targets the borrowed stream (e.g. torch's current stream per call).  On
+ * a change, the new stream waits (one event) for everything already enqueued
+ * on the old one, so work of this handle never overlaps across streams; the
+ * wait is skipped while either stream is capturing a CUDA graph.  Errors:
+ * INVALID_VALUE, CUDA. */
 BSPMM_API bspmm_status_t bspmm_set_stream(bspmm_handle_t h, void* stream);
 
 /* Planner hints (host scalars, optional; 0 = unknown).  max_rows: max n_i
@@ -210,8 +223,10 @@ BSPMM_API bspmm_status_t bspmm_mc_destroy(bspmm_mc_t mc);
  * A_i), the fast path (k, ldb, ldc % 4 == 0, aligned B, C) and no csr_*_out,
  * the conversion is FUSED into the SpMM launch: each unit's SparseTensor slice
  * is staged and sorted into CSR in shared memory (same canonical order, same
- * bits).  A matrix beyond the hints is then skipped and reported as
- * BSPMM_ERROR_INVALID_VALUE by the next bspmm_sync. */
+ * bits).  A matrix beyond the hints is then skipped -- ITS ROWS OF C ARE NOT
+ * WRITTEN -- and reported as BSPMM_ERROR_INVALID_VALUE by the next
+ * bspmm_sync: callers that cannot guarantee the hints must call bspmm_sync
+ * after the call (the Python binding's Handle.coo(checked=True) does). */
 BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
                                    const int32_t* sizes, const int64_t* nnz_off, const int32_t* idx,
                                    const float* vals, const float* B, int64_t ldb, float* C, int64_t ldc,
@@ -240,9 +255,14 @@ BSPMM_API bspmm_status_t bspmm_set_gcn_math(bspmm_handle_t h, int32_t mode);
  *         channel (channel-specific adjacency), absolute positions into the
  *         shared col / vals arrays; col LOCAL ids.
  *  Y      [total_rows x ldy] dev fp32 (overwritten).
- * One GEMM for all channels (cuBLAS, fp32-accurate) into handle workspace
- * (total_rows x channels x k floats), then one SpMM per channel with the bias
- * (as rowsum(A) * bias) and the channel sum fused into its epilogue. */
+ * U_ch = X W_ch is computed into handle workspace (total_rows x channels x k
+ * floats), then one SpMM per channel folds the bias (as rowsum(A) * bias)
+ * and the channel sum into its epilogue.  For 2..16 channels (and no
+ * VALIDATE) the channel GEMMs run one per channel on the handle's auxiliary
+ * stream and SpMM_ch waits only for GEMM_ch (GEMM_{ch+1} overlaps SpMM_ch;
+ * forked from and joined back into the caller's stream within the call, valid
+ * under graph capture); otherwise one strided-batched GEMM precedes the
+ * channel SpMMs on the caller's stream. */
 BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_t channels, int32_t n_x, int32_t k,
                                          const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
                                          const int32_t* col, const float* vals, const float* X, int64_t ldx,

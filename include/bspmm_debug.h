@@ -35,7 +35,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * do not store C (the result is then undefined); 2 = compute every unit from
  * global memory (no staging); 4 = no early B tile for the first unit of a
  * CTA; 8 = consumers repeat each unit's work 4 times;
- * 16 = (unused; was an L2 prefetch of small problems, no gain); 32 = always copy
+ * 16 = no TMA-descriptor prefetch in the tile kernel; 32 = always copy
  * the CSR slice with TMA; 64 = force the static unit schedule; 128 = force the
  * dynamic one; 256 = SDDMM by the standalone kernel instead of the SpMM
  * pipeline's SDDMM mode; 512 = standalone SDDMM without the L2 prefetch of
@@ -46,7 +46,9 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * transpose on the auxiliary stream (grad_B SpMM on the caller's stream);
  * 8192 = GCN layer with one batched GEMM before the channel SpMMs instead
  * of channel GEMMs pipelined on the auxiliary stream; 16384 = never the
- * small-batch tile kernel (small batches run the pipeline kernel).  0
+ * small-batch tile kernel (small batches run the pipeline kernel); 32768 =
+ * tile kernel stages B by cp.async even where 2-D TMA applies; 65536 = tile
+ * kernel issues its row-pointer round trip after the B tile.  0
  * (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 

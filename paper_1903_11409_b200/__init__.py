@@ -286,9 +286,14 @@ class Handle:
 
     def coo(self, row_off: Optional[torch.Tensor], sizes: Optional[torch.Tensor], nnz_off: torch.Tensor,
             idx: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None,
-            k: Optional[int] = None, total_rows: Optional[int] = None, csr_out=None) -> torch.Tensor:
+            k: Optional[int] = None, total_rows: Optional[int] = None, csr_out=None,
+            checked: bool = False) -> torch.Tensor:
         """Batched COO/SparseTensor SpMM (bspmm_coo): device COO->CSR, then the CSR kernel.
-        idx: int32 [nnz, 2] (row, col) local pairs.  csr_out: optional (row_ptr, col, vals) tensors."""
+        idx: int32 [nnz, 2] (row, col) local pairs.  csr_out: optional (row_ptr, col, vals) tensors.
+
+        With planner hints set (set_hints) the conversion is fused into the SpMM launch, and a
+        matrix larger than the hints is SKIPPED (its rows of C are left unwritten); that is
+        reported only by the next sync().  checked=True synchronises and raises here instead."""
         dev = self.device
         for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
                             ("nnz_off", nnz_off, torch.int64), ("idx", idx, torch.int32),
@@ -308,6 +313,8 @@ class Handle:
                            _ptr(B), ldb, _ptr(C), ldc, int(total_rows), int(idx.shape[0]),
                            _ptr(rp_o), _ptr(col_o), _ptr(val_o))
         self._raise(st, "bspmm_coo")
+        if checked:
+            self.sync()
         return C
 
     def coo_atomic(self, row_off: Optional[torch.Tensor], sizes: Optional[torch.Tensor], nnz_off: torch.Tensor,

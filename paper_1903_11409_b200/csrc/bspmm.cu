@@ -46,13 +46,20 @@ bspmm_status_t fail(bspmm_handle_t h, bspmm_status_t s, const char* msg) {
 
 inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// every stream that may still use handle-owned device memory
+cudaError_t sync_streams(bspmm_handle_t h) {
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e == cudaSuccess && h->s_aux) e = cudaStreamSynchronize(h->s_aux);
+  if (e == cudaSuccess && h->s_h2d) e = cudaStreamSynchronize(h->s_h2d);
+  if (e == cudaSuccess && h->s_d2h) e = cudaStreamSynchronize(h->s_d2h);
+  return e;
+}
+
 // grow a device buffer (synchronises the handle's streams before freeing)
 bspmm_status_t grow(bspmm_handle_t h, void** buf, size_t* cap, size_t need) {
   if (need <= *cap) return BSPMM_SUCCESS;
   if (*buf) {
-    CK(h, cudaStreamSynchronize(h->stream));
-    if (h->s_h2d) CK(h, cudaStreamSynchronize(h->s_h2d));
-    if (h->s_d2h) CK(h, cudaStreamSynchronize(h->s_d2h));
+    CK(h, sync_streams(h));
     CK(h, cudaFree(*buf));
     *buf = nullptr;
     *cap = 0;
@@ -83,7 +90,7 @@ bspmm_status_t scan_state(bspmm_handle_t h, int32_t batch, ScanState* ss) {
     const int32_t cap = std::max<int32_t>(tiles, 64);
     const size_t bytes = 256 + al256((size_t)cap * 4) + 2 * al256((size_t)cap * 8);
     if (h->scan_ws) {
-      CK(h, cudaStreamSynchronize(h->stream));
+      CK(h, sync_streams(h));
       CK(h, cudaFree(h->scan_ws));
       h->scan_ws = nullptr;
       h->scan_cap = 0;
@@ -203,6 +210,7 @@ BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* str
   // a backward call may be captured into a CUDA graph on its first use
   if (cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_handoff, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     cudaGetLastError();
     bspmm_destroy(h);
@@ -230,6 +238,7 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (h->s_aux) cudaStreamSynchronize(h->s_aux), cudaStreamDestroy(h->s_aux);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->ev_handoff) cudaEventDestroy(h->ev_handoff);
     for (auto& e : h->ev_ch)
       if (e) cudaEventDestroy(e);
     for (auto& e : h->ev)
@@ -246,9 +255,25 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
   return st;
 }
 
+// The handle's device state (workspace, scan tickets and status words, error
+// flag, schedule counter) is shared by its calls, so a call on a new stream must
+// not overlap work still queued on the previous one: on a change of stream the
+// new stream waits for everything enqueued so far on the old one (one event;
+// skipped while either stream is being captured into a CUDA graph, where the
+// capture itself orders the work).
 BSPMM_API bspmm_status_t bspmm_set_stream(bspmm_handle_t h, void* stream) {
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
-  h->stream = static_cast<cudaStream_t>(stream);
+  cudaStream_t next = static_cast<cudaStream_t>(stream);
+  if (next == h->stream) return BSPMM_SUCCESS;
+  DeviceGuard g(h->device);
+  cudaStreamCaptureStatus c0 = cudaStreamCaptureStatusNone, c1 = cudaStreamCaptureStatusNone;
+  CK(h, cudaStreamIsCapturing(h->stream, &c0));
+  CK(h, cudaStreamIsCapturing(next, &c1));
+  if (c0 == cudaStreamCaptureStatusNone && c1 == cudaStreamCaptureStatusNone) {
+    CK(h, cudaEventRecord(h->ev_handoff, h->stream));
+    CK(h, cudaStreamWaitEvent(next, h->ev_handoff, 0));
+  }
+  h->stream = next;
   return BSPMM_SUCCESS;
 }
 
@@ -283,7 +308,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 32767) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 131071) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -297,9 +322,7 @@ BSPMM_API bspmm_status_t bspmm_set_gcn_math(bspmm_handle_t h, int32_t mode) {
 BSPMM_API bspmm_status_t bspmm_sync(bspmm_handle_t h) {
   if (!h) return BSPMM_ERROR_INVALID_VALUE;
   DeviceGuard g(h->device);
-  CK(h, cudaStreamSynchronize(h->stream));
-  if (h->s_h2d) CK(h, cudaStreamSynchronize(h->s_h2d));
-  if (h->s_d2h) CK(h, cudaStreamSynchronize(h->s_d2h));
+  CK(h, sync_streams(h));
   CK(h, cudaGetLastError());
   if (h->coo_fused_pending) {  // a fused bspmm_coo skipped a matrix beyond the planner hints?
     h->coo_fused_pending = false;
@@ -379,7 +402,8 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
     plan.threads = 128;
     plan.smem_bytes = L.smem;
     h->last_plan = plan;
-    CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, nullptr, bias,
+    const TmaMaps* maps = L.cb >= 8 ? tma_maps(h, B, k, ldb, 4 * L.cb) : nullptr;
+    CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias,
               accumulate};
     CK(h, launch_spmm_tile(a, L, h->stream));
     h->launches++;
@@ -829,21 +853,32 @@ BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int
     if (st != BSPMM_SUCCESS) return st;
     CK(h, cudaEventRecord(h->ev_fork, h->stream));
     CK(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
+    // from here on every return joins s_aux back into the caller's stream (an
+    // unjoined fork would break a graph capture and leave s_aux work unordered)
+    struct Join {
+      bspmm_handle_t h;
+      cudaStream_t main;
+      ~Join() {
+        h->stream = main;
+        cudaEventRecord(h->ev_join, h->s_aux);
+        cudaStreamWaitEvent(main, h->ev_join, 0);
+      }
+    } join{h, h->stream};
     st = transpose_impl(h, batch, row_off, sizes, row_ptr, col, vals, w.rowT, w.colT, w.valsT, h->s_aux);
     if (st != BSPMM_SUCCESS) return st;
     if (!(h->dbg & 4096)) {  // grad_B = A^T grad_C on the auxiliary stream too, after the transpose
-      cudaStream_t main = h->stream;
       h->stream = h->s_aux;
       st = csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
-      h->stream = main;
+      h->stream = join.main;
       if (st != BSPMM_SUCCESS) return st;
     }
-    CK(h, cudaEventRecord(h->ev_join, h->s_aux));
     st = bspmm_sddmm(h, batch, k, row_off, sizes, row_ptr, col, B, ldb, grad_C, ldgc, grad_vals);
-    CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));  // joined even if the SDDMM call failed
     if (st != BSPMM_SUCCESS) return st;
-    if (h->dbg & 4096)
+    if (h->dbg & 4096) {  // grad_B on the caller's stream after the join
+      cudaEventRecord(h->ev_join, h->s_aux);
+      CK(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
       return csr_impl(h, batch, k, row_off, sizes, w.rowT, w.colT, w.valsT, grad_C, ldgc, grad_B, ldgb, false);
+    }
     return BSPMM_SUCCESS;
   }
   if (grad_vals) {  // dL/dval_e = <grad_C[row_e], B[col_e]>

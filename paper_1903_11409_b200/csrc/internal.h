@@ -164,6 +164,7 @@ struct bspmm_handle_s {
   // from and joined back into `stream` within the call)
   cudaStream_t s_aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_handoff = nullptr;  // bspmm_set_stream: new stream waits for the old one
   // GCN layer: per-channel GEMM done-events (channel GEMMs on s_aux overlap
   // the previous channel's SpMM on `stream`)
   static constexpr int kGcnEvents = 16;

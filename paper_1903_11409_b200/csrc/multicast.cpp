@@ -105,6 +105,20 @@ struct bspmm_mc_s {
   bool uc_reserved = false, mc_reserved = false;
 };
 
+// the mc_* entry points switch to the object's device and restore the caller's
+struct McDeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit McDeviceGuard(int d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != d) ok = cudaSetDevice(d) == cudaSuccess;
+  }
+  ~McDeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 extern "C" {
 
 BSPMM_API int32_t bspmm_mc_supported(int device) {
@@ -148,7 +162,8 @@ BSPMM_API bspmm_status_t bspmm_mc_create(int device, int num_devices, size_t byt
   *out = nullptr;
   if (!bspmm_mc_supported(device)) return BSPMM_ERROR_NOT_SUPPORTED;
   const Driver& d = drv();
-  if (cudaSetDevice(device) != cudaSuccess) return BSPMM_ERROR_CUDA;
+  McDeviceGuard dg(device);
+  if (!dg.ok) return BSPMM_ERROR_CUDA;
   bspmm_mc_s* m = new bspmm_mc_s;
   m->device = device;
   m->num_devices = num_devices;
@@ -176,7 +191,8 @@ BSPMM_API bspmm_status_t bspmm_mc_import(int device, int num_devices, size_t byt
   *out = nullptr;
   if (!bspmm_mc_supported(device)) return BSPMM_ERROR_NOT_SUPPORTED;
   const Driver& d = drv();
-  if (cudaSetDevice(device) != cudaSuccess) return BSPMM_ERROR_CUDA;
+  McDeviceGuard dg(device);
+  if (!dg.ok) return BSPMM_ERROR_CUDA;
   bspmm_mc_s* m = new bspmm_mc_s;
   m->device = device;
   m->num_devices = num_devices;
@@ -200,7 +216,8 @@ BSPMM_API bspmm_status_t bspmm_mc_import(int device, int num_devices, size_t byt
 BSPMM_API bspmm_status_t bspmm_mc_bind(bspmm_mc_t m, void** uc_ptr, void** mc_ptr) {
   if (!m || !uc_ptr || !mc_ptr) return BSPMM_ERROR_INVALID_VALUE;
   const Driver& d = drv();
-  if (cudaSetDevice(m->device) != cudaSuccess) return BSPMM_ERROR_CUDA;
+  McDeviceGuard dg(m->device);
+  if (!dg.ok) return BSPMM_ERROR_CUDA;
   CUmemAllocationProp ap = {};
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -240,7 +257,9 @@ BSPMM_API size_t bspmm_mc_bytes(bspmm_mc_t m) { return m ? m->bytes : 0; }
 BSPMM_API bspmm_status_t bspmm_mc_destroy(bspmm_mc_t m) {
   if (!m) return BSPMM_SUCCESS;
   const Driver& d = drv();
-  cudaSetDevice(m->device);
+  McDeviceGuard dg(m->device);
+  // the team buffer may be in use by work on any of the caller's streams,
+  // which the object does not know: drain the device before unmapping
   cudaDeviceSynchronize();
   if (m->mc_mapped) d.memUnmap(m->mc_va, m->bytes);
   if (m->mc_reserved) d.addrFree(m->mc_va, m->bytes);

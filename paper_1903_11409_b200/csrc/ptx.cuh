@@ -74,6 +74,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int32_t 
       : "memory");
 }
 
+// fetch a TMA descriptor (kernel parameter) into the TMA unit's cache ahead of
+// its first use: the first copy through a cold descriptor pays that fetch
+__device__ __forceinline__ void prefetch_tensormap(const void* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
 // L2 prefetch (fire-and-forget: no completion tracking, no SM-side state):
 // bytes at a 16-byte-aligned address, rounded down to a multiple of 16
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {

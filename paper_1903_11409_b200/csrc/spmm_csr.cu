@@ -1110,6 +1110,8 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
     mbar_init(early_bar(p, smem), 1);  // the first unit's early B tile
     fence_mbar_init();
   }
+  // warm the TMA descriptor cache for the k-tiled staging path
+  if (p.tma2d && threadIdx.x >= 32 && threadIdx.x < 32 + kTmaMaps) prefetch_tensormap(&maps.m[threadIdx.x - 32]);
   __syncthreads();
   // programmatic dependent launch: everything above overlapped the previous
   // kernel (e.g. the offsets builder); global memory is touched only after this

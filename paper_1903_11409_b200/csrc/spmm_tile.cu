@@ -60,6 +60,9 @@ struct TileParams {
   int64_t ldc4;
   const float4* __restrict__ bias;  // GCN epilogue (EPI 1): C += rowsum(A) (x) bias
   int32_t accumulate;               // GCN epilogue: C += previous C
+  int32_t tma;                      // 1: B tile by 2-D tensor TMA (maps: box {4 CB, 2^b rows})
+  int32_t rp_first;                 // 1: the row-pointer round trip is issued before the B tile
+  int32_t dbg_bits;                 // 1: no TMA descriptor prefetch
   unsigned long long* trace;        // debug: per-CTA phase timestamps (globaltimer ns), or null
 };
 
@@ -171,8 +174,10 @@ __device__ __forceinline__ void tile_rows(const TileParams& p, const float4* Bs,
 }
 
 template <int CB, int EPI>
-__global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParams p) {
+__global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParams p,
+                                                                 const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
   float4* Bs = reinterpret_cast<float4*>(smem);
   int32_t* rp_s = reinterpret_cast<int32_t*>(smem + p.rp_off);
   int32_t* col_s = reinterpret_cast<int32_t*>(smem + p.col_off);
@@ -182,6 +187,14 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
   const int32_t c0 = (int32_t)(blockIdx.x - (uint32_t)i * (uint32_t)p.tiles) * CB;
   const int32_t cw = min(CB, p.k4 - c0);
   tile_trace(p, 0);
+  if (CB >= 8 && p.tma) {  // before the wait: overlaps the previous kernel's tail
+    if (t == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+    if (t >= 32 && t < 32 + kTmaMaps && !(p.dbg_bits & 1)) prefetch_tensormap(&maps.m[t - 32]);
+    __syncthreads();
+  }
   // programmatic dependent launch: global memory only after the wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -200,9 +213,33 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
   if (n <= 0) return;
   tile_trace(p, 2);
 
-  // ---- B tile: n x cw float4 by 16-byte cp.async (row pitch CB in shared memory)
+  // ---- B tile: n x cw float4 (row pitch CB in shared memory), by 2-D tensor
+  // TMA -- popcount(n) boxes of 2^b rows, one per lane of warp 0, the higher
+  // bits first (every box lands 128-byte aligned: CB >= 8) -- or by 16-byte
+  // cp.async.  Columns past k are zero-filled by TMA and never stored.
   const bool bst = n <= p.cap_rows;
-  if (bst) {
+  const bool tma = CB >= 8 && p.tma && bst;
+  // RT2 issued first (its loads are in flight while the B copies are issued;
+  // they would otherwise queue behind the tile's bytes)
+  int32_t z0 = 0, z1 = 0, rp0 = 0;
+  if (p.rp_first) {
+    z0 = __ldg(p.row_ptr + g0);
+    z1 = __ldg(p.row_ptr + g0 + n);
+    if (t <= n) rp0 = __ldg(p.row_ptr + g0 + t);
+  }
+  if (tma) {
+    if (t < 32) {
+      if (t == 0) mbar_arrive_expect_tx(&bar, (uint32_t)n * CB * 16u);
+      __syncwarp();
+      const int32_t big = n >> 8, rem = n & 255;
+      for (int32_t q = t - 8; q >= 0 && q < big; q += 24)
+        tma_load_2d(Bs + (size_t)q * 256 * CB, &maps.m[kTmaMaps - 1], c0 * 4, (int32_t)(g0 + q * 256), &bar);
+      if (t < 8 && (rem & (1 << t))) {
+        const int32_t r0 = big * 256 + (rem >> (t + 1) << (t + 1));
+        tma_load_2d(Bs + (size_t)r0 * CB, &maps.m[t], c0 * 4, (int32_t)(g0 + r0), &bar);
+      }
+    }
+  } else if (bst) {
     const float4* src = p.B + g0 * p.ldb4 + c0;
     const int32_t cells = n * cw;
     if (cw == CB) {
@@ -219,11 +256,19 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
   tile_trace(p, 3);
 
   // ---- RT2 / RT3: row pointers, then the matrix's (col, val) run
-  const int32_t z0 = __ldg(p.row_ptr + g0), z1 = __ldg(p.row_ptr + g0 + n);
+  if (!p.rp_first) {
+    z0 = __ldg(p.row_ptr + g0);
+    z1 = __ldg(p.row_ptr + g0 + n);
+  }
   const int32_t nz = z1 - z0;
   const bool sst = bst && nz <= p.cap_nnz;
   if (sst) {
-    for (int32_t r = t; r <= n; r += kTileThreads) rp_s[r] = __ldg(p.row_ptr + g0 + r) - z0;
+    if (p.rp_first) {
+      if (t <= n) rp_s[t] = rp0 - z0;
+      for (int32_t r = t + kTileThreads; r <= n; r += kTileThreads) rp_s[r] = __ldg(p.row_ptr + g0 + r) - z0;
+    } else {
+      for (int32_t r = t; r <= n; r += kTileThreads) rp_s[r] = __ldg(p.row_ptr + g0 + r) - z0;
+    }
     constexpr int U = 4;
     for (int32_t e = t; e < nz; e += U * kTileThreads) {
       int32_t cv[U];
@@ -245,8 +290,13 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
     }
   }
   tile_trace(p, 4);
-  if (bst) cp_async_wait_all();
-  __syncthreads();
+  if (tma) {
+    __syncthreads();  // the structure in shared memory
+    mbar_wait(&bar, 0);
+  } else {
+    if (bst) cp_async_wait_all();
+    __syncthreads();
+  }
   tile_trace(p, 5);
 
   // ---- row pass
@@ -286,7 +336,9 @@ bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int3
     layout(cb, L);
   } else {
     // widest tiles that still give >= 8 tiles per SM (overlap between the CTAs
-    // of an SM), and a B tile of at most 32 KB
+    // of an SM), and a B tile of at most 32 KB; narrower than 8 float4 (128-byte
+    // rows, the 2-D TMA path) the pipeline kernel is faster (config 2: 3.9 vs
+    // 3.7 us, tools/kbench.py)
     int32_t cb = 1;
     while (cb < 32 && cb < k4) cb <<= 1;
     layout(cb, L);
@@ -294,6 +346,7 @@ bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int3
       cb >>= 1;
       layout(cb, L);
     }
+    if (cb < 8) return false;
   }
   if (L.smem > 200 * 1024 || L.per_sm < 1) return false;
   // one wave: every tile resident at once (beyond that the persistent
@@ -304,7 +357,7 @@ bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int3
 }
 
 template <int CB, int EPI>
-static cudaError_t launch_tile_t(const TileParams& tp, const TileLayout& L, cudaStream_t s) {
+static cudaError_t launch_tile_t(const TileParams& tp, const TmaMaps& maps, const TileLayout& L, cudaStream_t s) {
   auto kern = spmm_tile_kernel<CB, EPI>;
   static thread_local int configured[64] = {};
   int dev = 0;
@@ -324,18 +377,18 @@ static cudaError_t launch_tile_t(const TileParams& tp, const TileLayout& L, cuda
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tp);
+  return cudaLaunchKernelEx(&cfg, kern, tp, maps);
 }
 
 template <int EPI>
-static cudaError_t launch_tile_e(const TileParams& tp, const TileLayout& L, cudaStream_t s) {
+static cudaError_t launch_tile_e(const TileParams& tp, const TmaMaps& m, const TileLayout& L, cudaStream_t s) {
   switch (L.cb) {
-    case 1: return launch_tile_t<1, EPI>(tp, L, s);
-    case 2: return launch_tile_t<2, EPI>(tp, L, s);
-    case 4: return launch_tile_t<4, EPI>(tp, L, s);
-    case 8: return launch_tile_t<8, EPI>(tp, L, s);
-    case 16: return launch_tile_t<16, EPI>(tp, L, s);
-    default: return launch_tile_t<32, EPI>(tp, L, s);
+    case 1: return launch_tile_t<1, EPI>(tp, m, L, s);
+    case 2: return launch_tile_t<2, EPI>(tp, m, L, s);
+    case 4: return launch_tile_t<4, EPI>(tp, m, L, s);
+    case 8: return launch_tile_t<8, EPI>(tp, m, L, s);
+    case 16: return launch_tile_t<16, EPI>(tp, m, L, s);
+    default: return launch_tile_t<32, EPI>(tp, m, L, s);
   }
 }
 
@@ -363,8 +416,15 @@ cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t
   tp.bias = reinterpret_cast<const float4*>(a.bias);
   tp.accumulate = a.accumulate;
   tp.trace = a.trace;
+  // 2-D TMA needs the handle's descriptors for box width 4 * cb (tma_maps)
+  // and a 128-byte shared row pitch; debug bit 32768 forces cp.async
+  tp.tma = (a.maps != nullptr && L.cb >= 8 && !(a.dbg & 32768)) ? 1 : 0;
+  tp.rp_first = (a.dbg & 65536) ? 0 : 1;
+  tp.dbg_bits = (a.dbg & 16) ? 1 : 0;
+  static const TmaMaps no_maps{};
+  const TmaMaps& m = a.maps ? *a.maps : no_maps;
   const int epi = (a.bias != nullptr || a.accumulate != 0) ? 1 : 0;
-  return epi ? launch_tile_e<1>(tp, L, s) : launch_tile_e<0>(tp, L, s);
+  return epi ? launch_tile_e<1>(tp, m, L, s) : launch_tile_e<0>(tp, m, L, s);
 }
 
 }  // namespace bspmm

@@ -57,12 +57,16 @@ def assert_parity(b, C, what=""):
 
 
 # debug bit 16384 keeps small batches on the pipeline kernel (spmm_csr.cu);
-# 0 lets the planner pick the small-batch tile kernel (spmm_tile.cu)
-KERNELS = {"auto": 0, "pipeline": 16384}
+# 0 lets the planner choose; "tile" forces the small-batch tile kernel
+# (spmm_tile.cu) with 8-float4 column blocks (2-D TMA staging), "tile_cpasync"
+# the same kernel staging B by cp.async (debug bit 32768)
+KERNELS = {"auto": (0, 0), "pipeline": (16384, 0), "tile": (0, 8), "tile_cpasync": (32768, 8)}
 
 
 def use_kernel(h, kern):
-    h.set_debug(KERNELS[kern])
+    dbg, cb = KERNELS[kern]
+    h.set_debug(dbg)
+    h.set_tile_cb(cb)
 
 
 # ------------------------------------------------------------ a-1 offsets
@@ -85,7 +89,7 @@ def test_offsets_int64_no_wrap(h):
 
 # ------------------------------------------------------------ a-3..a-6 CSR SpMM
 
-@pytest.mark.parametrize("kern", ["auto", "pipeline"])
+@pytest.mark.parametrize("kern", list(KERNELS))
 @pytest.mark.parametrize("cid", [1, 2, 3, 4])
 @pytest.mark.parametrize("int_valued", [False, True])
 def test_configs_csr(h, cid, int_valued, kern):
@@ -93,10 +97,12 @@ def test_configs_csr(h, cid, int_valued, kern):
     use_kernel(h, kern)
     try:
         C = run_csr(h, b)
-        if kern == "auto":
-            assert h.last_plan()["kernel"] == 1, "configs 1-4 fit one wave: tile kernel expected"
+        if kern.startswith("tile"):
+            assert h.last_plan()["kernel"] == 1, "forced tile kernel did not run"
+        if kern == "pipeline":
+            assert h.last_plan()["kernel"] == 0
     finally:
-        h.set_debug(0)
+        use_kernel(h, "auto")
     assert_parity(b, C, f"config {cid}")
     if int_valued:
         Cref, _ = oracle.spmm(b.k, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
@@ -114,11 +120,11 @@ def test_k_sweep_adversarial(h, k):
                 assert_parity(b, run_csr(h, b), f"k={k} trial={trial} {kern}")
                 assert_parity(b, run_csr(h, b, sizes=True, hints=False), f"k={k} trial={trial} no hints {kern}")
             finally:
-                h.set_debug(0)
+                use_kernel(h, "auto")
 
 
 @pytest.mark.parametrize("k,ld", [(16, 20), (64, 68), (5, 7), (128, 129), (256, 260)])
-@pytest.mark.parametrize("kern", ["auto", "pipeline"])
+@pytest.mark.parametrize("kern", list(KERNELS))
 def test_leading_dimension(h, k, ld, kern):
     rng = np.random.default_rng(k * ld)
     b = synth.random_batch(rng, 30, k, nmax=40, dmax=5)
@@ -126,11 +132,11 @@ def test_leading_dimension(h, k, ld, kern):
     try:
         C = run_csr(h, b, ld=ld)
     finally:
-        h.set_debug(0)
+        use_kernel(h, "auto")
     assert_parity(b, C, f"k={k} ld={ld}")
 
 
-@pytest.mark.parametrize("kern", ["auto", "pipeline"])
+@pytest.mark.parametrize("kern", list(KERNELS))
 def test_padded_layout_untouched(h, kern):
     """row_off with gaps + sizes: only matrix rows are written (padding stays NaN)."""
     rng = np.random.default_rng(42)
@@ -153,7 +159,7 @@ def test_padded_layout_untouched(h, kern):
         h.csr(T(ro), T(b.sizes), T(rp), T(b.col), T(b.vals), T(Bp), Cd)
         C = Cd.cpu().numpy()
     finally:
-        h.set_debug(0)
+        use_kernel(h, "auto")
     Cref = oracle.spmm_f32(64, b.row_off, None, b.row_ptr, b.col, b.vals, b.B)
     for i in range(b.batch):
         n = int(b.sizes[i])
@@ -161,7 +167,7 @@ def test_padded_layout_untouched(h, kern):
         assert np.all(np.isnan(C[ro[i] + n:ro[i + 1]]))
 
 
-@pytest.mark.parametrize("kern", ["auto", "pipeline"])
+@pytest.mark.parametrize("kern", list(KERNELS))
 def test_large_matrices_direct_path(h, kern):
     """Matrices beyond the stage capacity (paper case 3) run from global memory."""
     use_kernel(h, kern)
@@ -174,7 +180,7 @@ def test_large_matrices_direct_path(h, kern):
             # and with hints large enough that some units stage, mixed with direct ones
             assert_parity(b, run_csr(h, b, hints=True), f"mixed k={k}")
     finally:
-        h.set_debug(0)
+        use_kernel(h, "auto")
 
 
 def test_empty_batch_and_empty_graphs(h):
@@ -203,7 +209,7 @@ def test_tuning_space_bitwise(h):
         for cid in (3, 4):
             bb = synth.config(cid)
             assert_parity(bb, run_csr(h, bb), f"sched {sched_bits} config {cid}")
-    h.set_debug(0)
+    use_kernel(h, "auto")
 
 
 def test_deterministic_repeat(h):
@@ -510,7 +516,7 @@ def test_early_first_tile_shapes(h, k, nlo, nhi, batch):
         h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cd)
         torch.cuda.synchronize()
         assert np.array_equal(Cd.cpu().numpy().view(np.uint32), ref.view(np.uint32))
-    h.set_debug(0)
+    use_kernel(h, "auto")
 
 
 def test_early_first_tile_empty_first_matrices(h):
@@ -527,7 +533,7 @@ def test_early_first_tile_empty_first_matrices(h):
         try:
             C = run_csr(h, b)
         finally:
-            h.set_debug(0)
+            use_kernel(h, "auto")
         assert_parity(b, C, f"empty first matrices {kern}")
 
 
@@ -580,7 +586,7 @@ def test_one_unit_consumer_path(h, k, nlo, nhi, batch):
             torch.cuda.synchronize()
             assert np.array_equal(Cd.cpu().numpy().view(np.uint32), ref.view(np.uint32))
         finally:
-            h.set_debug(0)
+            use_kernel(h, "auto")
             h.set_hints(0, 0)
 
 
@@ -594,7 +600,7 @@ def run_both(h, b, **kw):
             out[kern] = run_csr(h, b, **kw)
             out[kern + "_plan"] = h.last_plan()
         finally:
-            h.set_debug(0)
+            use_kernel(h, "auto")
     return out
 
 
@@ -616,14 +622,18 @@ def test_tile_shapes(h, k, nlo, nhi, batch):
     h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cd)   # fused offsets
     torch.cuda.synchronize()
     assert np.array_equal(Cd.cpu().numpy().view(np.uint32), out["pipeline"].view(np.uint32))
-    for cb in (1, 2, 4, 8, 16, 32):
-        h.set_tile_cb(cb)
-        try:
-            C = run_csr(h, b)
-            assert h.last_plan()["kernel"] == 1 and h.last_plan()["lanes"] == cb
-        finally:
-            h.set_tile_cb(0)
-        assert np.array_equal(C.view(np.uint32), out["pipeline"].view(np.uint32)), cb
+    for kern in ("tile", "tile_cpasync"):
+        assert np.array_equal(out[kern].view(np.uint32), out["pipeline"].view(np.uint32)), kern
+    for dbg in (0, 32768):                              # 2-D TMA / cp.async staging of B
+        for cb in (1, 2, 4, 8, 16, 32):
+            h.set_tile_cb(cb)
+            h.set_debug(dbg)
+            try:
+                C = run_csr(h, b)
+                assert h.last_plan()["kernel"] == 1 and h.last_plan()["lanes"] == cb
+            finally:
+                use_kernel(h, "auto")
+            assert np.array_equal(C.view(np.uint32), out["pipeline"].view(np.uint32)), (cb, dbg)
 
 
 def test_tile_fallbacks(h):
@@ -643,4 +653,5 @@ def test_tile_fallbacks(h):
         finally:
             h.set_hints(0, 0)
         assert_parity(b, out["auto"], "tile fallback")
-        assert np.array_equal(out["auto"].view(np.uint32), out["pipeline"].view(np.uint32))
+        for kern in KERNELS:
+            assert np.array_equal(out[kern].view(np.uint32), out["pipeline"].view(np.uint32)), kern
