@@ -11,7 +11,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
              -ftz=false -prec-div=true -prec-sqrt=true -Iinclude -Xptxas -v
 LIB       := $(PKG)/libbspmm.so
-CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu $(CSRC)/backward.cu $(CSRC)/spmm_coo_atomic.cu $(CSRC)/spmm_tile.cu
+CU_SRCS   := $(CSRC)/bspmm.cu $(CSRC)/spmm_csr.cu $(CSRC)/coo2csr.cu $(CSRC)/offsets.cu $(CSRC)/backward.cu $(CSRC)/spmm_coo_atomic.cu $(CSRC)/spmm_tile.cu $(CSRC)/gcn_fused.cu
 HOST_SRCS := $(CSRC)/partition.cpp $(CSRC)/plan.cpp $(CSRC)/multicast.cpp
 HDRS      := include/bspmm.h $(CSRC)/internal.h $(CSRC)/ptx.cuh
 
@@ -21,7 +21,7 @@ lib: $(LIB)
 
 $(LIB): $(CU_SRCS) $(HOST_SRCS) $(HDRS)
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) $(HOST_SRCS) -lcublas -Xlinker -rpath=/usr/local/cuda/lib64 \
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CU_SRCS) $(HOST_SRCS) -Xlinker -rpath=/usr/local/cuda/lib64 \
 	  2> build/ptxas.log || (cat build/ptxas.log; false)
 	@grep -E "registers|spill|smem" build/ptxas.log | sed 's/^ptxas info *: //' > build/ptxas_summary.txt || true
 

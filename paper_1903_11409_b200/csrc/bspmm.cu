@@ -8,7 +8,6 @@
 #include <new>
 #include <string>
 
-#include <cublas_v2.h>
 #include <cudaTypedefs.h>
 
 #include "internal.h"
@@ -113,12 +112,9 @@ bspmm_status_t scan_state(bspmm_handle_t h, int32_t batch, ScanState* ss) {
   return BSPMM_SUCCESS;
 }
 
-// 2-D TMA descriptors for the k-tiled staging path, cached per (B, k, ldb, kt).
-// Encoded with the driver's cuTensorMapEncodeTiled, fetched through the runtime
-// (no link-time libcuda dependency).  Returns nullptr when not applicable.
-const TmaMaps* tma_maps(bspmm_handle_t h, const float* B, int32_t k, int64_t ldb, int32_t kt) {
-  if (kt % 32 != 0 || kt > 256 || ldb == kt) return nullptr;
-  if (h->maps_ok && h->maps_B == B && h->maps_k == k && h->maps_ldb == ldb && h->maps_kt == kt) return &h->maps;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time libcuda dependency)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -130,6 +126,31 @@ const TmaMaps* tma_maps(bspmm_handle_t h, const float* B, int32_t k, int64_t ldb
     }
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  return encode;
+}
+
+// 2-D fp32 tensor map: `outer` rows of `inner` elements, row pitch `pitch_bytes`
+bool encode_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
+               uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swizzle) {
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 2-D TMA descriptors for the k-tiled staging path, cached per (B, k, ldb, kt).
+// Encoded with the driver's cuTensorMapEncodeTiled, fetched through the runtime
+// (no link-time libcuda dependency).  Returns nullptr when not applicable.
+const TmaMaps* tma_maps(bspmm_handle_t h, const float* B, int32_t k, int64_t ldb, int32_t kt) {
+  if (kt % 32 != 0 || kt > 256 || ldb == kt) return nullptr;
+  if (h->maps_ok && h->maps_B == B && h->maps_k == k && h->maps_ldb == ldb && h->maps_kt == kt) return &h->maps;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = tensor_map_encoder();
+  if (!encode) return nullptr;
   const cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)0x7fffffff};  // rows: never read out of range
   const cuuint64_t strides[1] = {(cuuint64_t)ldb * 4};
   const cuuint32_t estr[2] = {1, 1};
@@ -216,13 +237,6 @@ BSPMM_API bspmm_status_t bspmm_create(bspmm_handle_t* out, int device, void* str
     bspmm_destroy(h);
     return BSPMM_ERROR_CUDA;
   }
-  bool ev_ok = true;
-  for (auto& e : h->ev_ch) ev_ok = ev_ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
-  if (!ev_ok) {
-    cudaGetLastError();
-    bspmm_destroy(h);
-    return BSPMM_ERROR_CUDA;
-  }
   *out = h;
   return BSPMM_SUCCESS;
 }
@@ -239,8 +253,6 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ev_handoff) cudaEventDestroy(h->ev_handoff);
-    for (auto& e : h->ev_ch)
-      if (e) cudaEventDestroy(e);
     for (auto& e : h->ev)
       if (e) cudaEventDestroy(e);
     if (h->ws) cudaFree(h->ws);
@@ -249,7 +261,6 @@ BSPMM_API bspmm_status_t bspmm_destroy(bspmm_handle_t h) {
     if (h->dev_sched) cudaFree(h->dev_sched);
     if (h->scan_ws) cudaFree(h->scan_ws);
     if (h->gcn_ws) cudaFree(h->gcn_ws);
-    if (h->cublas) cublasDestroy(static_cast<cublasHandle_t>(h->cublas));
   }
   delete h;
   return st;
@@ -606,11 +617,12 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
 
 // ---- fused batched GCN layer (NEXT-1) ----------------------------------------
 // PAPER.md Fig. algo:graph_conv_batched: for ch: U = X W[ch]; B = U + bias[ch];
-// C[ch] = BatchedSpMM(A[ch], B); Y = sum_ch C[ch].  Here: ONE strided-batched
-// GEMM computes U for every channel (cuBLAS, fp32-accurate BF16x9 tensor-core
-// emulation when available, else plain fp32), then ONE SpMM launch per channel
-// folds the bias (A (U + 1 b^T) = A U + rowsum(A) b^T) and the channel sum
-// into its epilogue: channels + 1 launches instead of the paper's 3 x channels.
+// C[ch] = BatchedSpMM(A[ch], B); Y = sum_ch C[ch].  Here (gcn_fused.cu): one
+// preparation launch (W to K-major + TF32 split, tile table) and ONE fused
+// tcgen05 launch computing Y = [A_ch X | rowsum(A_ch)] . [W_ch; bias_ch] per
+// 128-row x nt-feature tile, Z produced by the SpMM row loop straight into the
+// tensor core's shared-memory operand, the channel sum and bias in the TMEM
+// accumulation.  No library GEMM, no U round trip through HBM.
 BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_t channels, int32_t n_x, int32_t k,
                                          const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
                                          const int32_t* col, const float* vals, const float* X, int64_t ldx,
@@ -621,78 +633,53 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
     return fail(h, BSPMM_ERROR_INVALID_VALUE, "bad batch / channels / sizes / leading dimensions");
   if (batch == 0 || total_rows == 0) return BSPMM_SUCCESS;
   if (!row_off || !row_ptr || !X || !W || !Y) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
+  if (total_rows >= INT32_MAX) return fail(h, BSPMM_ERROR_NOT_SUPPORTED, "bspmm_gcn_layer: total_rows >= 2^31");
   DeviceGuard g(h->device);
-  const int64_t N = total_rows, ldu = (int64_t)channels * k;
-  bspmm_status_t st = grow(h, &h->gcn_ws, &h->gcn_ws_bytes, al256((size_t)N * ldu * 4));
-  if (st != BSPMM_SUCCESS) return st;
-  float* U = static_cast<float*>(h->gcn_ws);
-  if (!h->cublas) {
-    cublasHandle_t cb;
-    if (cublasCreate(&cb) != CUBLAS_STATUS_SUCCESS) return fail(h, BSPMM_ERROR_CUDA, "cublasCreate failed");
-    h->cublas = cb;
-  }
-  cublasHandle_t cb = static_cast<cublasHandle_t>(h->cublas);
-  cublasSetStream(cb, h->stream);
-  // column-major view: U_ch^T (k x N, ld channels*k) = W_ch^T (k x n_x, ld k) * X^T (n_x x N, ld ldx)
-  const float one = 1.f, zero = 0.f;
-  // fp32 (default): BF16x9 tensor-core emulation when the loaded cuBLAS has
-  // it, else CUDA-core fp32; TF32 / BF16: tensor cores at reduced input
-  // precision (bspmm_set_gcn_math; the tests bound each by its own rounding)
-  const cublasComputeType_t ct = h->gcn_math == BSPMM_GCN_TF32   ? CUBLAS_COMPUTE_32F_FAST_TF32
-                                 : h->gcn_math == BSPMM_GCN_BF16 ? CUBLAS_COMPUTE_32F_FAST_16BF
-                                                                 : CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
-  if (channels > 1 && channels <= bspmm_handle_s::kGcnEvents && !(h->flags & BSPMM_VALIDATE) && !(h->dbg & 8192)) {
-    // channel-pipelined: GEMM_ch on the auxiliary stream, SpMM_ch (which
-    // accumulates into Y, so the SpMMs stay in channel order) on the caller's
-    // stream after GEMM_ch -- GEMM_{ch+1} overlaps SpMM_ch
-    CK(h, cudaEventRecord(h->ev_fork, h->stream));
-    CK(h, cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
-    cublasSetStream(cb, h->s_aux);
+  const int64_t N = total_rows;
+  if (h->flags & BSPMM_VALIDATE) {
     for (int32_t ch = 0; ch < channels; ++ch) {
-      float* Uc = U + (int64_t)ch * k;
-      const float* Wc = W + (int64_t)ch * n_x * k;
-      cublasStatus_t cs = cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, Wc, CUDA_R_32F, k, X,
-                                       CUDA_R_32F, (int)ldx, &zero, Uc, CUDA_R_32F, (int)ldu, ct, CUBLAS_GEMM_DEFAULT);
-      if (cs != CUBLAS_STATUS_SUCCESS && h->gcn_math == BSPMM_GCN_FP32)
-        cs = cublasGemmEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, Wc, CUDA_R_32F, k, X, CUDA_R_32F,
-                          (int)ldx, &zero, Uc, CUDA_R_32F, (int)ldu, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-      CK(h, cudaEventRecord(h->ev_ch[ch], h->s_aux));
-      if (cs != CUBLAS_STATUS_SUCCESS) {
-        cublasSetStream(cb, h->stream);
-        CK(h, cudaStreamWaitEvent(h->stream, h->ev_ch[ch], 0));
-        return fail(h, h->gcn_math != BSPMM_GCN_FP32 ? BSPMM_ERROR_NOT_SUPPORTED : BSPMM_ERROR_CUDA,
-                    "cuBLAS GEMM failed");
-      }
+      CK(h, cudaMemsetAsync(h->dev_flag, 0, sizeof(int), h->stream));
+      CK(h, launch_validate_csr(batch, row_off, sizes, row_ptr + (int64_t)ch * (N + 1), col, h->dev_flag, h->stream));
       h->launches++;
+      bspmm_status_t st = check_validate_flag(h);
+      if (st != BSPMM_SUCCESS) return st;
     }
-    cublasSetStream(cb, h->stream);
-    for (int32_t ch = 0; ch < channels; ++ch) {
-      CK(h, cudaStreamWaitEvent(h->stream, h->ev_ch[ch], 0));
-      st = csr_impl(h, batch, k, row_off, sizes, row_ptr + (int64_t)ch * (N + 1), col, vals, U + (int64_t)ch * k, ldu,
-                    Y, ldy, false, bias ? bias + (int64_t)ch * k : nullptr, ch > 0 ? 1 : 0);
-      if (st != BSPMM_SUCCESS) {  // join the auxiliary stream before returning
-        CK(h, cudaStreamWaitEvent(h->stream, h->ev_ch[channels - 1], 0));
-        return st;
-      }
-    }
-    return BSPMM_SUCCESS;
   }
-  cublasStatus_t cs = cublasGemmStridedBatchedEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, W, CUDA_R_32F, k,
-                                                 (long long)n_x * k, X, CUDA_R_32F, (int)ldx, 0, &zero, U, CUDA_R_32F,
-                                                 (int)ldu, k, channels, ct, CUBLAS_GEMM_DEFAULT);
-  if (cs != CUBLAS_STATUS_SUCCESS && h->gcn_math != BSPMM_GCN_FP32)
-    return fail(h, BSPMM_ERROR_NOT_SUPPORTED, "cuBLAS rejected the reduced-precision GEMM");
-  if (cs != CUBLAS_STATUS_SUCCESS)  // emulation unavailable in the loaded cuBLAS: plain fp32
-    cs = cublasGemmStridedBatchedEx(cb, CUBLAS_OP_N, CUBLAS_OP_N, k, (int)N, n_x, &one, W, CUDA_R_32F, k,
-                                    (long long)n_x * k, X, CUDA_R_32F, (int)ldx, 0, &zero, U, CUDA_R_32F, (int)ldu,
-                                    k, channels, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-  if (cs != CUBLAS_STATUS_SUCCESS) return fail(h, BSPMM_ERROR_CUDA, "cuBLAS GEMM failed");
+  GcnPlan L;
+  if (!plan_gcn(channels, n_x, k, N, h->hint_rows, h->smem_optin, h->gcn_math, &L))
+    return fail(h, BSPMM_ERROR_NOT_SUPPORTED, "bspmm_gcn_layer: no shared-memory plan for these sizes");
+  // X needs a 16-byte row pitch and base for TMA; otherwise a packed copy
+  const bool x_ok = (ldx % 4 == 0) && aligned16(X);
+  const int64_t ldxp = x_ok ? ldx : (n_x + 3) / 4 * 4;
+  // workspace: [Wt_hi k x ktot][Wt_lo k x ktot (3xTF32)][gfirst tiles_m][packed X]
+  const size_t wt_bytes = al256((size_t)k * L.ktot * 4);
+  const size_t o_hi = 0, o_lo = wt_bytes, o_gf = o_lo + (h->gcn_math == BSPMM_GCN_FP32 ? wt_bytes : 0);
+  const size_t o_x = o_gf + al256((size_t)L.tiles_m * 4);
+  const size_t bytes = o_x + (x_ok ? 0 : al256((size_t)N * ldxp * 4));
+  bspmm_status_t st = grow(h, &h->gcn_ws, &h->gcn_ws_bytes, bytes);
+  if (st != BSPMM_SUCCESS) return st;
+  char* wsb = static_cast<char*>(h->gcn_ws);
+  float* whi = reinterpret_cast<float*>(wsb + o_hi);
+  float* wlo = h->gcn_math == BSPMM_GCN_FP32 ? reinterpret_cast<float*>(wsb + o_lo) : whi;
+  int32_t* gfirst = reinterpret_cast<int32_t*>(wsb + o_gf);
+  const float* Xk = x_ok ? X : reinterpret_cast<const float*>(wsb + o_x);
+  CUtensorMap mx, mhi, mlo;
+  if (!encode_2d(&mx, Xk, (uint64_t)n_x, (uint64_t)N, (uint64_t)ldxp * 4, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_2d(&mhi, whi, (uint64_t)L.ktot, (uint64_t)k, (uint64_t)L.ktot * 4, 32, (uint32_t)L.nt,
+                 CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_2d(&mlo, wlo, (uint64_t)L.ktot, (uint64_t)k, (uint64_t)L.ktot * 4, 32, (uint32_t)L.nt,
+                 CU_TENSOR_MAP_SWIZZLE_128B))
+    return fail(h, BSPMM_ERROR_CUDA, "bspmm_gcn_layer: TMA descriptor encoding failed");
+  if (!x_ok) {
+    CK(h, launch_gcn_pack_x(X, ldx, n_x, N, const_cast<float*>(Xk), ldxp, h->num_sms, h->stream));
+    h->launches++;
+  }
+  CK(h, launch_gcn_prep(L, batch, channels, n_x, k, N, h->gcn_math, W, bias, whi, wlo, row_off, gfirst, h->stream));
   h->launches++;
-  for (int32_t ch = 0; ch < channels; ++ch) {
-    st = csr_impl(h, batch, k, row_off, sizes, row_ptr + (int64_t)ch * (N + 1), col, vals, U + (int64_t)ch * k, ldu,
-                  Y, ldy, (h->flags & BSPMM_VALIDATE) != 0, bias ? bias + (int64_t)ch * k : nullptr, ch > 0 ? 1 : 0);
-    if (st != BSPMM_SUCCESS) return st;
-  }
+  GcnArgs a{batch, channels, n_x, k, h->gcn_math, N, row_off, sizes, row_ptr, col, vals, Xk, ldxp, Y, ldy, gfirst,
+            &mx, &mhi, &mlo};
+  CK(h, launch_gcn_fused(L, a, h->stream));
+  h->launches++;
   return BSPMM_SUCCESS;
 }
 

@@ -86,6 +86,38 @@ struct TileLayout {
 bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int32_t num_sms, int32_t cb_override,
                TileLayout* out);
 cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t s);
+// fused GCN layer on tcgen05 (gcn_fused.cu)
+struct GcnPlan {
+  int32_t KX, nxb, nbias, ktot, nt, ntiles_n, tiles_m, xr, cap_e;
+  int32_t ws, zs, xs, w_stage, z_stage, x_stage;
+  int32_t off_w, off_z, off_x, off_rp, off_col, off_val, off_rb, off_bar, smem;
+  uint32_t idesc;
+};
+struct GcnArgs {
+  int32_t batch, channels, n_x, k, mode;
+  int64_t N;
+  const int64_t* row_off;
+  const int32_t* sizes;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const float* vals;
+  const float* X;
+  int64_t ldx;
+  float* Y;
+  int64_t ldy;
+  const int32_t* gfirst;
+  const CUtensorMap* map_x;
+  const CUtensorMap* map_whi;
+  const CUtensorMap* map_wlo;
+};
+bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_rows, int32_t smem_optin, int32_t mode,
+              GcnPlan* out);
+cudaError_t launch_gcn_prep(const GcnPlan& L, int32_t batch, int32_t channels, int32_t n_x, int32_t k, int64_t N,
+                            int32_t mode, const float* W, const float* bias, float* whi, float* wlo,
+                            const int64_t* row_off, int32_t* gfirst, cudaStream_t s);
+cudaError_t launch_gcn_pack_x(const float* X, int64_t ldx, int32_t n_x, int64_t N, float* out, int64_t ldo,
+                              int32_t num_sms, cudaStream_t s);
+cudaError_t launch_gcn_fused(const GcnPlan& L, const GcnArgs& a, cudaStream_t s);
 // decoupled look-back scan state (persistent per handle; epoch-tagged, never reset per call)
 struct ScanState {
   uint32_t* flags;                 // [tiles] (epoch << 2) | {1: aggregate, 2: inclusive}
@@ -140,9 +172,8 @@ struct bspmm_handle_s {
   int64_t maps_ldb = 0;
   int32_t maps_k = 0, maps_kt = 0;
   bool maps_ok = false;
-  void* cublas = nullptr;  // cublasHandle_t, created on first bspmm_gcn_layer
-  void* gcn_ws = nullptr;  // U = X W_ch for all channels
-  int32_t gcn_math = 0;    // bspmm_set_gcn_math: 0 fp32, 1 TF32 tensor cores, 2 BF16 tensor cores
+  void* gcn_ws = nullptr;  // GCN layer: K-major split W, tile table, packed X
+  int32_t gcn_math = 0;    // bspmm_set_gcn_math: 0 fp32 (3xTF32), 1 TF32, 2 BF16-rounded operands
   size_t gcn_ws_bytes = 0;
   int64_t launches = 0;
   std::string err;
@@ -165,9 +196,5 @@ struct bspmm_handle_s {
   cudaStream_t s_aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_handoff = nullptr;  // bspmm_set_stream: new stream waits for the old one
-  // GCN layer: per-channel GEMM done-events (channel GEMMs on s_aux overlap
-  // the previous channel's SpMM on `stream`)
-  static constexpr int kGcnEvents = 16;
-  cudaEvent_t ev_ch[kGcnEvents] = {};
   cudaEvent_t ev[64] = {};
 };

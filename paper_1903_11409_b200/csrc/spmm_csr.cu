@@ -1110,8 +1110,6 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
     mbar_init(early_bar(p, smem), 1);  // the first unit's early B tile
     fence_mbar_init();
   }
-  // warm the TMA descriptor cache for the k-tiled staging path
-  if (p.tma2d && threadIdx.x >= 32 && threadIdx.x < 32 + kTmaMaps) prefetch_tensormap(&maps.m[threadIdx.x - 32]);
   __syncthreads();
   // programmatic dependent launch: everything above overlapped the previous
   // kernel (e.g. the offsets builder); global memory is touched only after this
@@ -1168,14 +1166,14 @@ static cudaError_t launch_e(int epi, const SpmmParams& sp, const TmaMaps& maps, 
     // per CTA on the device): the consumers start without the producer's
     // header and slice (an instantiation of its own; plain and GCN epilogues)
     const int32_t rows_per_round = ((plan.threads >> 5) - 1) * (32 / plan.lanes);
-    if (epi <= 1 && plan.units <= plan.grid && plan.tiles == 1 && !sp.sched && plan.max_rows <= rows_per_round &&
-        !(sp.dbg & (2 | 4 | 1024))) {
-      if (epi == 1) return launch_t<CH, VEC, 1, false, true>(sp, maps, plan, s);
+    if (epi == 0 && plan.units <= plan.grid && plan.tiles == 1 && !sp.sched && plan.max_rows <= rows_per_round &&
+        !(sp.dbg & (2 | 4 | 1024)))
       return launch_t<CH, VEC, 0, false, true>(sp, maps, plan, s);
-    }
   }
   if (epi == 2) return launch_t<CH, VEC, 2>(sp, maps, plan, s);
-  if (epi == 1) return launch_t<CH, VEC, 1>(sp, maps, plan, s);
+  // EPI 1 (the round-1 GCN bias / channel-accumulate epilogue) is no longer
+  // instantiated: the GCN layer runs in gcn_fused.cu
+  if (epi == 1) return cudaErrorInvalidValue;
   return launch_t<CH, VEC, 0>(sp, maps, plan, s);
 }
 

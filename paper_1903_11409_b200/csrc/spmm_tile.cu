@@ -423,8 +423,8 @@ cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t
   tp.dbg_bits = (a.dbg & 16) ? 1 : 0;
   static const TmaMaps no_maps{};
   const TmaMaps& m = a.maps ? *a.maps : no_maps;
-  const int epi = (a.bias != nullptr || a.accumulate != 0) ? 1 : 0;
-  return epi ? launch_tile_e<1>(tp, m, L, s) : launch_tile_e<0>(tp, m, L, s);
+  if (a.bias != nullptr || a.accumulate != 0) return cudaErrorInvalidValue;  // no GCN epilogue here (gcn_fused.cu)
+  return launch_tile_e<0>(tp, m, L, s);
 }
 
 }  // namespace bspmm

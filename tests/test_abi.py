@@ -164,3 +164,36 @@ def test_multimem_store_sass():
     plain = stores("_ZN5bspmm15spmm_csr_kernelILi2ELb1ELi0ELb0ELb0EE")
     assert mc == {"STG.E.128"}, mc
     assert plain == {"STG.E.EF.128"}, plain
+
+
+def test_gcn_sass_uses_tcgen05():
+    """The fused layer's kernel issues tensor-core MMAs (UTCHMMA), TMEM loads
+    (LDTM) and tensor TMA (UTMALDG) -- checked in the shipped library."""
+    import os
+    import subprocess
+    lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1903_11409_b200", "libbspmm.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
+    i = out.find("gcn_fused_kernel")
+    assert i >= 0
+    body = out[i:out.find("Function :", i + 20)]
+    for mnem in ("UTCHMMA", "LDTM", "UTMALDG", "UTCBAR"):
+        assert mnem in body, mnem
+
+
+def test_hot_kernels_do_not_spill():
+    """The CSR pipeline's plain-store instantiations (the bench path), the tile
+    kernel and the fused GCN kernel keep everything in registers: a code change
+    that makes them spill (a 19% C5 regression once, from one added prologue
+    line) fails here, on the CPU, before any GPU time is spent."""
+    import os
+    import re
+    import subprocess
+    lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1903_11409_b200",
+                       "libbspmm.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--dump-resource-usage", lib], capture_output=True,
+                         text=True).stdout
+    funcs = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+)", out)
+    hot = [(f, int(st)) for f, _, st in funcs
+           if re.search(r"spmm_csr_kernelILi[124]ELb1ELi0ELb0E", f) or "spmm_tile_kernel" in f or "gcn_fused" in f]
+    assert len(hot) >= 6, hot
+    assert all(st == 0 for _, st in hot), [f for f, st in hot if st]

@@ -5,8 +5,10 @@ Shapes follow ChemGCN: Tox21 weight width 64, Reaction100
 width 512, on Tox21-shaped molecule graphs (G-mol 20-60 nodes).  The paper
 does not state the channel count; 4 adjacency channels (bond types) are
 assumed here.  Timed with CUDA graphs (device time), compared with the same
-layer built from torch.matmul + bias add + our SpMM per channel + add (the
-paper's 3-per-channel launch structure, Fig. algo:graph_conv_batched).
+layer built from torch.matmul (cuBLAS, fp32 and TF32) + bias add + our SpMM
+per channel + add (the paper's 3-per-channel launch structure, Fig.
+algo:graph_conv_batched).  The fused layer is bspmm_gcn_layer: a preparation
+launch + one tcgen05 launch (csrc/gcn_fused.cu).
 """
 import json
 import os
@@ -83,6 +85,9 @@ def main():
         h.set_gcn_math("fp32")
         t_fused = time_calls(h, reps, R, fused) * 1e3
         t_unf = time_calls(h, reps, R, unfused) * 1e3
+        torch.backends.cuda.matmul.allow_tf32 = True        # the same composition with cuBLAS TF32 GEMMs
+        t_unf_tf32 = time_calls(h, reps, R, unfused) * 1e3
+        torch.backends.cuda.matmul.allow_tf32 = False
         gemm_flops = 2.0 * b.n_rows * width * width * channels
         spmm_flops = 2.0 * len(col) * width
         print(json.dumps({"shape": name, "batch": batch, "rows": b.n_rows, "width": width, "channels": channels,
@@ -90,7 +95,8 @@ def main():
                           "fused_TFLOPs": (gemm_flops + spmm_flops) / t_fused / 1e6,
                           "fused_tf32_us": t_modes["tf32"], "fused_bf16_us": t_modes["bf16"],
                           "fused_tf32_TFLOPs": (gemm_flops + spmm_flops) / t_modes["tf32"] / 1e6,
-                          "launches_fused": 1 + channels, "launches_unfused": 3 * channels + 2}), flush=True)
+                          "unfused_tf32_us": t_unf_tf32, "launches_fused": 2, "launches_unfused": 3 * channels + 2}),
+              flush=True)
 
 
 if __name__ == "__main__":
