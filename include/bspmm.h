@@ -28,10 +28,10 @@
  *    workspace (grown on demand, freed by bspmm_destroy), one internal
  *    non-blocking auxiliary stream and its events (created with the handle, so
  *    calls can be captured into a CUDA graph on first use), and BORROWS the
- *    stream given to bspmm_create / bspmm_set_stream.  bspmm_csr_backward and
- *    bspmm_gcn_layer fork work onto the auxiliary stream and join it back into
- *    the caller's stream before returning (also on error), so to the caller
- *    every call is ordered on its stream.
+ *    stream given to bspmm_create / bspmm_set_stream.  bspmm_csr_backward
+ *    forks work onto the auxiliary stream and joins it back into the caller's
+ *    stream before returning (also on error), so to the caller every call is
+ *    ordered on its stream.
  *  - Handle state (workspace, scan state, error flag) is shared by the calls
  *    of a handle: when bspmm_set_stream changes the stream, the new stream is
  *    made to wait for all work enqueued so far on the previous one (the
@@ -233,14 +233,15 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
                                    int64_t total_rows, int64_t total_nnz, int32_t* csr_row_ptr_out,
                                    int32_t* csr_col_out, float* csr_val_out);
 
-/* Arithmetic of the dense X W_ch GEMM in bspmm_gcn_layer (the SpMM part is
- * always fp32):
- *  BSPMM_GCN_FP32 (default) fp32-accurate (BF16x9 tensor-core emulation when
- *                 the loaded cuBLAS offers it, else CUDA-core fp32);
- *  BSPMM_GCN_TF32 tensor cores, inputs rounded to TF32 (10-bit mantissa);
- *  BSPMM_GCN_BF16 tensor cores, inputs rounded to BF16 (7-bit mantissa).
- * Errors: INVALID_VALUE (unknown mode); a rejected mode surfaces as
- * NOT_SUPPORTED from bspmm_gcn_layer. */
+/* Arithmetic of the tensor-core GEMM in bspmm_gcn_layer (the SpMM part,
+ * Z = A_ch X, is always fp32 FMA in storage order):
+ *  BSPMM_GCN_FP32 (default) 3xTF32: both operands split into a TF32 head and
+ *                 an fp32 remainder, three tcgen05 MMAs per step
+ *                 (head.head + head.rem + rem.head): fp32-accurate;
+ *  BSPMM_GCN_TF32 one MMA on the fp32 values (TF32 inputs, 10-bit mantissa);
+ *  BSPMM_GCN_BF16 one MMA on operands rounded to BF16 (7-bit mantissa), run
+ *                 on the TF32 datapath (BF16 values are exact in TF32).
+ * Errors: INVALID_VALUE (unknown mode). */
 #define BSPMM_GCN_FP32 0
 #define BSPMM_GCN_TF32 1
 #define BSPMM_GCN_BF16 2
@@ -254,15 +255,18 @@ BSPMM_API bspmm_status_t bspmm_set_gcn_math(bspmm_handle_t h, int32_t mode);
  *  row_ptr [channels][total_rows + 1] dev int32: one block-diagonal CSR per
  *         channel (channel-specific adjacency), absolute positions into the
  *         shared col / vals arrays; col LOCAL ids.
- *  Y      [total_rows x ldy] dev fp32 (overwritten).
- * U_ch = X W_ch is computed into handle workspace (total_rows x channels x k
- * floats), then one SpMM per channel folds the bias (as rowsum(A) * bias)
- * and the channel sum into its epilogue.  For 2..16 channels (and no
- * VALIDATE) the channel GEMMs run one per channel on the handle's auxiliary
- * stream and SpMM_ch waits only for GEMM_ch (GEMM_{ch+1} overlaps SpMM_ch;
- * forked from and joined back into the caller's stream within the call, valid
- * under graph capture); otherwise one strided-batched GEMM precedes the
- * channel SpMMs on the caller's stream. */
+ *  Y      [total_rows x ldy] dev fp32 (overwritten; padding rows untouched).
+ * Computed as ONE tensor-core GEMM per 128-row x (<=128)-feature output tile
+ * through the exact identity Y = [A_1 X | ... | A_C X | r_1..r_C] .
+ * [W_1; ...; W_C; b_1^T; ...; b_C^T] (r_ch = rowsum A_ch): the left operand
+ * is produced in shared memory by the SpMM row loop (never in HBM), the
+ * channel sum and the bias are part of the TMEM accumulation (csrc/
+ * gcn_fused.cu).  Two launches: a preparation kernel (W to K-major, split for
+ * 3xTF32; tile table) and the fused kernel.  Handle workspace: 2 x k x
+ * (channels * ceil32(n_x) + 32 ceil(channels/32)) floats + one int per 128
+ * rows (+ a packed copy of X when ldx % 4 != 0 or X is not 16-byte aligned).
+ * Errors: INVALID_VALUE, NOT_SUPPORTED (total_rows >= 2^31), CUDA, INDEX
+ * (VALIDATE). */
 BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_t channels, int32_t n_x, int32_t k,
                                          const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
                                          const int32_t* col, const float* vals, const float* X, int64_t ldx,

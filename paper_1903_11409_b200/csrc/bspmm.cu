@@ -319,7 +319,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 131071) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 1048575) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -676,7 +676,7 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
   }
   CK(h, launch_gcn_prep(L, batch, channels, n_x, k, N, h->gcn_math, W, bias, whi, wlo, row_off, gfirst, h->stream));
   h->launches++;
-  GcnArgs a{batch, channels, n_x, k, h->gcn_math, N, row_off, sizes, row_ptr, col, vals, Xk, ldxp, Y, ldy, gfirst,
+  GcnArgs a{batch, channels, n_x, k, h->gcn_math, (h->dbg >> 17) & 3, N, row_off, sizes, row_ptr, col, vals, Xk, ldxp, Y, ldy, gfirst,
             &mx, &mhi, &mlo};
   CK(h, launch_gcn_fused(L, a, h->stream));
   h->launches++;

@@ -61,6 +61,7 @@ struct GcnParams {
   int32_t w_stage, z_stage, x_stage;  // bytes per stage
   int32_t off_w, off_z, off_x, off_rp, off_col, off_val, off_rb, off_bar;
   uint32_t idesc;
+  int32_t dbg;                    // timing experiments: 1 = no Z arithmetic, 2 = no MMAs (results undefined)
   const int64_t* __restrict__ row_off;
   const int32_t* __restrict__ sizes;
   const int32_t* __restrict__ row_ptr;  // [channels][N + 1]
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
         const uint64_t zh = smem_desc_sw128(zs), wh = smem_desc_sw128(ws);
         const uint64_t zl = smem_desc_sw128(zs + kGM * 128), wl = smem_desc_sw128(ws + (size_t)p.nt * 128);
 #pragma unroll
-        for (int j = 0; j < kGK / 8; ++j) {  // UMMA_K = 8 tf32 = 32 bytes: +2 in the 16-byte address field
+        for (int j = 0; j < kGK / 8 && !(p.dbg & 2); ++j) {  // UMMA_K = 8 tf32 = 32 bytes: +2 in the 16-byte address field
           mma_tf32(d, zh + 2 * j, wh + 2 * j, p.idesc, (kb | j) != 0);
           if (p.mode == 0) {
             mma_tf32(d, zh + 2 * j, wl + 2 * j, p.idesc, 1u);
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
         float z[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) z[c] = 0.f;
-        if (rb >= 0) {
+        if (rb >= 0 && !(p.dbg & 1)) {
           int32_t e, e1;
           row_range(ch, e, e1);
           for (; e < e1; ++e) {
@@ -605,6 +606,7 @@ cudaError_t launch_gcn_fused(const GcnPlan& L, const GcnArgs& a, cudaStream_t s)
   p.off_rb = L.off_rb;
   p.off_bar = L.off_bar;
   p.idesc = L.idesc;
+  p.dbg = a.dbg;
   p.row_off = a.row_off;
   p.sizes = a.sizes;
   p.row_ptr = a.row_ptr;

@@ -32,10 +32,13 @@ inline int32_t pow2_ceil(int32_t x) {
 }
 BSPMM_HD inline int32_t align_up(int32_t x, int32_t a) { return (x + a - 1) / a * a; }
 
-// smem carve-up shared by planner and kernel: [hdr S*32][full S*8][empty S*8] pad 128, then stages
-// per stage: header + "full" + "empty" barriers; then one barrier for the
-// first unit's early B tile (spmm_csr.cu early_b)
-BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stages * (kHdrBytes + 16) + 8, 128); }
+// smem carve-up shared by planner and kernel: [hdr S*32][full S*8][empty S*8]
+// [early 8][sfull S*8] pad 128, then stages.  Per stage: header + "full" +
+// "empty" barriers; one barrier for the first unit's early B tile
+// (spmm_csr.cu early_b); per stage a "slice full" barrier (fused COO mode: the
+// raw SparseTensor slice lands on its own barrier, so its conversion overlaps
+// the B tile's landing)
+BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stages * (kHdrBytes + 24) + 8, 128); }
 
 // planner (plan.cpp)
 bspmm_status_t make_plan(int32_t k, int32_t batch, bool aligned, int32_t max_rows, int64_t max_nnz,
@@ -94,7 +97,7 @@ struct GcnPlan {
   uint32_t idesc;
 };
 struct GcnArgs {
-  int32_t batch, channels, n_x, k, mode;
+  int32_t batch, channels, n_x, k, mode, dbg;
   int64_t N;
   const int64_t* row_off;
   const int32_t* sizes;

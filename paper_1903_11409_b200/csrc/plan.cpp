@@ -61,7 +61,8 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   auto a16 = [](int64_t x) { return (x + 15) / 16 * 16; };
   int64_t s_need = 2 * a16(16 + 4 * Zc) + a16(16 + 4 * (R + 1));
   if (coo)  // fused COO mode (spmm_csr.cu coo_stage_bytes): + raw pairs, raw values, cursors, slots
-    s_need = a16(s_need) + a16(8 * (Zc + 1)) + a16(4 * (Zc + 3)) + a16(4 * (R + 1)) + a16(4 * Zc);
+    s_need = a16(s_need) + a16(8 * (Zc + 1)) + a16(4 * (Zc + 3)) + a16(4 * (R + 1)) +
+             a16(4 * std::max<int64_t>(Zc, (R + 31) / 32));
   int64_t s_bytes64 = align_up((int32_t)s_need, 128);
   auto stages_in = [&](int32_t kt_, int32_t budget_) {
     int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 128);

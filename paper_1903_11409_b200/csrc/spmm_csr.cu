@@ -126,7 +126,9 @@ __host__ __device__ __forceinline__ int64_t coo_raw_off(int64_t nnz, int64_t n) 
 __host__ __device__ __forceinline__ int64_t coo_pairs_bytes(int64_t nnz) { return al16(8 * (nnz + 1)); }
 __host__ __device__ __forceinline__ int64_t coo_vals_bytes(int64_t nnz) { return al16(4 * (nnz + 3)); }
 __host__ __device__ __forceinline__ int64_t coo_stage_bytes(int64_t nnz, int64_t n) {
-  return coo_raw_off(nnz, n) + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz) + al16(4 * (n + 1)) + al16(4 * nnz);
+  // ... + cursors [n + 1] + slots [max(nnz, 32-row chunks)] (the chunk totals of the row scan live there first)
+  return coo_raw_off(nnz, n) + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz) + al16(4 * (n + 1)) +
+         al16(4 * (nnz > (n + 31) / 32 ? nnz : (n + 31) / 32));
 }
 
 // trace slots per CTA (bspmm_set_trace): 0 entry, 1 after PDL wait, 2 producer has unit-0 row
@@ -289,6 +291,10 @@ __device__ __forceinline__ void meta_rt2(const SpmmParams& p, int64_t uu, Meta& 
 __device__ __forceinline__ uint64_t* early_bar(const SpmmParams& p, unsigned char* smem) {
   return reinterpret_cast<uint64_t*>(smem + p.stages * (kHdrBytes + 16));
 }
+// fused COO mode: per-stage barrier of the raw slice (+ header)
+__device__ __forceinline__ uint64_t* sfull_bar(const SpmmParams& p, unsigned char* smem) {
+  return reinterpret_cast<uint64_t*>(smem + p.stages * (kHdrBytes + 16) + 8);
+}
 template <bool VEC, bool COO>
 __device__ __forceinline__ bool early_b_ok(const SpmmParams& p, int32_t n, int32_t kw) {
   // whole contiguous B_i only (one 1-D bulk copy): with k-tiles (2-D boxes) it
@@ -342,7 +348,8 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
     unsigned char* st = ring + (size_t)s * stage_bytes;
     const float* bsrc = p.B + g0 * p.ldb + c0;
     unsigned char* sreg = st + p.stage_b;
-    if (COO) {  // fused COO mode: B tile + the raw SparseTensor slice
+    if (COO) {  // fused COO mode: B tile (on full[s]) + the raw SparseTensor slice (on sfull[s])
+      uint64_t* sfull = sfull_bar(p, smem);
       const bool fits = (int64_t)n * kw * 4 <= p.stage_b && coo_stage_bytes(nnz, n) <= p.stage_s;
       if (fits && n > 0) {
         if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)n * (uint32_t)kw * 4u);
@@ -391,9 +398,10 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
         h.g0 = g0; h.n = n; h.nz0 = nz0; h.nnz = nnz; h.c0 = c0; h.kw = kw;
         h.flags = fits ? 3 : 4;
         hdr[s] = h;
+        mbar_arrive(&sfull[s]);
         mbar_arrive(&full[s]);
       }
-      cp_async_arrive_noinc(&full[s]);
+      cp_async_arrive_noinc(&sfull[s]);
       return;
     }
     // a unit is staged whole (tile + structure) or not at all (read from global memory)
@@ -525,11 +533,13 @@ __device__ __forceinline__ void issue_done(const SpmmParams& p, unsigned char* s
   const int lane = threadIdx.x & 31;
   const int s = j % p.stages;
   mbar_wait(&empty[s], ((uint32_t)(j / p.stages) & 1u) ^ 1u);
+  uint64_t* sfull = sfull_bar(p, smem);
   if (lane == 0) {
     hdr[s].flags = -1;
+    if (p.nnz_off) mbar_arrive(&sfull[s]);
     mbar_arrive(&full[s]);
   }
-  cp_async_arrive_noinc(&full[s]);
+  cp_async_arrive_noinc(p.nnz_off ? &sfull[s] : &full[s]);
 }
 
 template <bool VEC, bool COO>
@@ -964,7 +974,8 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
 // (named barrier 1); writes the standard CSR slice layout of the stage.
 __device__ __forceinline__ void consumer_bar(int T) { asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory"); }
 
-__device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& h, unsigned char* st, int t, int T) {
+__device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& h, unsigned char* st, int t, int T,
+                                            bool tr) {
   unsigned char* sreg = st + p.stage_b;
   const int32_t nnz = h.nnz, n = h.n, z0 = h.nz0;
   unsigned char* raw = sreg + coo_raw_off(nnz, n);
@@ -979,28 +990,42 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
   consumer_bar(T);
   for (int32_t e = t; e < nnz; e += T) atomicAdd(&cursor[pr[e].x], 1);
   consumer_bar(T);
-  if (t < 32) {  // exclusive scan of the row counts by the first consumer warp
-    int32_t carry = 0;
-    for (int32_t base = 0; base < n; base += 32) {
-      const int32_t r = base + t;
-      const int32_t v = r < n ? cursor[r] : 0;
-      int32_t x = v;
+  if (tr && t == 0) BSPMM_TRACE(p, 28);
+  // exclusive scan of the row counts: every consumer warp scans 32-row
+  // chunks, chunk totals go to `slot` (free until the scatter), then each
+  // thread adds the totals of the chunks before its own
+  const int32_t nchunk = (n + 31) >> 5;
+  const int lt = t & 31;
+  for (int32_t c = t >> 5; c < nchunk; c += T >> 5) {
+    const int32_t r = c * 32 + lt;
+    const int32_t v = r < n ? cursor[r] : 0;
+    int32_t x = v;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
-        if (t >= d) x += y;
-      }
-      if (r < n) {
-        cursor[r] = carry + x - v;
-        rp[r] = z0 + carry + x - v;
-      }
-      carry += __shfl_sync(0xffffffffu, x, 31);
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lt >= d) x += y;
     }
-    if (t == 0) rp[n] = z0 + nnz;
+    if (r < n) cursor[r] = x - v;                      // exclusive within the chunk
+    if (lt == 31) slot[c] = x;                         // chunk total
   }
   consumer_bar(T);
+  for (int32_t c = t >> 5; c < nchunk; c += T >> 5) {
+    int32_t base = 0;
+    for (int32_t q = lt; q < c; q += 32) base += slot[q];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) base += __shfl_xor_sync(0xffffffffu, base, d);
+    const int32_t r = c * 32 + lt;
+    if (r < n) {
+      cursor[r] += base;
+      rp[r] = z0 + cursor[r];
+    }
+  }
+  if (t == 0) rp[n] = z0 + nnz;
+  consumer_bar(T);
+  if (tr && t == 0) BSPMM_TRACE(p, 29);
   for (int32_t e = t; e < nnz; e += T) slot[atomicAdd(&cursor[pr[e].x], 1)] = e;
   consumer_bar(T);
+  if (tr && t == 0) BSPMM_TRACE(p, 30);
   for (int32_t q = t; q < nnz; q += T) {
     const int32_t e = slot[q];
     const int2 rc = pr[e];
@@ -1015,6 +1040,7 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
     val[s0 + rank] = rv[e];  // bitwise move
   }
   consumer_bar(T);
+  if (tr && t == 0) BSPMM_TRACE(p, 31);
 }
 
 template <int CH, bool VEC, int EPI, bool COO, bool ONE>
@@ -1065,14 +1091,20 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
   }
   for (int j = j0;; ++j) {
     const int s = j % p.stages;
-    mbar_wait(&full[s], (uint32_t)(j / p.stages) & 1u);
+    const uint32_t par = (uint32_t)(j / p.stages) & 1u;
+    // fused COO mode: the slice (and header) first; its conversion overlaps
+    // the B tile's landing, waited for below
+    mbar_wait(COO ? &sfull_bar(p, const_cast<unsigned char*>(smem))[s] : &full[s], par);
     if (j == 0 && cw == 0 && lane == 0) BSPMM_TRACE(p, 5);
     const UnitHdr h = hdr[s];
     if (h.flags < 0) break;  // the producer's "done" header
     if (j == 0 && (h.flags & 8)) mbar_wait(early_bar(p, const_cast<unsigned char*>(smem)), 0u);  // early B tile
     const unsigned char* st = ring + (size_t)s * stage_bytes;
-    if (COO && (h.flags & 3) == 3)  // fused COO mode: SparseTensor slice -> CSR slice in shared memory
-      coo_convert(p, h, const_cast<unsigned char*>(st), threadIdx.x - 32, W * 32);
+    if (COO) {
+      if ((h.flags & 3) == 3)  // SparseTensor slice -> CSR slice in shared memory
+        coo_convert(p, h, const_cast<unsigned char*>(st), threadIdx.x - 32, W * 32, j == 0);
+      mbar_wait(&full[s], par);
+    }
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
     for (int rep = 0; rep < reps && (h.flags & 4) == 0; ++rep) {  // 4: COO unit over capacity (skipped, flagged)
       if (EPI == 3) {  // SDDMM mode (NEXT-2)
@@ -1104,7 +1136,10 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
   if (threadIdx.x == 0) {
     const uint32_t W = (blockDim.x >> 5) - 1;
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1 + 32);  // producer lane-0 arrive + 32 cp.async arrivals
+      // producer lane-0 arrive + 32 cp.async arrivals; fused COO mode: the
+      // cp.async arrivals go to the slice barrier, full[s] tracks the B tile
+      mbar_init(&full[s], COO ? 1 : 1 + 32);
+      if (COO) mbar_init(&sfull_bar(p, smem)[s], 1 + 32);
       mbar_init(&empty[s], W);      // one arrival per consumer warp
     }
     mbar_init(early_bar(p, smem), 1);  // the first unit's early B tile

@@ -39,17 +39,56 @@ def main():
         Ca = h.coo_atomic(ro, None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B))
         torch.cuda.synchronize()
         assert torch.equal(C, C2) and torch.equal(C, Cf) and torch.equal(C, Cm)
-    # C4: whole-row units (1-D bulk B tiles of 100 KB), and the GCN layer
+    # C4: the small-batch tile kernel (2-D TMA and cp.async staging, every
+    # column block), the pipeline's whole-row units (1-D bulk B tiles of 100 KB)
     b = synth.config(4)
     h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    dbg0 = int(sys.argv[1]) if len(sys.argv) > 1 else 0
     C4 = h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
+    for cb in (1, 8, 32):
+        for d in (0, 32768):
+            h.set_tile_cb(cb)
+            h.set_debug(dbg0 | d)
+            Ct = h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
+            Cs = h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
+            torch.cuda.synchronize()
+            assert torch.equal(C4, Ct) and torch.equal(C4, Cs)
+    h.set_tile_cb(0)
+    h.set_debug(dbg0 | 16384)
+    Cp = h.csr(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
+    torch.cuda.synchronize()
+    assert torch.equal(C4, Cp)
+    h.set_debug(dbg0)
+    # the fused tcgen05 GCN layer: every precision mode, a packed-X leading
+    # dimension, 33 channels (structure from global memory), a large graph
+    # (X halo from global memory)
     b = synth.config(2)
     h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
-    X = torch.randn((b.n_rows, 32), device=dev)
-    W = torch.randn((2, 32, b.k), device=dev)
-    bias = torch.randn((2, b.k), device=dev)
     rps = torch.stack([T(b.row_ptr), T(b.row_ptr)])
-    h.gcn_layer(T(b.row_off), None, rps, T(b.col), T(b.vals), X, W, bias)
+    for n_x, ld in ((32, 32), (37, 41)):
+        X = torch.randn((b.n_rows, ld), device=dev)[:, :n_x]
+        W = torch.randn((2, n_x, b.k), device=dev)
+        bias = torch.randn((2, b.k), device=dev)
+        for mode in ("fp32", "tf32", "bf16"):
+            h.set_gcn_math(mode)
+            h.gcn_layer(T(b.row_off), None, rps, T(b.col), T(b.vals), X, W, bias)
+    h.set_gcn_math("fp32")
+    X = torch.randn((b.n_rows, 16), device=dev)
+    h.gcn_layer(T(b.row_off), None, torch.stack([T(b.row_ptr)] * 33), T(b.col), T(b.vals), X,
+                torch.randn((33, 16, 48), device=dev), torch.randn((33, 48), device=dev))
+    bl = synth.generate(synth.MIX, (300, 400, 1, 5), 3, 8, seed=9, dense=False)
+    h.set_hints(0, 0)
+    h.gcn_layer(T(bl.row_off), None, T(bl.row_ptr[None]), T(bl.col), T(bl.vals),
+                torch.randn((bl.n_rows, 40), device=dev), torch.randn((1, 40, 72), device=dev))
+    torch.cuda.synchronize()
+    # handle state across two streams (set_stream hand-off)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    b = synth.config(3)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    with torch.cuda.stream(s1):
+        h.csr_backward(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), T(b.B))
+    with torch.cuda.stream(s2):
+        h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B))
     torch.cuda.synchronize()
     del C4
     # backward of a streaming batch (standalone SDDMM kernel: > 8 matrices per SM)

@@ -21,6 +21,7 @@ SLOTS = ["entry", "after_pdl_wait", "prod_rowoff", "prod_struct_off", "prod_done
          "cons_done", "exit", "cons_unit0_done", "p0_after_empty", "p0_after_tma", "p0_before_arrive",
          "p1_before_arrive", "p0_after_arrive", "p1_after_arrive", "early_b_issued"]
 SLOTS += [f"u{j}_{w}" for j in range(3) for w in ("empty_ok", "slice_issued", "tma_issued", "copies_issued")]
+SLOTS += ["coo_hist", "coo_scan", "coo_scatter", "coo_rank"]  # fused COO conversion of a CTA's first unit
 # the small-batch tile kernel (spmm_tile.cu, plan kernel == 1)
 TILE_SLOTS = ["entry", "after_pdl_wait", "rt1_done", "b_issued", "struct_staged", "b_landed", "done"]
 
@@ -53,9 +54,10 @@ def main():
     ap.add_argument("--dbg", type=int, default=0, help="debug bits (bspmm_set_debug)")
     ap.add_argument("--warm", action="store_true", help="no L2 flush before the traced launch")
     ap.add_argument("--sizes", action="store_true", help="row_off = None (offsets fused into the launch)")
+    ap.add_argument("--coo", action="store_true", help="trace the fused COO launch (bspmm_coo with hints)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    b = synth.config(args.config)
+    b = synth.config(args.config, coo=args.coo)
     T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     h = bs.Handle(0)
     h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
@@ -63,9 +65,14 @@ def main():
     ro, rp, col, vals, B = T(b.row_off), T(b.row_ptr), T(b.col), T(b.vals), T(b.B)
     sz = T(b.sizes)
     C = torch.empty((b.n_rows, b.k), device=dev)
-    h.csr(ro, None, rp, col, vals, B, C)
+    def call():
+        if args.coo:
+            h.coo(ro, None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), B, C)
+        else:
+            h.csr(ro, None, rp, col, vals, B, C)
+    call()
     h.set_debug(args.dbg | (1 if args.nostore else 0))
-    h.csr(ro, None, rp, col, vals, B, C)
+    call()
     grid = h.last_plan()["grid"]
     buf = torch.zeros((grid, 32), dtype=torch.int64, device=dev)
     flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device=dev)
@@ -77,7 +84,9 @@ def main():
         h.set_trace(buf)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        if args.sizes:
+        if args.coo:
+            h.coo(ro, None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), B, C)
+        elif args.sizes:
             h.csr(None, sz, rp, col, vals, B, C)
         else:
             h.csr(ro, None, rp, col, vals, B, C)
