@@ -49,6 +49,7 @@ constexpr int kGK = 32;           // K per block: 32 x 4 B = one 128-byte swizzl
 constexpr int kGThreads = 192;    // warp 0 TMA, warp 1 MMA, warps 2-5 math
 constexpr int kGMath = 4;         // math warps
 constexpr int kXBox = 64;         // rows per X TMA box
+constexpr int kZCol = 128;        // first TMEM column of the Z stages (after the accumulator)
 
 struct GcnParams {
   int32_t batch, channels, n_x, k;
@@ -108,7 +109,9 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
   int32_t* rp_s = reinterpret_cast<int32_t*>(smem + p.off_rp);    // [channels][129] staged entry index
   int32_t* col_s = reinterpret_cast<int32_t*>(smem + p.off_col);
   float* val_s = reinterpret_cast<float*>(smem + p.off_val);
-  const uint32_t tmem_cols = p.nt <= 32 ? 32u : (p.nt <= 64 ? 64u : (p.nt <= 128 ? 128u : 256u));
+  // TMEM: accumulator columns [0, nt), Z stages from column kZCol (hi, then lo
+  // in 3xTF32), 32 columns of fp32 each; the whole 512 columns (1 CTA per SM)
+  const uint32_t tmem_cols = 512u;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.ws; ++s) mbar_init(&w_full[s], 1), mbar_init(&w_empty[s], 1);
@@ -250,15 +253,14 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
         mbar_wait(&z_full[zsi], zph);
         tc_fence_after();
         unsigned char* ws = smem + p.off_w + (size_t)wsi * p.w_stage;
-        unsigned char* zs = smem + p.off_z + (size_t)zsi * p.z_stage;
-        const uint64_t zh = smem_desc_sw128(zs), wh = smem_desc_sw128(ws);
-        const uint64_t zl = smem_desc_sw128(zs + kGM * 128), wl = smem_desc_sw128(ws + (size_t)p.nt * 128);
+        const uint64_t wh = smem_desc_sw128(ws), wl = smem_desc_sw128(ws + (size_t)p.nt * 128);
+        const uint32_t zh = d + kZCol + (uint32_t)zsi * (p.mode == 0 ? 64u : 32u), zl = zh + 32u;
 #pragma unroll
-        for (int j = 0; j < kGK / 8 && !(p.dbg & 2); ++j) {  // UMMA_K = 8 tf32 = 32 bytes: +2 in the 16-byte address field
-          mma_tf32(d, zh + 2 * j, wh + 2 * j, p.idesc, (kb | j) != 0);
+        for (int j = 0; j < kGK / 8 && !(p.dbg & 2); ++j) {  // UMMA_K = 8: 8 TMEM columns of A, +32 bytes of B
+          mma_tf32_ts(d, zh + 8 * j, wh + 2 * j, p.idesc, (kb | j) != 0);
           if (p.mode == 0) {
-            mma_tf32(d, zh + 2 * j, wl + 2 * j, p.idesc, 1u);
-            mma_tf32(d, zl + 2 * j, wh + 2 * j, p.idesc, 1u);
+            mma_tf32_ts(d, zh + 8 * j, wl + 2 * j, p.idesc, 1u);
+            mma_tf32_ts(d, zl + 8 * j, wh + 2 * j, p.idesc, 1u);
           }
         }
         mma_commit(&w_empty[wsi]);
@@ -275,9 +277,10 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     // :196-207), reading whole 128-byte X rows (swizzled like the operand
     // tiles) and writing one 128-byte swizzled row of Z -- no cross-lane
     // dependence, all loads of an entry in flight at once
-    const int mw = warp - 2;
-    const int r = mw * 32 + lane;
+    const int q = warp & 3;      // the TMEM lane quarter this warp may access
+    const int r = q * 32 + lane;  // its row (= TMEM lane) of the tile
     const int32_t rb = rbase[r];
+    const uint32_t tq = s_tmem + ((uint32_t)(q * 32) << 16);
     int zsi = 0, xsi = 0;
     uint32_t zph = 0, xph = 0;
     auto row_range = [&](int32_t ch, int32_t& e0, int32_t& e1) {
@@ -290,33 +293,33 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
         e1 = rp[1];
       }
     };
-    auto put_row = [&](unsigned char* zh, unsigned char* zl, const float (&z)[32]) {
+    // Z row -> TMEM stage zsi (hi = TF32 truncation, lo = the fp32 remainder in
+    // 3xTF32; BF16 mode: rounded to BF16), then make it visible to the MMA
+    auto put_row = [&](int zsi_, float (&z)[32]) {
+      const uint32_t col = kZCol + (uint32_t)zsi_ * (p.mode == 0 ? 64u : 32u);
+      if (p.mode == 0) {
+        float lo[32];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t off = (uint32_t)r * 128u + ((uint32_t)(j ^ (r & 7)) << 4);
-        float4 v = make_float4(z[4 * j], z[4 * j + 1], z[4 * j + 2], z[4 * j + 3]);
-        if (p.mode == 0) {
-          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          *reinterpret_cast<float4*>(zh + off) = h;
-          *reinterpret_cast<float4*>(zl + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-        } else {
-          if (p.mode == 2) {
-            v.x = __bfloat162float(__float2bfloat16_rn(v.x));
-            v.y = __bfloat162float(__float2bfloat16_rn(v.y));
-            v.z = __bfloat162float(__float2bfloat16_rn(v.z));
-            v.w = __bfloat162float(__float2bfloat16_rn(v.w));
-          }
-          *reinterpret_cast<float4*>(zh + off) = v;
+        for (int c = 0; c < 32; ++c) {
+          const float h = tf32_hi(z[c]);
+          lo[c] = z[c] - h;
+          z[c] = h;
         }
+        tmem_st32(tq + col + 32u, lo);
+      } else if (p.mode == 2) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) z[c] = __bfloat162float(__float2bfloat16_rn(z[c]));
       }
+      tmem_st32(tq + col, z);
+      tmem_wait_st();
+      tc_fence_before();
     };
     for (int32_t xb = 0; xb < p.nxb; ++xb) {
       mbar_wait(&x_full[xsi], xph);
       const unsigned char* xs = smem + p.off_x + (size_t)xsi * p.x_stage;
       for (int32_t ch = 0; ch < p.channels; ++ch) {
         mbar_wait(&z_empty[zsi], zph ^ 1u);
-        unsigned char* zh = smem + p.off_z + (size_t)zsi * p.z_stage;
-        unsigned char* zl = zh + kGM * 128;
+        tc_fence_after();
         float z[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) z[c] = 0.f;
@@ -343,8 +346,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
             }
           }
         }
-        put_row(zh, zl, z);
-        fence_proxy_async_smem();
+        put_row(zsi, z);
         __syncwarp();
         if (lane == 0) mbar_arrive(&z_full[zsi]);
         if (++zsi == p.zs) zsi = 0, zph ^= 1u;
@@ -355,8 +357,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     }
     for (int32_t j = 0; j < p.nbias; ++j) {  // K columns C*KX + 32 j + c: rowsum of channel 32 j + c
       mbar_wait(&z_empty[zsi], zph ^ 1u);
-      unsigned char* zh = smem + p.off_z + (size_t)zsi * p.z_stage;
-      unsigned char* zl = zh + kGM * 128;
+      tc_fence_after();
       float z[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
@@ -369,8 +370,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
         }
         z[c] = sum;
       }
-      put_row(zh, zl, z);
-      fence_proxy_async_smem();
+      put_row(zsi, z);
       __syncwarp();
       if (lane == 0) mbar_arrive(&z_full[zsi]);
       if (++zsi == p.zs) zsi = 0, zph ^= 1u;
@@ -378,7 +378,6 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     // ======== epilogue: TMEM -> registers -> Y ========
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int re = q * 32 + lane;
     const int64_t g = r0 + re;
     const bool live = re < rows_in && rbase[re] >= 0;
@@ -497,10 +496,10 @@ bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_r
   L.xr = (int32_t)std::min<int64_t>(256, (kGM + 2 * (R - 1) + kXBox - 1) / kXBox * kXBox);
   const int32_t split = mode == 0 ? 2 : 1;
   L.w_stage = L.nt * 128 * split;
-  L.z_stage = kGM * 128 * split;
+  L.z_stage = 0;  // Z lives in TMEM (32 columns per stage and split part)
   L.x_stage = L.xr * 128;
-  L.ws = 3;
-  L.zs = 2;
+  L.ws = 4;
+  L.zs = std::min(8, (512 - kZCol) / (32 * split));
   L.xs = 2;
   auto layout = [&]() {
     int32_t off = 0;
@@ -527,7 +526,7 @@ bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_r
     L.smem = off + 1024;
   };
   layout();
-  while (L.cap_e < 1024 && L.ws > 2) {  // room for the structure first
+  while (L.cap_e < 2048 && L.ws > 2) {  // room for the structure first
     --L.ws;
     layout();
   }

@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--ctas", default="0,1,2")
     ap.add_argument("--chunks", default="0")
     ap.add_argument("--ncu-mode", action="store_true", help="plain launches only (for ncu)")
+    ap.add_argument("--ncu-coo", action="store_true", help="with --ncu-mode: also 6 fused COO launches")
     ap.add_argument("--dbg", default="0", help="comma list of debug bit sets to sweep (bspmm_set_debug)")
     ap.add_argument("--replicas", type=int, default=0, help="override the replica count (1 = L2-warm)")
     ap.add_argument("--copy-baseline", action="store_true", help="also time C.copy_(B) on the same replicas")
@@ -189,6 +190,9 @@ def main():
         if args.ncu_mode:
             for i in range(6):
                 full_step(h, reps[i % len(reps)])
+            if args.ncu_coo and "idx" in reps[0]:  # then the fused COO launches (bspmm_coo with hints)
+                for i in range(6):
+                    coo_convert_csr(h, reps[i % len(reps)])
             torch.cuda.synchronize()
             print(json.dumps({"config": cid, "ncu_mode": True, "plan": h.last_plan()}), flush=True)
             del reps
