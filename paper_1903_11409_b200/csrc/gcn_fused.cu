@@ -46,10 +46,10 @@ namespace bspmm {
 
 constexpr int kGM = 128;          // node rows per tile (MMA M, TMEM lanes)
 constexpr int kGK = 32;           // K per block: 32 x 4 B = one 128-byte swizzle row
-constexpr int kGThreads = 192;    // warp 0 TMA, warp 1 MMA, warps 2-5 math
-constexpr int kGMath = 4;         // math warps
+constexpr int kGThreads = 320;    // warp 0 TMA, warp 1 MMA, warps 2-9 math (two groups of 4)
+constexpr int kGMath = 4;         // math warps per group (one per TMEM lane quarter)
 constexpr int kXBox = 64;         // rows per X TMA box
-constexpr int kZCol = 128;        // first TMEM column of the Z stages (after the accumulator)
+constexpr int kZCol = 256;        // first TMEM column of the Z stages (after the accumulator, nt <= 256)
 
 struct GcnParams {
   int32_t batch, channels, n_x, k;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.ws; ++s) mbar_init(&w_full[s], 1), mbar_init(&w_empty[s], 1);
     for (int s = 0; s < p.zs; ++s) mbar_init(&z_full[s], kGMath), mbar_init(&z_empty[s], 1);
-    for (int s = 0; s < p.xs; ++s) mbar_init(&x_full[s], 1), mbar_init(&x_empty[s], kGMath);
+    for (int s = 0; s < p.xs; ++s) mbar_init(&x_full[s], 1), mbar_init(&x_empty[s], 2 * kGMath);
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
@@ -186,21 +186,21 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
   __syncthreads();
   const bool staged_s = s_staged_s != 0;
   if (staged_s && warp >= 2) {  // the math warps stage row pointers, columns and values
-    const int mt = threadIdx.x - 64;
+    const int mt = threadIdx.x - 64, MT = kGThreads - 64;
     for (int32_t ch = 0; ch < p.channels; ++ch) {
       const int32_t* rp = p.row_ptr + (int64_t)ch * (p.N + 1) + r0;
       const int32_t e0 = rp[0];
       const int32_t eb = s_ebase[ch];
-      for (int r = mt; r <= kGM; r += 128) rp_s[ch * (kGM + 1) + r] = eb + (r <= rows_in ? rp[r] - e0 : rp[rows_in] - e0);
+      for (int r = mt; r <= kGM; r += MT) rp_s[ch * (kGM + 1) + r] = eb + (r <= rows_in ? rp[r] - e0 : rp[rows_in] - e0);
       const int32_t ne = s_ebase[ch + 1] - eb;
-      for (int32_t e = mt; e < ne; e += 128) {
+      for (int32_t e = mt; e < ne; e += MT) {
         col_s[eb + e] = p.col[e0 + e];
         val_s[eb + e] = p.vals[e0 + e];
       }
     }
   }
   __syncthreads();
-  if (staged_s && warp >= 2) {  // entries of row r: col -> halo row of the neighbour (rbase[r] + col)
+  if (staged_s && warp >= 2 && warp < 2 + kGMath) {  // entries of row r: col -> halo row (rbase[r] + col)
     const int r = threadIdx.x - 64;
     const int32_t rb = rbase[r];
     if (rb >= 0)
@@ -281,8 +281,9 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     const int r = q * 32 + lane;  // its row (= TMEM lane) of the tile
     const int32_t rb = rbase[r];
     const uint32_t tq = s_tmem + ((uint32_t)(q * 32) << 16);
-    int zsi = 0, xsi = 0;
-    uint32_t zph = 0, xph = 0;
+    // two groups of four warps take alternate K blocks (kb % 2): while one
+    // group forms Z block kb, the other forms kb + 1
+    const int grp = (warp - 2) / kGMath;
     auto row_range = [&](int32_t ch, int32_t& e0, int32_t& e1) {
       if (staged_s) {
         e0 = rp_s[ch * (kGM + 1) + r];
@@ -315,10 +316,18 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
       tc_fence_before();
     };
     for (int32_t xb = 0; xb < p.nxb; ++xb) {
-      mbar_wait(&x_full[xsi], xph);
+      const int xsi = xb % p.xs;
       const unsigned char* xs = smem + p.off_x + (size_t)xsi * p.x_stage;
+      bool waited_x = false;
       for (int32_t ch = 0; ch < p.channels; ++ch) {
-        mbar_wait(&z_empty[zsi], zph ^ 1u);
+        const int32_t kb = xb * p.channels + ch;
+        if ((kb & 1) != grp) continue;
+        const int zsi = kb % p.zs;
+        if (!waited_x) {
+          mbar_wait(&x_full[xsi], (uint32_t)(xb / p.xs) & 1u);
+          waited_x = true;
+        }
+        mbar_wait(&z_empty[zsi], ((uint32_t)(kb / p.zs) & 1u) ^ 1u);
         tc_fence_after();
         float z[32];
 #pragma unroll
@@ -349,14 +358,18 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
         put_row(zsi, z);
         __syncwarp();
         if (lane == 0) mbar_arrive(&z_full[zsi]);
-        if (++zsi == p.zs) zsi = 0, zph ^= 1u;
       }
+      // both groups release every X block (a group with no K block in it too;
+      // the X ring then never runs ahead of either)
+      if (!waited_x) mbar_wait(&x_full[xsi], (uint32_t)(xb / p.xs) & 1u);
       __syncwarp();
       if (lane == 0) mbar_arrive(&x_empty[xsi]);
-      if (++xsi == p.xs) xsi = 0, xph ^= 1u;
     }
     for (int32_t j = 0; j < p.nbias; ++j) {  // K columns C*KX + 32 j + c: rowsum of channel 32 j + c
-      mbar_wait(&z_empty[zsi], zph ^ 1u);
+      const int32_t kb = p.nxb * p.channels + j;
+      if ((kb & 1) != grp) continue;
+      const int zsi = kb % p.zs;
+      mbar_wait(&z_empty[zsi], ((uint32_t)(kb / p.zs) & 1u) ^ 1u);
       tc_fence_after();
       float z[32];
 #pragma unroll
@@ -373,7 +386,6 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
       put_row(zsi, z);
       __syncwarp();
       if (lane == 0) mbar_arrive(&z_full[zsi]);
-      if (++zsi == p.zs) zsi = 0, zph ^= 1u;
     }
     // ======== epilogue: TMEM -> registers -> Y ========
     mbar_wait(acc_full, 0);
@@ -383,7 +395,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     const bool live = re < rows_in && rbase[re] >= 0;
     const bool vec = ((p.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0);
     float* yrow = p.Y + g * p.ldy;
-    for (int32_t c0 = 0; c0 < p.nt; c0 += 16) {
+    const int32_t half = ((p.nt >> 1) + 15) & ~15;  // group 0: columns [0, half), group 1: [half, nt)
+    for (int32_t c0 = grp ? half : 0; c0 < (grp ? p.nt : half); c0 += 16) {
       float v[16];
       tmem_ld16(s_tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);  // whole warp, converged
       const int32_t cg = n0 + c0;
@@ -489,7 +502,9 @@ bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_r
   L.nxb = L.KX / kGK;
   L.nbias = (channels + 31) / 32;
   L.ktot = channels * L.KX + L.nbias * kGK;
-  L.nt = k > 64 ? 128 : (k > 32 ? 64 : 32);
+  // output features per tile (MMA N, TMEM accumulator columns): up to 256, so
+  // that k = 512 takes two feature tiles (Z is formed once per feature tile)
+  L.nt = k > 128 ? 256 : (k > 64 ? 128 : (k > 32 ? 64 : 32));
   L.ntiles_n = (k + L.nt - 1) / L.nt;
   L.tiles_m = (int32_t)((N + kGM - 1) / kGM);
   const int64_t R = max_rows > 0 ? max_rows : 64;
