@@ -50,7 +50,9 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * tile kernel stages B by cp.async even where 2-D TMA applies; 65536 = tile
  * kernel issues its row-pointer round trip after the B tile; 131072 = GCN
  * layer without the Z arithmetic, 262144 = GCN layer without the MMAs (both
- * leave Y undefined; timing only).  0
+ * leave Y undefined; timing only); 524288 = GCN layer with two groups of
+ * Z-producer warps instead of three (3xTF32: three instead of two);
+ * bits 20-21 = GCN feature-tile width (1: 64, 2: 128, 3: 256; 0: planner).  0
  * (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 

@@ -319,7 +319,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 1048575) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits > 4194303) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -646,7 +646,9 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
     }
   }
   GcnPlan L;
-  if (!plan_gcn(channels, n_x, k, N, h->hint_rows, h->smem_optin, h->gcn_math, &L))
+  // debug bits 20-21: feature-tile width override (1: 64, 2: 128, 3: 256)
+  const int32_t nt_ovr = ((h->dbg >> 20) & 3) ? (32 << ((h->dbg >> 20) & 3)) : 0;
+  if (!plan_gcn(channels, n_x, k, N, h->hint_rows, h->smem_optin, h->gcn_math, h->num_sms, nt_ovr, &L))
     return fail(h, BSPMM_ERROR_NOT_SUPPORTED, "bspmm_gcn_layer: no shared-memory plan for these sizes");
   // X needs a 16-byte row pitch and base for TMA; otherwise a packed copy
   const bool x_ok = (ldx % 4 == 0) && aligned16(X);
@@ -676,7 +678,7 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
   }
   CK(h, launch_gcn_prep(L, batch, channels, n_x, k, N, h->gcn_math, W, bias, whi, wlo, row_off, gfirst, h->stream));
   h->launches++;
-  GcnArgs a{batch, channels, n_x, k, h->gcn_math, (h->dbg >> 17) & 3, N, row_off, sizes, row_ptr, col, vals, Xk, ldxp, Y, ldy, gfirst,
+  GcnArgs a{batch, channels, n_x, k, h->gcn_math, (h->dbg >> 17) & 7, N, row_off, sizes, row_ptr, col, vals, Xk, ldxp, Y, ldy, gfirst,
             &mx, &mhi, &mlo};
   CK(h, launch_gcn_fused(L, a, h->stream));
   h->launches++;

@@ -46,8 +46,9 @@ namespace bspmm {
 
 constexpr int kGM = 128;          // node rows per tile (MMA M, TMEM lanes)
 constexpr int kGK = 32;           // K per block: 32 x 4 B = one 128-byte swizzle row
-constexpr int kGThreads = 320;    // warp 0 TMA, warp 1 MMA, warps 2-9 math (two groups of 4)
 constexpr int kGMath = 4;         // math warps per group (one per TMEM lane quarter)
+// CTA size with NG groups of Z-producer warps (the groups take K blocks kb % NG)
+__host__ __device__ constexpr int gcn_threads(int NG) { return 64 + 32 * kGMath * NG; }
 constexpr int kXBox = 64;         // rows per X TMA box
 constexpr int kZCol = 256;        // first TMEM column of the Z stages (after the accumulator, nt <= 256)
 
@@ -62,7 +63,7 @@ struct GcnParams {
   int32_t w_stage, z_stage, x_stage;  // bytes per stage
   int32_t off_w, off_z, off_x, off_rp, off_col, off_val, off_rb, off_bar;
   uint32_t idesc;
-  int32_t dbg;                    // timing experiments: 1 = no Z arithmetic, 2 = no MMAs (results undefined)
+  int32_t dbg;                    // 1 = no Z arithmetic, 2 = no MMAs (timing only, results undefined); 4 = 2 groups
   const int64_t* __restrict__ row_off;
   const int32_t* __restrict__ sizes;
   const int32_t* __restrict__ row_ptr;  // [channels][N + 1]
@@ -83,7 +84,11 @@ struct GcnMaps {
 
 __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
-__global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams p, const __grid_constant__ GcnMaps m) {
+template <int NG>
+__global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const GcnParams p,
+                                                                     const __grid_constant__ GcnMaps m) {
+  constexpr int kGGroups = NG;
+  constexpr int kGThreads = gcn_threads(NG);
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte aligned base (128-byte swizzle atoms), by an offset on the shared
   // pointer itself so that every access below compiles to LDS/STS (an integer
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.ws; ++s) mbar_init(&w_full[s], 1), mbar_init(&w_empty[s], 1);
     for (int s = 0; s < p.zs; ++s) mbar_init(&z_full[s], kGMath), mbar_init(&z_empty[s], 1);
-    for (int s = 0; s < p.xs; ++s) mbar_init(&x_full[s], 1), mbar_init(&x_empty[s], 2 * kGMath);
+    for (int s = 0; s < p.xs; ++s) mbar_init(&x_full[s], 1), mbar_init(&x_empty[s], kGGroups * kGMath);
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
@@ -281,8 +286,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     const int r = q * 32 + lane;  // its row (= TMEM lane) of the tile
     const int32_t rb = rbase[r];
     const uint32_t tq = s_tmem + ((uint32_t)(q * 32) << 16);
-    // two groups of four warps take alternate K blocks (kb % 2): while one
-    // group forms Z block kb, the other forms kb + 1
+    // NG groups of four warps take K blocks in turn (kb % NG): while one group
+    // forms Z block kb, the others form kb + 1, ...
     const int grp = (warp - 2) / kGMath;
     auto row_range = [&](int32_t ch, int32_t& e0, int32_t& e1) {
       if (staged_s) {
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
       bool waited_x = false;
       for (int32_t ch = 0; ch < p.channels; ++ch) {
         const int32_t kb = xb * p.channels + ch;
-        if ((kb & 1) != grp) continue;
+        if (kb % kGGroups != grp) continue;
         const int zsi = kb % p.zs;
         if (!waited_x) {
           mbar_wait(&x_full[xsi], (uint32_t)(xb / p.xs) & 1u);
@@ -335,23 +340,61 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
         if (rb >= 0 && !(p.dbg & 1)) {
           int32_t e, e1;
           row_range(ch, e, e1);
-          for (; e < e1; ++e) {
-            const int32_t xr = staged_s ? col_s[e] : rb + p.col[e];  // staged: halo row already
-            const float a = staged_s ? val_s[e] : p.vals[e];
-            if (staged_x) {
-              const unsigned char* xrow = xs + (size_t)xr * 128;
+          if (staged_s && staged_x) {
+            // two entries per iteration: both X rows' loads in flight before
+            // the FMAs, which stay in storage order (entry e, then e + 1)
+            auto xrow4 = [&](int32_t xr, int j) {
+              return *reinterpret_cast<const float4*>(xs + (size_t)xr * 128 + ((j ^ (xr & 7)) << 4));
+            };
+            for (; e + 1 < e1; e += 2) {
+              const int32_t xr0 = col_s[e], xr1 = col_s[e + 1];  // halo rows (staged)
+              const float a0 = val_s[e], a1 = val_s[e + 1];
+              float4 v0[8], v1[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v0[j] = xrow4(xr0, j), v1[j] = xrow4(xr1, j);
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float4 v = *reinterpret_cast<const float4*>(xrow + ((j ^ (xr & 7)) << 4));
-                z[4 * j] = fmaf(a, v.x, z[4 * j]);
-                z[4 * j + 1] = fmaf(a, v.y, z[4 * j + 1]);
-                z[4 * j + 2] = fmaf(a, v.z, z[4 * j + 2]);
-                z[4 * j + 3] = fmaf(a, v.w, z[4 * j + 3]);
+                z[4 * j] = fmaf(a0, v0[j].x, z[4 * j]);
+                z[4 * j + 1] = fmaf(a0, v0[j].y, z[4 * j + 1]);
+                z[4 * j + 2] = fmaf(a0, v0[j].z, z[4 * j + 2]);
+                z[4 * j + 3] = fmaf(a0, v0[j].w, z[4 * j + 3]);
+                z[4 * j] = fmaf(a1, v1[j].x, z[4 * j]);
+                z[4 * j + 1] = fmaf(a1, v1[j].y, z[4 * j + 1]);
+                z[4 * j + 2] = fmaf(a1, v1[j].z, z[4 * j + 2]);
+                z[4 * j + 3] = fmaf(a1, v1[j].w, z[4 * j + 3]);
               }
-            } else {
-              const float* xg = p.X + (xlo + xr) * p.ldx + xb * kGK;
+            }
+            if (e < e1) {
+              const int32_t xr0 = col_s[e];
+              const float a0 = val_s[e];
 #pragma unroll
-              for (int c = 0; c < 32; ++c) z[c] = fmaf(a, xb * kGK + c < p.n_x ? __ldg(xg + c) : 0.f, z[c]);
+              for (int j = 0; j < 8; ++j) {
+                const float4 v = xrow4(xr0, j);
+                z[4 * j] = fmaf(a0, v.x, z[4 * j]);
+                z[4 * j + 1] = fmaf(a0, v.y, z[4 * j + 1]);
+                z[4 * j + 2] = fmaf(a0, v.z, z[4 * j + 2]);
+                z[4 * j + 3] = fmaf(a0, v.w, z[4 * j + 3]);
+              }
+            }
+          } else {
+            for (; e < e1; ++e) {
+              const int32_t xr = staged_s ? col_s[e] : rb + p.col[e];  // staged: halo row already
+              const float a = staged_s ? val_s[e] : p.vals[e];
+              if (staged_x) {
+                const unsigned char* xrow = xs + (size_t)xr * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float4 v = *reinterpret_cast<const float4*>(xrow + ((j ^ (xr & 7)) << 4));
+                  z[4 * j] = fmaf(a, v.x, z[4 * j]);
+                  z[4 * j + 1] = fmaf(a, v.y, z[4 * j + 1]);
+                  z[4 * j + 2] = fmaf(a, v.z, z[4 * j + 2]);
+                  z[4 * j + 3] = fmaf(a, v.w, z[4 * j + 3]);
+                }
+              } else {
+                const float* xg = p.X + (xlo + xr) * p.ldx + xb * kGK;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) z[c] = fmaf(a, xb * kGK + c < p.n_x ? __ldg(xg + c) : 0.f, z[c]);
+              }
             }
           }
         }
@@ -367,7 +410,7 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     }
     for (int32_t j = 0; j < p.nbias; ++j) {  // K columns C*KX + 32 j + c: rowsum of channel 32 j + c
       const int32_t kb = p.nxb * p.channels + j;
-      if ((kb & 1) != grp) continue;
+      if (kb % kGGroups != grp) continue;
       const int zsi = kb % p.zs;
       mbar_wait(&z_empty[zsi], ((uint32_t)(kb / p.zs) & 1u) ^ 1u);
       tc_fence_after();
@@ -395,8 +438,8 @@ __global__ void __launch_bounds__(kGThreads, 1) gcn_fused_kernel(const GcnParams
     const bool live = re < rows_in && rbase[re] >= 0;
     const bool vec = ((p.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0);
     float* yrow = p.Y + g * p.ldy;
-    const int32_t half = ((p.nt >> 1) + 15) & ~15;  // group 0: columns [0, half), group 1: [half, nt)
-    for (int32_t c0 = grp ? half : 0; c0 < (grp ? p.nt : half); c0 += 16) {
+    const int32_t part = ((p.nt + kGGroups - 1) / kGGroups + 15) & ~15;  // group g: columns [g part, (g+1) part)
+    for (int32_t c0 = grp * part; c0 < min(p.nt, (grp + 1) * part); c0 += 16) {
       float v[16];
       tmem_ld16(s_tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);  // whole warp, converged
       const int32_t cg = n0 + c0;
@@ -496,17 +539,22 @@ __global__ void __launch_bounds__(256) gcn_pack_x_kernel(const float* __restrict
 }
 
 bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_rows, int32_t smem_optin, int32_t mode,
-              GcnPlan* out) {
+              int32_t num_sms, int32_t nt_override, GcnPlan* out) {
   GcnPlan L{};
   L.KX = (n_x + kGK - 1) / kGK * kGK;
   L.nxb = L.KX / kGK;
   L.nbias = (channels + 31) / 32;
   L.ktot = channels * L.KX + L.nbias * kGK;
   // output features per tile (MMA N, TMEM accumulator columns): up to 256, so
-  // that k = 512 takes two feature tiles (Z is formed once per feature tile)
-  L.nt = k > 128 ? 256 : (k > 64 ? 128 : (k > 32 ? 64 : 32));
-  L.ntiles_n = (k + L.nt - 1) / L.nt;
+  // that k = 512 takes two feature tiles (Z is formed once per feature tile);
+  // 128 when 256-wide tiles would leave SMs idle (small batches: more CTAs,
+  // each forming its Z again; Reaction100-like 86 -> 70 us, 64-wide tiles
+  // measured slower again, 131 us)
   L.tiles_m = (int32_t)((N + kGM - 1) / kGM);
+  L.nt = k > 128 ? 256 : (k > 64 ? 128 : (k > 32 ? 64 : 32));
+  if (L.nt == 256 && (int64_t)L.tiles_m * ((k + 255) / 256) < num_sms) L.nt = 128;
+  if (nt_override >= 32 && nt_override <= 256) L.nt = nt_override;
+  L.ntiles_n = (k + L.nt - 1) / L.nt;
   const int64_t R = max_rows > 0 ? max_rows : 64;
   L.xr = (int32_t)std::min<int64_t>(256, (kGM + 2 * (R - 1) + kXBox - 1) / kXBox * kXBox);
   const int32_t split = mode == 0 ? 2 : 1;
@@ -635,20 +683,25 @@ cudaError_t launch_gcn_fused(const GcnPlan& L, const GcnArgs& a, cudaStream_t s)
   maps.x = *a.map_x;
   maps.whi = *a.map_whi;
   maps.wlo = *a.map_wlo;
-  static thread_local int configured[64] = {};
+  // Z-producer groups: 3xTF32 2 (its tensor-core operand traffic bounds it;
+  // a third group measured 6% slower), the one-pass modes 3; debug bit
+  // 524288 swaps
+  const int ng = ((a.mode == 0) != ((a.dbg & 4) != 0)) ? 2 : 3;
+  auto kern = ng == 2 ? gcn_fused_kernel<2> : gcn_fused_kernel<3>;
+  static thread_local int configured[2][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (configured[dev & 63] < L.smem) {
-    cudaError_t e = cudaFuncSetAttribute(gcn_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
+  if (configured[ng - 2][dev & 63] < L.smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
-    configured[dev & 63] = L.smem;
+    configured[ng - 2][dev & 63] = L.smem;
   }
   const int64_t grid = (int64_t)L.tiles_m * L.ntiles_n;
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kGThreads);
+  cfg.blockDim = dim3(gcn_threads(ng));
   cfg.dynamicSmemBytes = L.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -656,7 +709,7 @@ cudaError_t launch_gcn_fused(const GcnPlan& L, const GcnArgs& a, cudaStream_t s)
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gcn_fused_kernel, p, maps);
+  return cudaLaunchKernelEx(&cfg, kern, p, maps);
 }
 
 }  // namespace bspmm

@@ -114,7 +114,7 @@ struct GcnArgs {
   const CUtensorMap* map_wlo;
 };
 bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_rows, int32_t smem_optin, int32_t mode,
-              GcnPlan* out);
+              int32_t num_sms, int32_t nt_override, GcnPlan* out);
 cudaError_t launch_gcn_prep(const GcnPlan& L, int32_t batch, int32_t channels, int32_t n_x, int32_t k, int64_t N,
                             int32_t mode, const float* W, const float* bias, float* whi, float* wlo,
                             const int64_t* row_off, int32_t* gfirst, cudaStream_t s);
