@@ -271,16 +271,17 @@ __global__ void __launch_bounds__(kBwdThreads) sddmm_kernel(int32_t batch, int32
 // iteration from shared memory (independent loads first), reduced across the
 // warp with a fixed butterfly (deterministic).  Matrices whose B_i exceeds
 // the capacity read B from global memory in the same loop.
-template <int CH, bool STAGED>
+template <int CH, bool STAGED, int PF = 1>
 __device__ __forceinline__ void sddmm_rows(int32_t n, int32_t chunks, const float* __restrict__ Bsrc, int64_t bld,
                                            const float* __restrict__ Grow0, int64_t ldg,
                                            const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                            float* __restrict__ out, int lane, int warp, int nw,
                                            uint64_t* bar = nullptr, uint32_t phase = 0) {
-  // rows r = warp, warp + nw, ...; the next row's grad_C chunks and row range
-  // are loaded while the current row computes (one exposed latency per matrix)
-  float4 gn[CH];
-  int32_t n0 = 0, n1 = 0;
+  // rows r = warp, warp + nw, ...; the grad_C chunks and row ranges of the
+  // next PF rows are in flight while the current row computes (one exposed
+  // latency per matrix)
+  float4 gq[PF][CH];
+  int32_t q0[PF], q1[PF];
   bool ok[CH];
 #pragma unroll
   for (int v = 0; v < CH; ++v) ok[v] = lane + 32 * v < chunks;
@@ -289,22 +290,34 @@ __device__ __forceinline__ void sddmm_rows(int32_t n, int32_t chunks, const floa
 #pragma unroll
     for (int v = 0; v < CH; ++v) dst[v] = ok[v] ? ldg_nc_f4(grow + 4 * (lane + 32 * v)) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  if (warp < n) {
-    n0 = __ldg(rp + warp);
-    n1 = __ldg(rp + warp + 1);
-    gload(warp, gn);
+#pragma unroll
+  for (int f = 0; f < PF; ++f) {
+    const int32_t rr = warp + f * nw;
+    q0[f] = q1[f] = 0;
+    if (rr < n) {
+      q0[f] = __ldg(rp + rr);
+      q1[f] = __ldg(rp + rr + 1);
+      gload(rr, gq[f]);
+    }
   }
-  // staged: the first row's grad_C loads are in flight while B_i lands
+  // staged: the first rows' grad_C loads are in flight while B_i lands
   if (STAGED) mbar_wait(bar, phase);
   for (int32_t r = warp; r < n; r += nw) {
-    const int32_t e0 = n0, e1 = n1;
+    const int32_t e0 = q0[0], e1 = q1[0];
     float4 gv[CH];
 #pragma unroll
-    for (int v = 0; v < CH; ++v) gv[v] = gn[v];
-    if (r + nw < n) {
-      n0 = __ldg(rp + r + nw);
-      n1 = __ldg(rp + r + nw + 1);
-      gload(r + nw, gn);
+    for (int v = 0; v < CH; ++v) gv[v] = gq[0][v];
+#pragma unroll
+    for (int f = 0; f + 1 < PF; ++f) {
+      q0[f] = q0[f + 1];
+      q1[f] = q1[f + 1];
+#pragma unroll
+      for (int v = 0; v < CH; ++v) gq[f][v] = gq[f + 1][v];
+    }
+    if (r + PF * nw < n) {
+      q0[PF - 1] = __ldg(rp + r + PF * nw);
+      q1[PF - 1] = __ldg(rp + r + PF * nw + 1);
+      gload(r + PF * nw, gq[PF - 1]);
     }
     if (e1 == e0) continue;
     auto bload = [&](int32_t cc, int v) -> float4 {
@@ -420,6 +433,7 @@ __global__ void __launch_bounds__(kBwdThreads) sddmm_staged_kernel(int32_t batch
     __syncthreads();  // every warp is done with Bs before the next matrix's copy
   }
 }
+
 
 cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
