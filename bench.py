@@ -77,7 +77,9 @@ def peaks():
 
 
 class Clocks:
-    """NVML sampler of SM clocks and throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    (the device found by its UUID, then by index), else an `nvidia-smi -lms`
+    subprocess on the same GPU."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -86,23 +88,71 @@ class Clocks:
     def __init__(self, index: int, period: float = 0.002):
         self.samples, self.reasons, self.ok = [], 0, False
         self.max_mhz = None
+        self.source = None
+        self.uuid = None
+        try:
+            import torch
+            self.uuid = "GPU-" + str(torch.cuda.get_device_properties(index).uuid)
+        except Exception:
+            pass
         try:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.dev = pynvml.nvmlDeviceGetHandleByIndex(index)
+            dev = None
+            if self.uuid:
+                try:
+                    dev = pynvml.nvmlDeviceGetHandleByUUID(self.uuid)
+                except Exception:
+                    dev = None
+            if dev is None:
+                dev = pynvml.nvmlDeviceGetHandleByIndex(index if pynvml.nvmlDeviceGetCount() > index else 0)
+            self.dev = dev
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.dev, pynvml.NVML_CLOCK_SM)
             self.ok = True
-        except Exception:
-            pass
+            self.source = "nvml"
+        except Exception as e:
+            print(f"bench: NVML clock sampling unavailable ({type(e).__name__}: {e}); trying nvidia-smi",
+                  file=sys.stderr)
+            self.ok = self._smi_probe()
         self.period = period
         self._stop = threading.Event()
         # samples are kept only while `active` is set (the timed region); the
-        # thread starts before the warm-up so NVML's first-call latency is
-        # paid outside the region
+        # thread starts before the warm-up so the sampler's first-call latency
+        # is paid outside the region
         self.active = threading.Event()
 
+    def _smi_cmd(self, extra):
+        sel = ["-i", self.uuid] if self.uuid else []
+        return ["nvidia-smi", *sel, "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                "--format=csv,noheader,nounits", *extra]
+
+    def _smi_probe(self) -> bool:
+        try:
+            out = subprocess.run(self._smi_cmd([]), capture_output=True, text=True, timeout=20).stdout.strip()
+            self.max_mhz = int(float(out.splitlines()[0].split(",")[1]))
+            self.source = "nvidia-smi"
+            return True
+        except Exception:
+            return False
+
     def _run(self):
+        if self.source == "nvidia-smi":
+            proc = subprocess.Popen(self._smi_cmd(["-lms", "20"]), stdout=subprocess.PIPE, text=True)
+            try:
+                for line in proc.stdout:
+                    if self._stop.is_set():
+                        break
+                    if self.active.is_set():
+                        try:
+                            f = [x.strip() for x in line.split(",")]
+                            self.samples.append(float(f[0]))
+                            self.reasons |= int(f[2], 16)
+                        except Exception:
+                            pass
+            finally:
+                proc.kill()
+            return
         nv = self.nv
         get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             nv.nvmlDeviceGetCurrentClocksThrottleReasons
@@ -113,8 +163,10 @@ class Clocks:
                 if self.active.is_set():
                     self.samples.append(mhz)
                     self.reasons |= why
-            except Exception:
-                pass
+            except Exception as e:
+                if not getattr(self, "_warned", False):
+                    print(f"bench: NVML sample failed ({type(e).__name__}: {e})", file=sys.stderr)
+                    self._warned = True
             time.sleep(self.period)
 
     def __enter__(self):
@@ -126,14 +178,15 @@ class Clocks:
     def __exit__(self, *a):
         if self.ok:
             self._stop.set()
-            self._t.join()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml-unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["clock-sampling-unavailable"],
+                    "samples": 0, "source": self.source}
         names = [v for b, v in self.REASONS.items() if self.reasons & b and b != 0x1]
         return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": names,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": self.source}
 
 
 def cpu_baseline(b, budget_s: float = 12.0):
