@@ -319,7 +319,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits > 4194303) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits >= (1 << 26)) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -413,7 +413,7 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
     plan.threads = 128;
     plan.smem_bytes = L.smem;
     h->last_plan = plan;
-    const TmaMaps* maps = L.cb >= 8 ? tma_maps(h, B, k, ldb, 4 * L.cb) : nullptr;
+    const TmaMaps* maps = (L.cb >= 8 && (h->dbg & 32768)) ? tma_maps(h, B, k, ldb, 4 * L.cb) : nullptr;
     CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias,
               accumulate};
     CK(h, launch_spmm_tile(a, L, h->stream));

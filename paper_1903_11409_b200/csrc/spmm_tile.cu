@@ -304,6 +304,11 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
   else if (bst) tile_rows<CB, EPI, true, false>(p, Bs, rp_s, col_s, val_s, g0, n, c0, cw);
   else tile_rows<CB, EPI, false, false>(p, Bs, rp_s, col_s, val_s, g0, n, c0, cw);
   tile_trace(p, 6);
+  if (p.trace && threadIdx.x == 0) {  // debug: which SM ran the tile (load-balance analysis)
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    p.trace[(size_t)blockIdx.x * 32 + 7] = sm;
+  }
 }
 
 // Launch geometry for a batch; false when the batch is better served by the
@@ -416,9 +421,11 @@ cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t
   tp.bias = reinterpret_cast<const float4*>(a.bias);
   tp.accumulate = a.accumulate;
   tp.trace = a.trace;
-  // 2-D TMA needs the handle's descriptors for box width 4 * cb (tma_maps)
-  // and a 128-byte shared row pitch; debug bit 32768 forces cp.async
-  tp.tma = (a.maps != nullptr && L.cb >= 8 && !(a.dbg & 32768)) ? 1 : 0;
+  // B by 16-byte cp.async (config 4: 6.69-6.71 us per call against 6.87-6.88
+  // for 2-D tensor TMA, tools/probe/tile_balance.py); debug bit 32768 stages
+  // it by 2-D TMA where that applies (the handle's descriptors for box width
+  // 4 * cb, a 128-byte shared row pitch)
+  tp.tma = (a.maps != nullptr && L.cb >= 8 && (a.dbg & 32768)) ? 1 : 0;
   tp.rp_first = (a.dbg & 65536) ? 0 : 1;
   tp.dbg_bits = (a.dbg & 16) ? 1 : 0;
   static const TmaMaps no_maps{};
