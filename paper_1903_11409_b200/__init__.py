@@ -159,7 +159,9 @@ class Handle:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        # at interpreter shutdown the module globals may already be gone: the
+        # process exit releases the handle's device memory then
+        if h is not None and h.value and lib is not None:
             lib.bspmm_destroy(h)
             self._h = None
 

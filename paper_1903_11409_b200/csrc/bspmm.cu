@@ -600,6 +600,12 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
       a.coo_nnz_off = nnz_off;
       a.coo_idx = idx;
       a.err = h->dev_flag;
+      a.cvt_warps = kCooWarps - 1 - coo_consumer_warps(h->tune_warps);
+      if (h->dbg & 128) {  // dynamic unit schedule (global ticket counter)
+        plan.sched = 1;
+        h->last_plan = plan;
+        a.sched = h->dev_sched;
+      }
       CK(h, launch_spmm_csr(a, plan, h->stream));
       if (plan.units > 0) h->launches++;
       h->coo_fused_pending = true;

@@ -33,12 +33,19 @@ inline int32_t pow2_ceil(int32_t x) {
 BSPMM_HD inline int32_t align_up(int32_t x, int32_t a) { return (x + a - 1) / a * a; }
 
 // smem carve-up shared by planner and kernel: [hdr S*32][full S*8][empty S*8]
-// [early 8][sfull S*8] pad 128, then stages.  Per stage: header + "full" +
-// "empty" barriers; one barrier for the first unit's early B tile
-// (spmm_csr.cu early_b); per stage a "slice full" barrier (fused COO mode: the
-// raw SparseTensor slice lands on its own barrier, so its conversion overlaps
-// the B tile's landing)
-BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stages * (kHdrBytes + 24) + 8, 128); }
+// [early 8][sfull S*8][cvt S*8] pad 128, then stages.  Per stage: header +
+// "full" + "empty" barriers; one barrier for the first unit's early B tile
+// (spmm_csr.cu early_b); fused COO mode, per stage: a "slice full" barrier
+// (the raw SparseTensor slice lands on its own barrier) and a "converted"
+// barrier (the converter warps have written the stage's CSR slice)
+BSPMM_HD inline int32_t ring_prefix_bytes(int32_t stages) { return align_up(stages * (kHdrBytes + 32) + 8, 128); }
+// fused COO mode: 20 warps per CTA (5 per SM sub-partition: 96 registers) --
+// the producer, W consumer warps and 19 - W converter warps that convert the
+// next unit's SparseTensor slice while the consumers compute the current one
+// (spmm_csr.cu convert_units); W from the tuning knob, else kCooConsumers
+constexpr int kCooWarps = 20;
+constexpr int kCooConsumers = 10;
+inline int32_t coo_consumer_warps(int32_t tune) { return tune > 0 ? (tune < 18 ? tune : 18) : kCooConsumers; }
 
 // planner (plan.cpp)
 bspmm_status_t make_plan(int32_t k, int32_t batch, bool aligned, int32_t max_rows, int64_t max_nnz,
@@ -72,6 +79,7 @@ struct CsrArgs {
   const int64_t* coo_nnz_off = nullptr; // fused COO mode: per-matrix entry offsets (col/vals = raw COO)
   const int32_t* coo_idx = nullptr;     // fused COO mode: (row, col) pairs
   int* err = nullptr;                   // device error flag (bit 64: COO unit over stage capacity)
+  int32_t cvt_warps = 0;                // fused COO mode: converter warps (coo_consumer_warps)
   int32_t mc = 0;                       // NEXT-4b: C is a multicast VA (multimem.st epilogue)
   const float* G = nullptr;             // SDDMM mode (NEXT-2): sd_out[e] = <G[row_e], B[col_e]>
   int64_t ldg = 0;

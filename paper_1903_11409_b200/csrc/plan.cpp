@@ -60,9 +60,8 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   const int64_t Zc = std::min<int64_t>(Z, 1 << 20);
   auto a16 = [](int64_t x) { return (x + 15) / 16 * 16; };
   int64_t s_need = 2 * a16(16 + 4 * Zc) + a16(16 + 4 * (R + 1));
-  if (coo)  // fused COO mode (spmm_csr.cu coo_stage_bytes): + raw pairs, raw values, cursors, slots
-    s_need = a16(s_need) + a16(8 * (Zc + 1)) + a16(4 * (Zc + 3)) + a16(4 * (R + 1)) +
-             a16(4 * std::max<int64_t>(Zc, (R + 31) / 32));
+  if (coo)  // fused COO mode (spmm_csr.cu coo_stage_bytes): + raw pairs, raw values, slots, row counters
+    s_need = a16(s_need) + a16(8 * (Zc + 1)) + a16(4 * (Zc + 3)) + a16(4 * Zc) + a16(4 * (R + 1));
   int64_t s_bytes64 = align_up((int32_t)s_need, 128);
   auto stages_in = [&](int32_t kt_, int32_t budget_) {
     int64_t b = align_up(std::max<int32_t>(16, R * kt_ * 4), 128);
@@ -103,12 +102,12 @@ bspmm_status_t make_plan(int32_t k, int32_t batch, bool vec, int32_t max_rows, i
   p.chunks = ch <= 1 ? 1 : (ch <= 2 ? 2 : 4);
   // consumer warps: 16 (544-thread CTA) up to 2 chunks per lane, 15 with 4
   const int32_t wmax = p.chunks >= 4 ? 15 : 16;
-  const int32_t W = warps > 0 ? std::min(warps, wmax) : wmax;
+  const int32_t W = coo ? coo_consumer_warps(warps) : warps > 0 ? std::min(warps, wmax) : wmax;
   p.stages = stages;
   p.stage_b_bytes = b_bytes;
   p.stage_s_bytes = s_bytes;
   p.smem_bytes = ring_prefix_bytes(stages) + stages * (b_bytes + s_bytes);
-  p.threads = 32 * (1 + W);
+  p.threads = coo ? 32 * kCooWarps : 32 * (1 + W);
   p.units = (int64_t)batch * p.tiles;
   p.grid = (int32_t)std::min<int64_t>(p.units, (int64_t)num_sms * ctas);
   p.max_rows = R;

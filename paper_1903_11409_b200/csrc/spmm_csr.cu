@@ -58,6 +58,8 @@ struct SpmmParams {
   const int64_t* __restrict__ nnz_off;
   const int32_t* __restrict__ idx;   // [nnz][2] (row, col) local pairs
   int* err;                          // device flag: bit 64 = a unit exceeded the stage (hint too small)
+  int32_t cvt_warps;                 // fused COO mode: converter warps (the last ones of the CTA)
+  int32_t coo_rows;                  // fused COO mode: row capacity of a stage (the hinted max_rows)
   int32_t mc;                        // NEXT-4b: C is a multicast address (EPI == 2: multimem.st stores)
   // SDDMM mode (EPI == 3, NEXT-2 backward): sd_out[e] = <G[row_e], B[col_e]>
   // over the staged B_i, whole-row units (tiles == 1); C is not written
@@ -125,10 +127,13 @@ __host__ __device__ __forceinline__ int64_t al16(int64_t x) { return (x + 15) & 
 __host__ __device__ __forceinline__ int64_t coo_raw_off(int64_t nnz, int64_t n) { return al16(slice_bytes(nnz, n)); }
 __host__ __device__ __forceinline__ int64_t coo_pairs_bytes(int64_t nnz) { return al16(8 * (nnz + 1)); }
 __host__ __device__ __forceinline__ int64_t coo_vals_bytes(int64_t nnz) { return al16(4 * (nnz + 3)); }
-__host__ __device__ __forceinline__ int64_t coo_stage_bytes(int64_t nnz, int64_t n) {
-  // ... + cursors [n + 1] + slots [max(nnz, 32-row chunks)] (the chunk totals of the row scan live there first)
-  return coo_raw_off(nnz, n) + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz) + al16(4 * (n + 1)) +
-         al16(4 * (nnz > (n + 31) / 32 ? nnz : (n + 31) / 32));
+// ... + slots [nnz]; the per-row counters live at a FIXED place, the end of
+// the stage's structure region (capacity `cap` rows): they are zeroed once at
+// kernel start and left at zero by every conversion (counted up by the row
+// histogram, back down by the scatter)
+__host__ __device__ __forceinline__ int64_t coo_cursor_bytes(int64_t cap) { return al16(4 * (cap + 1)); }
+__host__ __device__ __forceinline__ int64_t coo_stage_bytes(int64_t nnz, int64_t n, int64_t cap) {
+  return coo_raw_off(nnz, n) + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz) + al16(4 * nnz) + coo_cursor_bytes(cap);
 }
 
 // trace slots per CTA (bspmm_set_trace): 0 entry, 1 after PDL wait, 2 producer has unit-0 row
@@ -150,6 +155,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 // up to 2 chunks per lane; 4 chunks need ~128 registers -> 15 consumer warps
 constexpr int kMaxThreads(int ch) { return ch >= 4 ? 512 : 544; }
 constexpr int kMaxRegs(int ch) { return ch >= 4 ? 128 : 120; }
+// fused COO mode: kCooWarps warps (5 per SM sub-partition: 96 registers)
+constexpr int kMaxThreadsK(int ch, bool coo) { return coo ? 32 * kCooWarps : kMaxThreads(ch); }
+constexpr int kMaxRegsK(int ch, bool coo) { return coo ? 96 : kMaxRegs(ch); }
 
 struct __align__(16) UnitHdr {
   int64_t g0;     // first global row of the matrix
@@ -295,6 +303,10 @@ __device__ __forceinline__ uint64_t* early_bar(const SpmmParams& p, unsigned cha
 __device__ __forceinline__ uint64_t* sfull_bar(const SpmmParams& p, unsigned char* smem) {
   return reinterpret_cast<uint64_t*>(smem + p.stages * (kHdrBytes + 16) + 8);
 }
+// fused COO mode: per-stage "converted" barrier (one arrival per converter warp)
+__device__ __forceinline__ uint64_t* cvt_bar(const SpmmParams& p, unsigned char* smem) {
+  return reinterpret_cast<uint64_t*>(smem + p.stages * (kHdrBytes + 24) + 8);
+}
 template <bool VEC, bool COO>
 __device__ __forceinline__ bool early_b_ok(const SpmmParams& p, int32_t n, int32_t kw) {
   // whole contiguous B_i only (one 1-D bulk copy): with k-tiles (2-D boxes) it
@@ -350,7 +362,8 @@ __device__ __forceinline__ void issue_unit(const SpmmParams& p, const TmaMaps& m
     unsigned char* sreg = st + p.stage_b;
     if (COO) {  // fused COO mode: B tile (on full[s]) + the raw SparseTensor slice (on sfull[s])
       uint64_t* sfull = sfull_bar(p, smem);
-      const bool fits = (int64_t)n * kw * 4 <= p.stage_b && coo_stage_bytes(nnz, n) <= p.stage_s;
+      const bool fits = (int64_t)n * kw * 4 <= p.stage_b && n <= p.coo_rows &&
+                        coo_stage_bytes(nnz, n, p.coo_rows) <= p.stage_s;
       if (fits && n > 0) {
         if (lane == 0) mbar_expect_tx(&full[s], (uint32_t)n * (uint32_t)kw * 4u);
         __syncwarp();
@@ -970,9 +983,10 @@ __device__ __forceinline__ void rows_direct(const SpmmParams& p, const UnitHdr& 
 // Fused COO -> CSR of one staged unit (row a-2 inside the SpMM): counting
 // sort by row + rank of the unique key (col, original position) within each
 // row segment -- the same canonical order as coo2csr.cu, so the SpMM that
-// follows is bitwise identical to the two-kernel path.  Consumer warps only
-// (named barrier 1); writes the standard CSR slice layout of the stage.
-__device__ __forceinline__ void consumer_bar(int T) { asm volatile("bar.sync 1, %0;" ::"r"(T) : "memory"); }
+// follows is bitwise identical to the two-kernel path.  Converter warps only
+// (named barrier 2); writes the standard CSR slice layout of the stage.
+// (named barrier 2: the converter warps)
+__device__ __forceinline__ void consumer_bar(int T) { asm volatile("bar.sync 2, %0;" ::"r"(T) : "memory"); }
 
 __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& h, unsigned char* st, int t, int T,
                                             bool tr) {
@@ -981,22 +995,25 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
   unsigned char* raw = sreg + coo_raw_off(nnz, n);
   const int2* pr = reinterpret_cast<const int2*>(raw) + (z0 & 1);
   const float* rv = reinterpret_cast<const float*>(raw + coo_pairs_bytes(nnz)) + (z0 & 3);
-  int32_t* cursor = reinterpret_cast<int32_t*>(raw + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz));
-  int32_t* slot = cursor + al16(4 * (n + 1)) / 4;
+  int32_t* slot = reinterpret_cast<int32_t*>(raw + coo_pairs_bytes(nnz) + coo_vals_bytes(nnz));
+  int32_t* cursor = reinterpret_cast<int32_t*>(sreg + p.stage_s - coo_cursor_bytes(p.coo_rows));  // zero here
   int32_t* col = reinterpret_cast<int32_t*>(sreg) + (z0 & 3);
   float* val = reinterpret_cast<float*>(sreg + slice_region(nnz)) + (z0 & 3);
   int32_t* rp = reinterpret_cast<int32_t*>(sreg + 2 * slice_region(nnz)) + (h.g0 & 3);
-  for (int32_t r = t; r < n; r += T) cursor[r] = 0;
-  consumer_bar(T);
   for (int32_t e = t; e < nnz; e += T) atomicAdd(&cursor[pr[e].x], 1);
   consumer_bar(T);
   if (tr && t == 0) BSPMM_TRACE(p, 28);
-  // exclusive scan of the row counts: every consumer warp scans 32-row
-  // chunks, chunk totals go to `slot` (free until the scatter), then each
-  // thread adds the totals of the chunks before its own
+  // exclusive scan of the row counts into the row pointers, one phase: the
+  // warp that owns a 32-row chunk sums the counts of every row before it
+  // itself (no chunk-total exchange, no second barrier); the counts stay in
+  // `cursor` for the scatter
   const int32_t nchunk = (n + 31) >> 5;
   const int lt = t & 31;
   for (int32_t c = t >> 5; c < nchunk; c += T >> 5) {
+    int32_t base = 0;
+    for (int32_t q = lt; q < 32 * c; q += 32) base += cursor[q];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) base += __shfl_xor_sync(0xffffffffu, base, d);
     const int32_t r = c * 32 + lt;
     const int32_t v = r < n ? cursor[r] : 0;
     int32_t x = v;
@@ -1005,39 +1022,73 @@ __device__ __forceinline__ void coo_convert(const SpmmParams& p, const UnitHdr& 
       const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
       if (lt >= d) x += y;
     }
-    if (r < n) cursor[r] = x - v;                      // exclusive within the chunk
-    if (lt == 31) slot[c] = x;                         // chunk total
-  }
-  consumer_bar(T);
-  for (int32_t c = t >> 5; c < nchunk; c += T >> 5) {
-    int32_t base = 0;
-    for (int32_t q = lt; q < c; q += 32) base += slot[q];
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) base += __shfl_xor_sync(0xffffffffu, base, d);
-    const int32_t r = c * 32 + lt;
-    if (r < n) {
-      cursor[r] += base;
-      rp[r] = z0 + cursor[r];
-    }
+    if (r < n) rp[r] = z0 + base + x - v;
   }
   if (t == 0) rp[n] = z0 + nnz;
   consumer_bar(T);
   if (tr && t == 0) BSPMM_TRACE(p, 29);
-  for (int32_t e = t; e < nnz; e += T) slot[atomicAdd(&cursor[pr[e].x], 1)] = e;
+  // scatter into the row segments (any order within a segment: sorted next);
+  // the count is consumed downwards
+  for (int32_t e = t; e < nnz; e += T) {
+    const int32_t r = pr[e].x;
+    slot[rp[r] - z0 + atomicSub(&cursor[r], 1) - 1] = e;
+  }
   consumer_bar(T);
   if (tr && t == 0) BSPMM_TRACE(p, 30);
-  for (int32_t q = t; q < nnz; q += T) {
-    const int32_t e = slot[q];
-    const int2 rc = pr[e];
-    const int32_t s0 = rp[rc.x] - z0, s1 = rp[rc.x + 1] - z0;
-    int32_t rank = 0;
-    for (int32_t f = s0; f < s1; ++f) {
-      const int32_t fe = slot[f];
-      const int32_t cf = pr[fe].y;
-      rank += (cf < rc.y) || (cf == rc.y && fe < e);
+  // order within each row segment by the unique key (col, original position):
+  // a thread per row sorts up to 8 keys in registers (a sorting network; the
+  // molecule and paper-style graphs have <= 8 entries per row), longer rows
+  // rank each entry by counting smaller keys in its segment
+  for (int32_t r = t; r < n; r += T) {
+    const int32_t s0 = rp[r] - z0, s1 = rp[r + 1] - z0, d = s1 - s0;
+    if (d <= 8) {
+      // key = (col << 16) | position: unique, ordered as (col, position); both
+      // fit 16 bits (a stage holds < 2^16 rows and entries)
+      uint32_t key[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int32_t e = q < d ? slot[s0 + q] : 0;
+        key[q] = q < d ? ((uint32_t)pr[e].y << 16) | (uint32_t)e : 0xffffffffu;
+      }
+#define BSPMM_CX(a, b)                                   \
+      {                                                  \
+        const uint32_t lo = min(key[a], key[b]);         \
+        key[b] = max(key[a], key[b]);                    \
+        key[a] = lo;                                     \
+      }
+      if (d <= 4) {  // 4 keys: 5 compare-exchanges
+        BSPMM_CX(0, 1) BSPMM_CX(2, 3) BSPMM_CX(0, 2) BSPMM_CX(1, 3) BSPMM_CX(1, 2)
+      } else {       // Batcher's odd-even merge sort network, 8 keys (19)
+        BSPMM_CX(0, 1) BSPMM_CX(2, 3) BSPMM_CX(4, 5) BSPMM_CX(6, 7)
+        BSPMM_CX(0, 2) BSPMM_CX(1, 3) BSPMM_CX(4, 6) BSPMM_CX(5, 7)
+        BSPMM_CX(1, 2) BSPMM_CX(5, 6)
+        BSPMM_CX(0, 4) BSPMM_CX(1, 5) BSPMM_CX(2, 6) BSPMM_CX(3, 7)
+        BSPMM_CX(2, 4) BSPMM_CX(3, 5)
+        BSPMM_CX(1, 2) BSPMM_CX(3, 4) BSPMM_CX(5, 6)
+      }
+#undef BSPMM_CX
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < d) {
+          const int32_t e = (int32_t)(key[q] & 0xffffu);
+          col[s0 + q] = (int32_t)(key[q] >> 16);
+          val[s0 + q] = rv[e];  // bitwise move
+        }
+      }
+    } else {
+      for (int32_t q = s0; q < s1; ++q) {
+        const int32_t e = slot[q];
+        const int32_t ce = pr[e].y;
+        int32_t rank = 0;
+        for (int32_t f = s0; f < s1; ++f) {
+          const int32_t fe = slot[f];
+          const int32_t cf = pr[fe].y;
+          rank += (cf < ce) || (cf == ce && fe < e);
+        }
+        col[s0 + rank] = ce;
+        val[s0 + rank] = rv[e];
+      }
     }
-    col[s0 + rank] = rc.y;
-    val[s0 + rank] = rv[e];  // bitwise move
   }
   consumer_bar(T);
   if (tr && t == 0) BSPMM_TRACE(p, 31);
@@ -1052,7 +1103,7 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
   const int32_t stage_bytes = p.stage_b + p.stage_s;
   const int lane = threadIdx.x & 31;
   const int cw = (threadIdx.x >> 5) - 1;
-  const int W = (blockDim.x >> 5) - 1;
+  const int W = (blockDim.x >> 5) - 1 - (COO ? p.cvt_warps : 0);
   const int L = p.lanes;
   const int rpw = 32 / L;
   const int sub = lane / L, li = lane % L;
@@ -1100,9 +1151,8 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
     if (h.flags < 0) break;  // the producer's "done" header
     if (j == 0 && (h.flags & 8)) mbar_wait(early_bar(p, const_cast<unsigned char*>(smem)), 0u);  // early B tile
     const unsigned char* st = ring + (size_t)s * stage_bytes;
-    if (COO) {
-      if ((h.flags & 3) == 3)  // SparseTensor slice -> CSR slice in shared memory
-        coo_convert(p, h, const_cast<unsigned char*>(st), threadIdx.x - 32, W * 32, j == 0);
+    if (COO) {  // the converter warps' CSR slice, then the B tile
+      mbar_wait(&cvt_bar(p, const_cast<unsigned char*>(smem))[s], par);
       mbar_wait(&full[s], par);
     }
     const int reps = (p.dbg & 8) ? 4 : 1;  // debug: repeat the unit's work (consumer cost in isolation)
@@ -1127,23 +1177,57 @@ __device__ __forceinline__ void consume(const SpmmParams& p, const TmaMaps& maps
   if (cw == 0 && lane == 0) BSPMM_TRACE(p, 6);
 }
 
+// Fused COO mode: the converter warps walk the units in the consumers' order.
+// Unit j's SparseTensor slice is converted as soon as it lands (sfull), while
+// the consumer warps still compute unit j-1 -- the conversion leaves the
+// consumers' critical path except for a CTA's first unit.  Every unit's
+// "converted" barrier is arrived on (also units that need no conversion), so
+// its phases stay in step with the ring.
+__device__ __forceinline__ void convert_units(const SpmmParams& p, unsigned char* smem, int W) {
+  const UnitHdr* hdr = reinterpret_cast<const UnitHdr*>(smem);
+  unsigned char* ring = smem + ring_prefix_bytes(p.stages);
+  const int32_t stage_bytes = p.stage_b + p.stage_s;
+  const int t = threadIdx.x - 32 * (1 + W);
+  for (int j = 0;; ++j) {
+    const int s = j % p.stages;
+    const uint32_t par = (uint32_t)(j / p.stages) & 1u;
+    mbar_wait(&sfull_bar(p, smem)[s], par);
+    const UnitHdr h = hdr[s];
+    if (h.flags < 0) break;  // the producer's "done" header
+    if ((h.flags & 3) == 3)  // SparseTensor slice -> CSR slice in shared memory
+      coo_convert(p, h, ring + (size_t)s * stage_bytes, t, p.cvt_warps * 32, j == 0);
+    __syncwarp();
+    if ((t & 31) == 0) mbar_arrive(&cvt_bar(p, smem)[s]);
+  }
+}
+
 template <int CH, bool VEC, int EPI, bool COO, bool ONE = false>
-__global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(kMaxThreadsK(CH, COO), 1) __maxnreg__(kMaxRegsK(CH, COO)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * kHdrBytes);
   uint64_t* empty = full + p.stages;
   if (threadIdx.x == 0) BSPMM_TRACE(p, 0);
   if (threadIdx.x == 0) {
-    const uint32_t W = (blockDim.x >> 5) - 1;
+    const uint32_t W = (blockDim.x >> 5) - 1 - (COO ? p.cvt_warps : 0);
     for (int s = 0; s < p.stages; ++s) {
       // producer lane-0 arrive + 32 cp.async arrivals; fused COO mode: the
       // cp.async arrivals go to the slice barrier, full[s] tracks the B tile
       mbar_init(&full[s], COO ? 1 : 1 + 32);
       if (COO) mbar_init(&sfull_bar(p, smem)[s], 1 + 32);
+      if (COO) mbar_init(&cvt_bar(p, smem)[s], p.cvt_warps);
       mbar_init(&empty[s], W);      // one arrival per consumer warp
     }
     mbar_init(early_bar(p, smem), 1);  // the first unit's early B tile
     fence_mbar_init();
+  }
+  if (COO) {  // the per-row counters of every stage start at zero (coo_cursor_bytes)
+    unsigned char* ring = smem + ring_prefix_bytes(p.stages);
+    const int32_t stage_bytes = p.stage_b + p.stage_s;
+    const int32_t nc = (int32_t)(coo_cursor_bytes(p.coo_rows) / 4);
+    for (int s = 0; s < p.stages; ++s) {
+      int32_t* cur = reinterpret_cast<int32_t*>(ring + (size_t)s * stage_bytes + p.stage_b + p.stage_s) - nc;
+      for (int32_t r = threadIdx.x; r < nc; r += blockDim.x) cur[r] = 0;
+    }
   }
   __syncthreads();
   // programmatic dependent launch: everything above overlapped the previous
@@ -1151,8 +1235,10 @@ __global__ void __launch_bounds__(kMaxThreads(CH), 1) __maxnreg__(kMaxRegs(CH)) 
   pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
+  const int Wc = (blockDim.x >> 5) - 1 - (COO ? p.cvt_warps : 0);
   if ((threadIdx.x >> 5) == 0) produce<VEC, COO>(p, maps, smem);
-  else consume<CH, VEC, EPI, COO, ONE>(p, maps, smem);
+  else if (!COO || (int)(threadIdx.x >> 5) <= Wc) consume<CH, VEC, EPI, COO, ONE>(p, maps, smem);
+  else convert_units(p, smem, Wc);
   if (p.trace) {
     __syncthreads();
     if (threadIdx.x == 0) BSPMM_TRACE(p, 7);
@@ -1251,6 +1337,8 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.nnz_off = a.coo_nnz_off;
   sp.idx = a.coo_idx;
   sp.err = a.err;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
+  sp.cvt_warps = a.cvt_warps;
+  sp.coo_rows = plan.max_rows;
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {
