@@ -654,7 +654,16 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
   GcnPlan L;
   // debug bits 20-21: feature-tile width override (1: 64, 2: 128, 3: 256)
   const int32_t nt_ovr = ((h->dbg >> 20) & 3) ? (32 << ((h->dbg >> 20) & 3)) : 0;
-  if (!plan_gcn(channels, n_x, k, N, h->hint_rows, h->smem_optin, h->gcn_math, h->num_sms, nt_ovr, &L))
+  // CTA pairs (tcgen05 cta_group::2, M = 256, each CTA staging half of W) for
+  // the fp32 (3xTF32) layer over many row tiles: 65536 graphs 27.0-27.1 vs
+  // 27.4-28.2 ms; the one-pass modes and small batches measured slower with
+  // pairs (TF32 20.8 vs 17.3 ms; Reaction100-like 92.8 vs 70.7 us), so they
+  // keep one CTA per tile.  Debug bit 1<<22 forces pairs, 1<<23 single CTAs.
+  const bool big = (N + 127) / 128 >= 4LL * h->num_sms;
+  int32_t cg = (h->gcn_math == BSPMM_GCN_FP32 && big) ? 2 : 1;
+  if (h->dbg & (1 << 22)) cg = 2;
+  if (h->dbg & (1 << 23)) cg = 1;
+  if (!plan_gcn(channels, n_x, k, N, h->hint_rows, h->smem_optin, h->gcn_math, h->num_sms, nt_ovr, cg, &L))
     return fail(h, BSPMM_ERROR_NOT_SUPPORTED, "bspmm_gcn_layer: no shared-memory plan for these sizes");
   // X needs a 16-byte row pitch and base for TMA; otherwise a packed copy
   const bool x_ok = (ldx % 4 == 0) && aligned16(X);
@@ -673,9 +682,9 @@ BSPMM_API bspmm_status_t bspmm_gcn_layer(bspmm_handle_t h, int32_t batch, int32_
   const float* Xk = x_ok ? X : reinterpret_cast<const float*>(wsb + o_x);
   CUtensorMap mx, mhi, mlo;
   if (!encode_2d(&mx, Xk, (uint64_t)n_x, (uint64_t)N, (uint64_t)ldxp * 4, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_2d(&mhi, whi, (uint64_t)L.ktot, (uint64_t)k, (uint64_t)L.ktot * 4, 32, (uint32_t)L.nt,
+      !encode_2d(&mhi, whi, (uint64_t)L.ktot, (uint64_t)k, (uint64_t)L.ktot * 4, 32, (uint32_t)(L.nt / L.cg),
                  CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_2d(&mlo, wlo, (uint64_t)L.ktot, (uint64_t)k, (uint64_t)L.ktot * 4, 32, (uint32_t)L.nt,
+      !encode_2d(&mlo, wlo, (uint64_t)L.ktot, (uint64_t)k, (uint64_t)L.ktot * 4, 32, (uint32_t)(L.nt / L.cg),
                  CU_TENSOR_MAP_SWIZZLE_128B))
     return fail(h, BSPMM_ERROR_CUDA, "bspmm_gcn_layer: TMA descriptor encoding failed");
   if (!x_ok) {

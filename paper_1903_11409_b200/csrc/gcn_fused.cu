@@ -84,7 +84,15 @@ struct GcnMaps {
 
 __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
-template <int NG>
+// CG = 2: a CTA pair (cluster of two) per 256-row tile -- each CTA forms the
+// Z operand of its 128 rows in its own TMEM and stages HALF of the W block
+// (nt / 2 output features) in its shared memory; the leader's single thread
+// issues tcgen05.mma.cta_group::2 (M = 256), which reads both CTAs' Z and both
+// W halves, so each SM's tensor core reads half the W bytes per K step from
+// its shared memory.  Both CTAs' W loads complete on the leader's barrier; the
+// peer's Z producers arrive on the leader's Z barrier; the leader's commits
+// arrive on both CTAs' barriers.
+template <int NG, int CG>
 __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const GcnParams p,
                                                                      const __grid_constant__ GcnMaps m) {
   constexpr int kGGroups = NG;
@@ -99,8 +107,12 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
   __shared__ int32_t s_xrows, s_staged_x, s_staged_s;
   __shared__ int32_t s_ebase[33];       // per channel: first staged entry (channels <= 32 staged)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t tm = (int32_t)(blockIdx.x / (uint32_t)p.ntiles_n);
-  const int32_t tn = (int32_t)(blockIdx.x - (uint32_t)tm * (uint32_t)p.ntiles_n);
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const uint32_t pair = CG == 2 ? blockIdx.x >> 1 : blockIdx.x;
+  const int32_t tmp = (int32_t)(pair / (uint32_t)p.ntiles_n);
+  const int32_t tn = (int32_t)(pair - (uint32_t)tmp * (uint32_t)p.ntiles_n);
+  const int32_t tm = CG == 2 ? 2 * tmp + (int32_t)rank : tmp;
+  const bool has_rows = tm < p.tiles_m;  // CG = 2, odd tile count: the last pair's second CTA has none
   const int64_t r0 = (int64_t)tm * kGM;
   const int32_t n0 = tn * p.nt;
   uint64_t* w_full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
@@ -120,24 +132,34 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.ws; ++s) mbar_init(&w_full[s], 1), mbar_init(&w_empty[s], 1);
-    for (int s = 0; s < p.zs; ++s) mbar_init(&z_full[s], kGMath), mbar_init(&z_empty[s], 1);
+    for (int s = 0; s < p.zs; ++s) mbar_init(&z_full[s], kGMath * CG), mbar_init(&z_empty[s], 1);
     for (int s = 0; s < p.xs; ++s) mbar_init(&x_full[s], 1), mbar_init(&x_empty[s], kGGroups * kGMath);
     mbar_init(acc_full, 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane < 3) prefetch_tensormap(lane == 0 ? (const void*)&m.x : lane == 1 ? (const void*)&m.whi : (const void*)&m.wlo);
-  if (warp == 1) tmem_alloc(&s_tmem, tmem_cols);
+  if (warp == 1) {
+    if (CG == 2) tmem_alloc2(&s_tmem, tmem_cols);
+    else tmem_alloc(&s_tmem, tmem_cols);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // the peer's barriers exist before any remote arrive / copy
   tc_fence_after();
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ---- tile setup: the graphs covering rows [r0, r0 + 128), the X halo, the structure
-  const int32_t rows_in = (int32_t)(p.N - r0 < kGM ? p.N - r0 : kGM);
+  const int32_t rows_in = !has_rows ? 0 : (int32_t)(p.N - r0 < kGM ? p.N - r0 : kGM);
   for (int r = threadIdx.x; r < kGM; r += kGThreads) rbase[r] = -1;
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 2 && !has_rows) {
+    if (lane == 0) {
+      s_xlo = 0;
+      s_xrows = 0;
+      s_staged_x = 1;
+    }
+  } else if (warp == 2) {
     const int32_t g0 = p.gfirst[tm];
     const int64_t xlo = p.row_off[g0];
     int64_t xhi = xlo;
@@ -170,7 +192,7 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
     for (int32_t c0 = 0; c0 < p.channels; c0 += 32) {
       const int32_t ch = c0 + lane;
       int32_t cnt = 0;
-      if (ch < p.channels) {
+      if (ch < p.channels && has_rows) {
         const int32_t* rp = p.row_ptr + (int64_t)ch * (p.N + 1) + r0;
         cnt = rp[rows_in] - rp[0];
       }
@@ -190,7 +212,7 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
   }
   __syncthreads();
   const bool staged_s = s_staged_s != 0;
-  if (staged_s && warp >= 2) {  // the math warps stage row pointers, columns and values
+  if (staged_s && warp >= 2 && has_rows) {  // the math warps stage row pointers, columns and values
     const int mt = threadIdx.x - 64, MT = kGThreads - 64;
     for (int32_t ch = 0; ch < p.channels; ++ch) {
       const int32_t* rp = p.row_ptr + (int64_t)ch * (p.N + 1) + r0;
@@ -222,14 +244,25 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
     if (lane == 0) {
       int wsi = 0, xsi = 0;
       uint32_t wph = 0, xph = 0;
+      // CG = 2: this CTA's half of the W block (nt / 2 features), its bytes
+      // completing on the leader's barrier, which the leader arms for both halves
       const uint32_t wbytes = (uint32_t)p.nt * 128u * (p.mode == 0 ? 2u : 1u);
+      const int32_t nh = p.nt / CG;
       const int32_t nbox = (s_xrows + kXBox - 1) / kXBox;
       auto issue_w = [&](int32_t kcoord) {
         mbar_wait(&w_empty[wsi], wph ^ 1u);
         unsigned char* st = smem + p.off_w + (size_t)wsi * p.w_stage;
-        mbar_arrive_expect_tx(&w_full[wsi], wbytes);
-        tma_load_2d(st, &m.whi, kcoord, n0, &w_full[wsi]);
-        if (p.mode == 0) tma_load_2d(st + (size_t)p.nt * 128, &m.wlo, kcoord, n0, &w_full[wsi]);
+        if (CG == 2) {
+          const uint32_t lb = mapa_rank(&w_full[wsi], 0);
+          if (rank == 0) mbar_arrive_expect_tx(&w_full[wsi], wbytes);
+          const int32_t y = n0 + (int32_t)rank * nh;
+          tma2_load_2d(st, &m.whi, kcoord, y, lb);
+          if (p.mode == 0) tma2_load_2d(st + (size_t)nh * 128, &m.wlo, kcoord, y, lb);
+        } else {
+          mbar_arrive_expect_tx(&w_full[wsi], wbytes);
+          tma_load_2d(st, &m.whi, kcoord, n0, &w_full[wsi]);
+          if (p.mode == 0) tma_load_2d(st + (size_t)p.nt * 128, &m.wlo, kcoord, n0, &w_full[wsi]);
+        }
         if (++wsi == p.ws) wsi = 0, wph ^= 1u;
       };
       for (int32_t xb = 0; xb < p.nxb; ++xb) {
@@ -248,8 +281,8 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
       for (int32_t j = 0; j < p.nbias; ++j) issue_w(p.channels * p.KX + j * kGK);
     }
   } else if (warp == 1) {
-    // ======== MMA issuer (one thread) ========
-    if (lane == 0) {
+    // ======== MMA issuer (one thread; CG = 2: the leader CTA's) ========
+    if (lane == 0 && (CG == 1 || rank == 0)) {
       const uint32_t d = s_tmem;
       int wsi = 0, zsi = 0;
       uint32_t wph = 0, zph = 0;
@@ -258,22 +291,36 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
         mbar_wait(&z_full[zsi], zph);
         tc_fence_after();
         unsigned char* ws = smem + p.off_w + (size_t)wsi * p.w_stage;
-        const uint64_t wh = smem_desc_sw128(ws), wl = smem_desc_sw128(ws + (size_t)p.nt * 128);
+        const uint64_t wh = smem_desc_sw128(ws), wl = smem_desc_sw128(ws + (size_t)(p.nt / CG) * 128);
         const uint32_t zh = d + kZCol + (uint32_t)zsi * (p.mode == 0 ? 64u : 32u), zl = zh + 32u;
 #pragma unroll
         for (int j = 0; j < kGK / 8 && !(p.dbg & 2); ++j) {  // UMMA_K = 8: 8 TMEM columns of A, +32 bytes of B
-          mma_tf32_ts(d, zh + 8 * j, wh + 2 * j, p.idesc, (kb | j) != 0);
-          if (p.mode == 0) {
-            mma_tf32_ts(d, zh + 8 * j, wl + 2 * j, p.idesc, 1u);
-            mma_tf32_ts(d, zl + 8 * j, wh + 2 * j, p.idesc, 1u);
+          if (CG == 2) {
+            mma2_tf32_ts(d, zh + 8 * j, wh + 2 * j, p.idesc, (kb | j) != 0);
+            if (p.mode == 0) {
+              mma2_tf32_ts(d, zh + 8 * j, wl + 2 * j, p.idesc, 1u);
+              mma2_tf32_ts(d, zl + 8 * j, wh + 2 * j, p.idesc, 1u);
+            }
+          } else {
+            mma_tf32_ts(d, zh + 8 * j, wh + 2 * j, p.idesc, (kb | j) != 0);
+            if (p.mode == 0) {
+              mma_tf32_ts(d, zh + 8 * j, wl + 2 * j, p.idesc, 1u);
+              mma_tf32_ts(d, zl + 8 * j, wh + 2 * j, p.idesc, 1u);
+            }
           }
         }
-        mma_commit(&w_empty[wsi]);
-        mma_commit(&z_empty[zsi]);
+        if (CG == 2) {
+          mma2_commit_both(&w_empty[wsi]);
+          mma2_commit_both(&z_empty[zsi]);
+        } else {
+          mma_commit(&w_empty[wsi]);
+          mma_commit(&z_empty[zsi]);
+        }
         if (++wsi == p.ws) wsi = 0, wph ^= 1u;
         if (++zsi == p.zs) zsi = 0, zph ^= 1u;
       }
-      mma_commit(acc_full);
+      if (CG == 2) mma2_commit_both(acc_full);
+      else mma_commit(acc_full);
     }
   } else {
     // ======== math warps: Z = [A_ch X | rowsums] block by block ========
@@ -301,6 +348,11 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
     };
     // Z row -> TMEM stage zsi (hi = TF32 truncation, lo = the fp32 remainder in
     // 3xTF32; BF16 mode: rounded to BF16), then make it visible to the MMA
+    // the Z stage is ready: arrive on the MMA issuer's barrier (CG = 2: the leader's)
+    auto z_arrive = [&](int zsi_) {
+      if (CG == 2) mbar_arrive_cluster(mapa_rank(&z_full[zsi_], 0));
+      else mbar_arrive(&z_full[zsi_]);
+    };
     auto put_row = [&](int zsi_, float (&z)[32]) {
       const uint32_t col = kZCol + (uint32_t)zsi_ * (p.mode == 0 ? 64u : 32u);
       if (p.mode == 0) {
@@ -400,7 +452,7 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
         }
         put_row(zsi, z);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&z_full[zsi]);
+        if (lane == 0) z_arrive(zsi);
       }
       // both groups release every X block (a group with no K block in it too;
       // the X ring then never runs ahead of either)
@@ -428,7 +480,7 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
       }
       put_row(zsi, z);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&z_full[zsi]);
+      if (lane == 0) z_arrive(zsi);
     }
     // ======== epilogue: TMEM -> registers -> Y ========
     mbar_wait(acc_full, 0);
@@ -459,7 +511,12 @@ __global__ void __launch_bounds__(gcn_threads(NG), 1) gcn_fused_kernel(const Gcn
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(s_tmem, tmem_cols);
+  if (CG == 2) {
+    cluster_sync_all();  // neither CTA frees its TMEM while the pair's MMAs may read it
+    if (warp == 1) tmem_dealloc2(s_tmem, tmem_cols);
+  } else if (warp == 1) {
+    tmem_dealloc(s_tmem, tmem_cols);
+  }
 }
 
 // ---- preparation: W -> K-major (transposed, padded, split), bias rows, and
@@ -539,8 +596,9 @@ __global__ void __launch_bounds__(256) gcn_pack_x_kernel(const float* __restrict
 }
 
 bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_rows, int32_t smem_optin, int32_t mode,
-              int32_t num_sms, int32_t nt_override, GcnPlan* out) {
+              int32_t num_sms, int32_t nt_override, int32_t cg, GcnPlan* out) {
   GcnPlan L{};
+  L.cg = cg == 2 ? 2 : 1;
   L.KX = (n_x + kGK - 1) / kGK * kGK;
   L.nxb = L.KX / kGK;
   L.nbias = (channels + 31) / 32;
@@ -554,11 +612,12 @@ bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_r
   L.nt = k > 128 ? 256 : (k > 64 ? 128 : (k > 32 ? 64 : 32));
   if (L.nt == 256 && (int64_t)L.tiles_m * ((k + 255) / 256) < num_sms) L.nt = 128;
   if (nt_override >= 32 && nt_override <= 256) L.nt = nt_override;
+  if (L.cg == 2 && L.nt < 64) L.cg = 1;  // a CTA pair splits the features: nt / 2 >= 32 (one 128-byte row group)
   L.ntiles_n = (k + L.nt - 1) / L.nt;
   const int64_t R = max_rows > 0 ? max_rows : 64;
   L.xr = (int32_t)std::min<int64_t>(256, (kGM + 2 * (R - 1) + kXBox - 1) / kXBox * kXBox);
   const int32_t split = mode == 0 ? 2 : 1;
-  L.w_stage = L.nt * 128 * split;
+  L.w_stage = L.nt / L.cg * 128 * split;  // CG = 2: this CTA's half of the features
   L.z_stage = 0;  // Z lives in TMEM (32 columns per stage and split part)
   L.x_stage = L.xr * 128;
   L.ws = 4;
@@ -598,8 +657,10 @@ bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_r
     layout();
   }
   if (L.smem > smem_optin) return false;
-  // instruction descriptor: D fp32, A = B = TF32, both K-major, M = 128, N = nt
-  L.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L.nt >> 3) << 17) | ((uint32_t)(kGM >> 4) << 24);
+  // instruction descriptor: D fp32, A = B = TF32, both K-major, M = 128 (256
+  // for a CTA pair), N = nt
+  L.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(L.nt >> 3) << 17) |
+            ((uint32_t)((kGM * L.cg) >> 4) << 24);
   *out = L;
   return true;
 }
@@ -687,16 +748,20 @@ cudaError_t launch_gcn_fused(const GcnPlan& L, const GcnArgs& a, cudaStream_t s)
   // a third group measured 6% slower), the one-pass modes 3; debug bit
   // 524288 swaps
   const int ng = ((a.mode == 0) != ((a.dbg & 4) != 0)) ? 2 : 3;
-  auto kern = ng == 2 ? gcn_fused_kernel<2> : gcn_fused_kernel<3>;
-  static thread_local int configured[2][64] = {};
+  const int cg = L.cg;
+  auto kern = cg == 2 ? (ng == 2 ? gcn_fused_kernel<2, 2> : gcn_fused_kernel<3, 2>)
+                      : (ng == 2 ? gcn_fused_kernel<2, 1> : gcn_fused_kernel<3, 1>);
+  const int ki = (ng - 2) + 2 * (cg - 1);
+  static thread_local int configured[4][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (configured[ng - 2][dev & 63] < L.smem) {
+  if (configured[ki][dev & 63] < L.smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
-    configured[ng - 2][dev & 63] = L.smem;
+    configured[ki][dev & 63] = L.smem;
   }
-  const int64_t grid = (int64_t)L.tiles_m * L.ntiles_n;
+  // CG = 2: pairs of CTAs (tile rows 2t, 2t + 1) per feature tile
+  const int64_t grid = cg == 2 ? 2 * ((int64_t)(L.tiles_m + 1) / 2) * L.ntiles_n : (int64_t)L.tiles_m * L.ntiles_n;
   if (grid == 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
@@ -704,11 +769,15 @@ cudaError_t launch_gcn_fused(const GcnPlan& L, const GcnArgs& a, cudaStream_t s)
   cfg.blockDim = dim3(gcn_threads(ng));
   cfg.dynamicSmemBytes = L.smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cg;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = cg == 2 ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, p, maps);
 }
 

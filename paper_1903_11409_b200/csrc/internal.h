@@ -100,6 +100,7 @@ cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t
 // fused GCN layer on tcgen05 (gcn_fused.cu)
 struct GcnPlan {
   int32_t KX, nxb, nbias, ktot, nt, ntiles_n, tiles_m, xr, cap_e;
+  int32_t cg;  // 1: one CTA per 128-row tile; 2: a CTA pair per 256 rows (tcgen05 cta_group::2)
   int32_t ws, zs, xs, w_stage, z_stage, x_stage;
   int32_t off_w, off_z, off_x, off_rp, off_col, off_val, off_rb, off_bar, smem;
   uint32_t idesc;
@@ -122,7 +123,7 @@ struct GcnArgs {
   const CUtensorMap* map_wlo;
 };
 bool plan_gcn(int32_t channels, int32_t n_x, int32_t k, int64_t N, int32_t max_rows, int32_t smem_optin, int32_t mode,
-              int32_t num_sms, int32_t nt_override, GcnPlan* out);
+              int32_t num_sms, int32_t nt_override, int32_t cg, GcnPlan* out);
 cudaError_t launch_gcn_prep(const GcnPlan& L, int32_t batch, int32_t channels, int32_t n_x, int32_t k, int64_t N,
                             int32_t mode, const float* W, const float* bias, float* whi, float* wlo,
                             const int64_t* row_off, int32_t* gfirst, cudaStream_t s);

@@ -180,6 +180,22 @@ def test_gcn_sass_uses_tcgen05():
         assert mnem in body, mnem
 
 
+def test_gcn_cta_pair_sass():
+    """The CTA-pair instantiation of the fused layer issues the 2-SM MMA
+    (UTCHMMA.2CTA), its multicast commit (UTCBAR.2CTA.MULTICAST), 2-SM tensor
+    TMA (UTMALDG.2D.2CTA) and the pair TMEM allocation."""
+    import os
+    import re
+    import subprocess
+    lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1903_11409_b200", "libbspmm.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
+    m = re.search(r"Function : \S*gcn_fused_kernelILi2ELi2E", out)
+    assert m, "no CTA-pair instantiation of gcn_fused_kernel"
+    body = out[m.start():out.find("Function :", m.start() + 20)]
+    for mnem in ("UTCHMMA.2CTA", "UTCBAR.2CTA.MULTICAST", "UTMALDG.2D.2CTA", "UTCATOMSWS.2CTA"):
+        assert mnem in body, mnem
+
+
 def test_hot_kernels_do_not_spill():
     """The CSR pipeline's plain-store instantiations (the bench path), the tile
     kernel and the fused GCN kernel keep everything in registers: a code change

@@ -31,10 +31,15 @@ pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda", 0)
 
 
-@pytest.fixture(scope="module")
-def h():
+# every test runs twice: one CTA per 128-row tile (debug bit 1<<23) and CTA
+# pairs (debug bit 1<<22: tcgen05 cta_group::2, M = 256, W split across the
+# pair; the default for the fp32 layer over >= 4 x 148 row tiles)
+@pytest.fixture(scope="module", params=[1 << 23, 1 << 22], ids=["cta1", "cta_pair"])
+def h(request):
     assert torch.cuda.is_available()
-    return bs.Handle(0)
+    hd = bs.Handle(0)
+    hd.set_debug(request.param)
+    return hd
 
 
 def T(a):
