@@ -80,6 +80,18 @@ def main():
     h.set_hints(0, 0)
     h.gcn_layer(T(bl.row_off), None, T(bl.row_ptr[None]), T(bl.col), T(bl.vals),
                 torch.randn((bl.n_rows, 40), device=dev), torch.randn((1, 40, 72), device=dev))
+    # CTA pairs (tcgen05 cta_group::2; debug bit 1<<22): every precision mode,
+    # an odd row-tile count (the last pair's second CTA has no rows), k = 512
+    b = synth.config(2)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    h.set_debug(dbg0 | (1 << 22))
+    X = torch.randn((b.n_rows, 64), device=dev)
+    for mode in ("fp32", "tf32", "bf16"):
+        h.set_gcn_math(mode)
+        h.gcn_layer(T(b.row_off), None, rps, T(b.col), T(b.vals), X, torch.randn((2, 64, 512), device=dev),
+                    torch.randn((2, 512), device=dev))
+    h.set_gcn_math("fp32")
+    h.set_debug(dbg0)
     torch.cuda.synchronize()
     # handle state across two streams (set_stream hand-off)
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
