@@ -227,3 +227,16 @@ def test_gcn_accumulate_writes_each_element_once(h, cid):
                 T(np.stack([np.eye(k, dtype=np.float32)] * channels)), Y=Yd)
     AX = oracle.spmm_f32(k, b.row_off, None, b.row_ptr, b.col, b.vals, X)
     assert np.array_equal(Yd.cpu().numpy(), channels * AX)
+
+
+def test_gcn_big_batch_default_policy():
+    """The planner's default at a batch large enough for CTA pairs (4096
+    molecule-like graphs = ~1280 row tiles >= 4 x 148): the fp32 layer runs on
+    tcgen05 cta_group::2, the TF32 layer on single CTAs; both within their
+    derived bounds everywhere, every element written once."""
+    hd = bs.Handle(0)
+    b = synth.generate(synth.MOL, (20, 60, 0, 0), 4096, 8, seed=21, dense=False)
+    assert (b.n_rows + 127) // 128 >= 4 * 148
+    hd.set_hints(int(b.sizes.max()), 0)
+    run_case(hd, b, 2, 64, 256, np.random.default_rng(21))
+    run_case(hd, b, 2, 64, 256, np.random.default_rng(22), mode="tf32")
