@@ -341,17 +341,19 @@ bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int3
     layout(cb, L);
   } else {
     // widest tiles that still give >= 8 tiles per SM (overlap between the CTAs
-    // of an SM), and a B tile of at most 32 KB; narrower than 8 float4 (128-byte
-    // rows, the 2-D TMA path) the pipeline kernel is faster (config 2: 3.9 vs
-    // 3.7 us, tools/kbench.py)
+    // of an SM), and a B tile of at most 32 KB, but no narrower than 2 float4
+    // (32-byte rows) -- with cp.async staging the narrow blocks beat the
+    // pipeline on small batches (config 2: cb 2 = 800 tiles 3.38 us, cb 4 3.58,
+    // cb 1 3.90, the pipeline 3.81; config 4: cb 8 6.66, cb 16 6.98, cb 4 8.51;
+    // tools/probe/tile_balance.py)
     int32_t cb = 1;
     while (cb < 32 && cb < k4) cb <<= 1;
     layout(cb, L);
-    while (cb > 1 && (L.units < 8LL * num_sms || R * cb * 16 > 32768)) {
+    while (cb > 2 && (L.units < 8LL * num_sms || R * cb * 16 > 32768)) {
       cb >>= 1;
       layout(cb, L);
     }
-    if (cb < 8) return false;
+    if (cb < 2) return false;
   }
   if (L.smem > 200 * 1024 || L.per_sm < 1) return false;
   // one wave: every tile resident at once (beyond that the persistent
