@@ -589,6 +589,36 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
   // request for the built CSR.
   const bool aligned = (k % 4 == 0) && (ldb % 4 == 0) && (ldc % 4 == 0) && aligned16(B) && aligned16(C);
   if (!out_given && aligned && h->hint_rows > 0 && h->hint_nnz > 0 && !(h->flags & BSPMM_VALIDATE)) {
+    // small batches (every tile resident at once): the tile kernel's SparseTensor
+    // variant (spmm_tile.cu, each tile CTA converts its matrix while its B tile
+    // lands); debug bit 16384 keeps the pipeline's converter warps
+    TileLayout TL;
+    const bool tuned = h->tune_kt || h->tune_warps || h->tune_ctas || h->tune_chunks;
+    if (!tuned && !(h->dbg & (16384 | 128)) &&
+        plan_tile(batch, k, h->hint_rows, h->hint_nnz, h->num_sms, h->tune_tile_cb, &TL, /*coo=*/true)) {
+      bspmm_plan_t plan{};
+      plan.kernel = 1;
+      plan.kt = 4 * TL.cb;
+      plan.tiles = TL.tiles;
+      plan.lanes = TL.cb;
+      plan.vec = 1;
+      plan.chunks = 1;
+      plan.stages = 1;
+      plan.units = TL.units;
+      plan.grid = (int32_t)TL.units;
+      plan.threads = 128;
+      plan.smem_bytes = TL.smem;
+      plan.max_rows = h->hint_rows;
+      h->last_plan = plan;
+      CsrArgs a{batch, k, ro, sizes, nullptr, nullptr, vals, B, ldb, C, ldc, h->trace, h->dbg, nullptr};
+      a.coo_nnz_off = nnz_off;
+      a.coo_idx = idx;
+      a.err = h->dev_flag;
+      CK(h, launch_spmm_tile(a, TL, h->stream));
+      h->launches++;
+      h->coo_fused_pending = true;
+      return BSPMM_SUCCESS;
+    }
     bspmm_plan_t plan;
     st = make_plan(k, batch, true, h->hint_rows, h->hint_nnz, h->num_sms, h->smem_optin, h->tune_kt, h->tune_warps,
                    h->tune_ctas, h->tune_chunks, &plan, /*coo=*/true);

@@ -92,10 +92,11 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
 struct TileLayout {
   int32_t cb, tiles, per_sm, smem;
   int32_t cap_rows, cap_nnz, rp_off, col_off, val_off;
+  int32_t pair_off = 0, cval_off = 0, slot_off = 0, cnt_off = 0;  // SparseTensor conversion scratch
   int64_t units;
 };
 bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int32_t num_sms, int32_t cb_override,
-               TileLayout* out);
+               TileLayout* out, bool coo = false);
 cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t s);
 // fused GCN layer on tcgen05 (gcn_fused.cu)
 struct GcnPlan {

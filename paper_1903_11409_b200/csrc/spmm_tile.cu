@@ -64,6 +64,12 @@ struct TileParams {
   int32_t rp_first;                 // 1: the row-pointer round trip is issued before the B tile
   int32_t dbg_bits;                 // 1: no TMA descriptor prefetch
   unsigned long long* trace;        // debug: per-CTA phase timestamps (globaltimer ns), or null
+  // SparseTensor input (spmm_tile_coo_kernel): per-matrix entry offsets, local
+  // (row, col) pairs, values; scratch for the conversion after val_off
+  const int64_t* __restrict__ nnz_off;
+  const int32_t* __restrict__ idx;
+  int32_t pair_off, cval_off, slot_off, cnt_off;
+  int* err;                         // bit 64: a matrix beyond the hinted capacity (skipped)
 };
 
 __device__ __forceinline__ void tile_trace(const TileParams& p, int slot) {
@@ -311,10 +317,156 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
   }
 }
 
+// SparseTensor input on the tile kernel (row a-2 fused, small batches): each
+// tile CTA converts its matrix's unsorted (row, col) slice to the canonical
+// CSR order (row, col, original position) in shared memory -- the order of
+// coo2csr.cu and of the pipeline's converter warps, so the same bits -- while
+// its B tile is still landing: the raw slice is the first cp.async group, the
+// tile the second, and the conversion waits only for the first.  A matrix is
+// converted once per column block (L2 serves the repeats; C2: 8 CTAs x ~130
+// entries).  Conversion: row histogram (shared atomics), a warp scan into the
+// row pointers, scatter into the row segments (counts consumed downwards),
+// then a thread per row orders its segment by the key (col << 16) | position
+// (a sorting network up to 8 entries, rank counting beyond).
+template <int CB>
+__global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float4* Bs = reinterpret_cast<float4*>(smem);
+  int32_t* rp_s = reinterpret_cast<int32_t*>(smem + p.rp_off);
+  int32_t* col_s = reinterpret_cast<int32_t*>(smem + p.col_off);
+  float* val_s = reinterpret_cast<float*>(smem + p.val_off);
+  int2* pr = reinterpret_cast<int2*>(smem + p.pair_off);
+  float* rv = reinterpret_cast<float*>(smem + p.cval_off);
+  int32_t* slot = reinterpret_cast<int32_t*>(smem + p.slot_off);
+  int32_t* cnt = reinterpret_cast<int32_t*>(smem + p.cnt_off);
+  const int t = threadIdx.x;
+  const int32_t i = (int32_t)(blockIdx.x / (uint32_t)p.tiles);
+  const int32_t c0 = (int32_t)(blockIdx.x - (uint32_t)i * (uint32_t)p.tiles) * CB;
+  const int32_t cw = min(CB, p.k4 - c0);
+  tile_trace(p, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  tile_trace(p, 1);
+  // ---- RT1: where the matrix and its entries live (independent loads)
+  const int64_t g0 = p.row_off[i];
+  const int32_t n = p.sizes ? __ldg(p.sizes + i) : (int32_t)(p.row_off[i + 1] - g0);
+  const int64_t z0 = p.nnz_off[i];
+  const int32_t nz = (int32_t)(p.nnz_off[i + 1] - z0);
+  if (n <= 0) return;
+  if (n > p.cap_rows || nz > p.cap_nnz) {  // beyond the hints: skipped, reported by bspmm_sync
+    if (t == 0) atomicOr(p.err, 64);
+    return;
+  }
+  tile_trace(p, 2);
+  // ---- the raw slice (group 0), then the B tile (group 1)
+  for (int32_t e = t; e < nz; e += kTileThreads) {
+    cp_async8(pr + e, p.idx + 2 * (z0 + e));
+    cp_async4(rv + e, p.vals + z0 + e);
+  }
+  cp_async_commit();
+  {
+    const float4* src = p.B + g0 * p.ldb4 + c0;
+    const int32_t cells = n * cw;
+    if (cw == CB) {
+      for (int32_t q = t; q < cells; q += kTileThreads)
+        cp_async16(Bs + q, src + (int64_t)(q / CB) * p.ldb4 + (q % CB));
+    } else {
+      for (int32_t q = t; q < cells; q += kTileThreads) {
+        const int32_t j = q / cw, c = q - j * cw;
+        cp_async16(Bs + j * CB + c, src + (int64_t)j * p.ldb4 + c);
+      }
+    }
+  }
+  cp_async_commit();
+  for (int32_t r = t; r < n; r += kTileThreads) cnt[r] = 0;
+  tile_trace(p, 3);
+  cp_async_wait_group<1>();  // this thread's slice copies
+  __syncthreads();
+  // ---- COO -> CSR in shared memory
+  for (int32_t e = t; e < nz; e += kTileThreads) atomicAdd(&cnt[pr[e].x], 1);
+  __syncthreads();
+  if (t < 32) {  // exclusive scan of the row counts -> rp_s (relative to the matrix's first entry)
+    int32_t carry = 0;
+    for (int32_t r0 = 0; r0 < n; r0 += 32) {
+      const int32_t r = r0 + t;
+      const int32_t v = r < n ? cnt[r] : 0;
+      int32_t x = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (t >= d) x += y;
+      }
+      if (r < n) rp_s[r] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (t == 0) rp_s[n] = nz;
+  }
+  __syncthreads();
+  for (int32_t e = t; e < nz; e += kTileThreads) {
+    const int32_t r = pr[e].x;
+    slot[rp_s[r] + atomicSub(&cnt[r], 1) - 1] = e;
+  }
+  __syncthreads();
+  for (int32_t r = t; r < n; r += kTileThreads) {
+    const int32_t s0 = rp_s[r], s1 = rp_s[r + 1], d = s1 - s0;
+    if (d <= 8) {
+      uint32_t key[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int32_t e = q < d ? slot[s0 + q] : 0;
+        key[q] = q < d ? ((uint32_t)pr[e].y << 16) | (uint32_t)e : 0xffffffffu;
+      }
+#define BSPMM_TCX(a, b)                                   \
+      {                                                   \
+        const uint32_t lo = min(key[a], key[b]);          \
+        key[b] = max(key[a], key[b]);                     \
+        key[a] = lo;                                      \
+      }
+      if (d <= 4) {
+        BSPMM_TCX(0, 1) BSPMM_TCX(2, 3) BSPMM_TCX(0, 2) BSPMM_TCX(1, 3) BSPMM_TCX(1, 2)
+      } else {
+        BSPMM_TCX(0, 1) BSPMM_TCX(2, 3) BSPMM_TCX(4, 5) BSPMM_TCX(6, 7)
+        BSPMM_TCX(0, 2) BSPMM_TCX(1, 3) BSPMM_TCX(4, 6) BSPMM_TCX(5, 7)
+        BSPMM_TCX(1, 2) BSPMM_TCX(5, 6)
+        BSPMM_TCX(0, 4) BSPMM_TCX(1, 5) BSPMM_TCX(2, 6) BSPMM_TCX(3, 7)
+        BSPMM_TCX(2, 4) BSPMM_TCX(3, 5)
+        BSPMM_TCX(1, 2) BSPMM_TCX(3, 4) BSPMM_TCX(5, 6)
+      }
+#undef BSPMM_TCX
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < d) {
+          col_s[s0 + q] = (int32_t)(key[q] >> 16);
+          val_s[s0 + q] = rv[key[q] & 0xffffu];  // bitwise move
+        }
+      }
+    } else {
+      for (int32_t q = s0; q < s1; ++q) {
+        const int32_t e = slot[q];
+        const int32_t ce = pr[e].y;
+        int32_t rank = 0;
+        for (int32_t f = s0; f < s1; ++f) {
+          const int32_t fe = slot[f];
+          const int32_t cf = pr[fe].y;
+          rank += (cf < ce) || (cf == ce && fe < e);
+        }
+        col_s[s0 + rank] = ce;
+        val_s[s0 + rank] = rv[e];
+      }
+    }
+  }
+  tile_trace(p, 4);
+  cp_async_wait_all();  // the B tile
+  __syncthreads();
+  tile_trace(p, 5);
+  tile_rows<CB, 0, true, true>(p, Bs, rp_s, col_s, val_s, g0, n, c0, cw);
+  tile_trace(p, 6);
+}
+
 // Launch geometry for a batch; false when the batch is better served by the
 // persistent pipeline (more tiles than the GPU holds at once).
 bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int32_t num_sms, int32_t cb_override,
-               TileLayout* out) {
+               TileLayout* out, bool coo) {
   if (batch < 1 || k % 4 != 0) return false;
   const int32_t k4 = k / 4;
   const int64_t R = max_rows > 0 ? max_rows : kDefaultRows;
@@ -330,6 +482,13 @@ bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int3
     L.col_off = (int32_t)(L.rp_off + a16(4LL * (L.cap_rows + 1)));
     L.val_off = (int32_t)(L.col_off + a16(4LL * L.cap_nnz));
     L.smem = (int32_t)(L.val_off + a16(4LL * L.cap_nnz));
+    if (coo) {  // SparseTensor conversion scratch: raw pairs, raw values, slots, row counters
+      L.pair_off = L.smem;
+      L.cval_off = (int32_t)(L.pair_off + a16(8LL * L.cap_nnz));
+      L.slot_off = (int32_t)(L.cval_off + a16(4LL * L.cap_nnz));
+      L.cnt_off = (int32_t)(L.slot_off + a16(4LL * L.cap_nnz));
+      L.smem = (int32_t)(L.cnt_off + a16(4LL * (L.cap_rows + 1)));
+    }
     // resident CTAs per SM: 16 by threads (2048 / 128), fewer by shared memory
     // (228 KB per SM, 1 KB reserved per CTA)
     L.per_sm = (int32_t)std::min<int64_t>(16, 233472 / (L.smem + 1024 + 64));
@@ -356,6 +515,8 @@ bool plan_tile(int32_t batch, int32_t k, int32_t max_rows, int64_t max_nnz, int3
     if (cb < 2) return false;
   }
   if (L.smem > 200 * 1024 || L.per_sm < 1) return false;
+  // the conversion's 16-bit sort keys: positions and columns below 2^16
+  if (coo && (L.cap_nnz >= 65536 || L.cap_rows >= 65536)) return false;
   // one wave: every tile resident at once (beyond that the persistent
   // pipeline streams better, e.g. config 5)
   if (cb_override <= 0 && L.units > (int64_t)L.per_sm * num_sms) return false;
@@ -399,6 +560,30 @@ static cudaError_t launch_tile_e(const TileParams& tp, const TmaMaps& m, const T
   }
 }
 
+template <int CB>
+static cudaError_t launch_tile_coo_t(const TileParams& tp, const TileLayout& L, cudaStream_t s) {
+  auto kern = spmm_tile_coo_kernel<CB>;
+  static thread_local int configured[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (L.smem > 48 * 1024 && configured[dev & 63] < L.smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
+    if (e != cudaSuccess) return e;
+    configured[dev & 63] = L.smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)L.units);
+  cfg.blockDim = dim3(kTileThreads);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tp);
+}
+
 cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t s) {
   if (L.units == 0) return cudaSuccess;
   if (L.units > 0x7fffffffLL) return cudaErrorInvalidValue;
@@ -430,6 +615,24 @@ cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t
   tp.tma = (a.maps != nullptr && L.cb >= 8 && (a.dbg & 32768)) ? 1 : 0;
   tp.rp_first = (a.dbg & 65536) ? 0 : 1;
   tp.dbg_bits = (a.dbg & 16) ? 1 : 0;
+  tp.nnz_off = a.coo_nnz_off;
+  tp.idx = a.coo_idx;
+  tp.pair_off = L.pair_off;
+  tp.cval_off = L.cval_off;
+  tp.slot_off = L.slot_off;
+  tp.cnt_off = L.cnt_off;
+  tp.err = a.err;
+  if (a.coo_nnz_off) {  // SparseTensor input: the converting variant (row_off required)
+    if (!a.row_off || !a.err || a.bias != nullptr || a.accumulate != 0) return cudaErrorInvalidValue;
+    switch (L.cb) {
+      case 1: return launch_tile_coo_t<1>(tp, L, s);
+      case 2: return launch_tile_coo_t<2>(tp, L, s);
+      case 4: return launch_tile_coo_t<4>(tp, L, s);
+      case 8: return launch_tile_coo_t<8>(tp, L, s);
+      case 16: return launch_tile_coo_t<16>(tp, L, s);
+      default: return launch_tile_coo_t<32>(tp, L, s);
+    }
+  }
   static const TmaMaps no_maps{};
   const TmaMaps& m = a.maps ? *a.maps : no_maps;
   if (a.bias != nullptr || a.accumulate != 0) return cudaErrorInvalidValue;  // no GCN epilogue here (gcn_fused.cu)

@@ -467,22 +467,76 @@ def test_fused_offsets_adversarial(h):
 
 # ------------------------------------------------------------ a-2 fused into the SpMM (bspmm_coo with hints)
 
+# fused conversion paths: 0 = the planner's choice (small batches: the tile
+# kernel's SparseTensor variant), 16384 = the pipeline's converter warps,
+# ("tile", cb) = the tile variant at a forced column block
+COO_PATHS = {"auto": (0, 0), "pipeline": (16384, 0), "tile_cb1": (0, 1), "tile_cb8": (0, 8)}
+
+
+@pytest.mark.parametrize("path", list(COO_PATHS))
 @pytest.mark.parametrize("seed", range(5))
-def test_coo_fused_adversarial(h, seed):
+def test_coo_fused_adversarial(h, seed, path):
+    """Unsorted SparseTensor input with duplicates, empty rows and graphs,
+    through each fused conversion path: bitwise O3' over the oracle's CSR, and
+    the kernel that ran is the one asked for."""
     rng = np.random.default_rng(700 + seed)
     k = [16, 64, 128, 256, 512][seed]
     b = synth.random_batch(rng, int(rng.integers(1, 200)), k, nmax=60, dmax=6, duplicates=True)
     h.set_hints(max(int(b.sizes.max()), 1), max(int(b.nnz.max()), 1))
-    C = h.coo(None, T(b.sizes), T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B)).cpu().numpy()
-    h.sync()
+    dbg, cb = COO_PATHS[path]
+    h.set_debug(dbg)
+    h.set_tile_cb(cb)
+    try:
+        C = h.coo(None, T(b.sizes), T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B)).cpu().numpy()
+        h.sync()
+        kern = h.last_plan()["kernel"]
+    finally:
+        h.set_debug(0)
+        h.set_tile_cb(0)
+    if path == "pipeline":
+        assert kern == 0
+    elif path.startswith("tile"):
+        assert kern == 1 and h.last_plan()["lanes"] == cb
     orp, ocol, ov = oracle.coo2csr(b.row_off, None, b.nnz_off, b.coo_idx, b.coo_vals)
     C32 = oracle.spmm_f32(b.k, b.row_off, None, orp, ocol, ov, b.B)
     assert np.array_equal(C.view(np.uint32), C32.view(np.uint32))
 
 
-def test_coo_fused_hint_too_small_is_reported(h):
-    b = synth.config(3, coo=True)
-    h.set_hints(50, 100)                      # C3 has matrices up to 300 rows / 1500 entries
+@pytest.mark.parametrize("cid", [1, 2, 4])
+def test_coo_tile_configs_and_long_rows(h, cid):
+    """The tile kernel's SparseTensor variant on the small configs (the
+    planner's choice there), and on rows longer than the 8-key sorting network
+    (the rank-counting path): bitwise equal to the pipeline's converter warps
+    and to O3' over the oracle's CSR."""
+    b = synth.config(cid, coo=True)
+    cases = [b]
+    rng = np.random.default_rng(cid)
+    cases.append(synth.random_batch(rng, 60, b.k, nmax=40, dmax=20, duplicates=True))
+    for bb in cases:
+        h.set_hints(int(bb.sizes.max()), int(bb.nnz.max()))
+        outs = []
+        for dbg in (0, 16384):
+            h.set_debug(dbg)
+            try:
+                outs.append(h.coo(T(bb.row_off), None, T(bb.nnz_off), T(bb.coo_idx), T(bb.coo_vals),
+                                  T(bb.B)).cpu().numpy())
+                h.sync()
+                if dbg == 0 and bb is b:
+                    assert h.last_plan()["kernel"] == 1
+            finally:
+                h.set_debug(0)
+        orp, ocol, ov = oracle.coo2csr(bb.row_off, None, bb.nnz_off, bb.coo_idx, bb.coo_vals)
+        C32 = oracle.spmm_f32(bb.k, bb.row_off, None, orp, ocol, ov, bb.B)
+        for C in outs:
+            assert np.array_equal(C.view(np.uint32), C32.view(np.uint32))
+
+
+@pytest.mark.parametrize("cid", [3, 2])
+def test_coo_fused_hint_too_small_is_reported(h, cid):
+    """A matrix beyond the hints is skipped and reported by bspmm_sync, on the
+    pipeline's converter warps (config 3) and on the tile variant (config 2)."""
+    b = synth.config(cid, coo=True)
+    h.set_hints(10, 20)                       # below the largest matrices of both configs
     h.coo(T(b.row_off), None, T(b.nnz_off), T(b.coo_idx), T(b.coo_vals), T(b.B))
     with pytest.raises(bs.BspmmError, match="INVALID"):
         h.sync()
