@@ -109,7 +109,8 @@ typedef struct {
   int32_t sched;          /* 0: static round-robin units; 1: dynamic (global ticket counter)    */
   int64_t units;          /* batch * tiles                                                      */
   int32_t kernel;         /* 0: persistent TMA-ring pipeline; 1: small-batch tile kernel (one   *
-                           * CTA per (matrix, column block); kt = 4 * block, lanes = block)     */
+                           * CTA per (matrix, column block); kt = 4 * block, lanes = block;   *
+                           * CSR and, in bspmm_coo, SparseTensor input)                        */
 } bspmm_plan_t;
 
 /* ---- lifetime -------------------------------------------------------- */
@@ -223,7 +224,10 @@ BSPMM_API bspmm_status_t bspmm_mc_destroy(bspmm_mc_t mc);
  * A_i), the fast path (k, ldb, ldc % 4 == 0, aligned B, C) and no csr_*_out,
  * the conversion is FUSED into the SpMM launch: each unit's SparseTensor slice
  * is staged and sorted into CSR in shared memory (same canonical order, same
- * bits).  A matrix beyond the hints is then skipped -- ITS ROWS OF C ARE NOT
+ * bits) -- by converter warps of the persistent kernel, or, for batches whose
+ * tiles are all resident at once, by each tile CTA of the small-batch kernel
+ * while its B tile lands (bspmm_last_plan: kernel 0 / 1).  A matrix beyond
+ * the hints is then skipped -- ITS ROWS OF C ARE NOT
  * WRITTEN -- and reported as BSPMM_ERROR_INVALID_VALUE by the next
  * bspmm_sync: callers that cannot guarantee the hints must call bspmm_sync
  * after the call (the Python binding's Handle.coo(checked=True) does). */
