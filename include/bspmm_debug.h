@@ -53,8 +53,11 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * layer without the Z arithmetic, 262144 = GCN layer without the MMAs (both
  * leave Y undefined; timing only); 524288 = GCN layer with two groups of
  * Z-producer warps instead of three (3xTF32: three instead of two);
- * bits 20-21 = GCN feature-tile width (1: 64, 2: 128, 3: 256; 0: planner).  0
- * (default) = normal. */
+ * bits 20-21 = GCN feature-tile width (1: 64, 2: 128, 3: 256; 0: planner);
+ * bit 22 (4194304) = standalone SDDMM reading the CSR structure from global
+ * memory (the round-1 kernel) instead of the double-buffered shared stage;
+ * bit 23 (8388608) = standalone SDDMM prefetching two grad_C rows ahead
+ * instead of one (k = 256).  0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Small-batch tile kernel (spmm_tile.cu): float4 columns per tile (1, 2, 4,

@@ -24,6 +24,11 @@
 namespace bspmm {
 
 constexpr int kBwdThreads = 256;
+// experiment bits (include/bspmm_debug.h): the standalone SDDMM with its
+// structure read from global memory (the round-1 kernel); two grad_C rows
+// prefetched instead of one
+constexpr int32_t kDbgSddmmGlobalStruct = 1 << 22;
+constexpr int32_t kDbgSddmmPf2 = 1 << 23;
 
 // CSR -> per-matrix transposed CSR, one warp per matrix (see the header).
 // Entries of A_i are visited in storage order = (row, position) order, so a
@@ -180,7 +185,7 @@ cudaError_t launch_transpose_csr(int32_t batch, const int64_t* row_off, const in
   const int smem = kTrWarps * ((small ? 256 : 512) + kTrRp + ridcap) * 4;
   cudaError_t e = cudaSuccess;
   auto go = [&](auto kern) {
-    if (smem > 48 * 1024) {
+    if (smem > 47 * 1024) {  // dynamic + static above the 48 KB default
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return;
     }
@@ -434,11 +439,202 @@ __global__ void __launch_bounds__(kBwdThreads) sddmm_staged_kernel(int32_t batch
   }
 }
 
+// the rare over-capacity matrix of sddmm_struct_kernel, out of line so that
+// its registers do not count against the staged loop's
+template <int CH>
+__device__ __noinline__ void sddmm_rows_global(bool staged, int32_t n, int32_t chunks, const float* Bs, int32_t k,
+                                               const float* Bg, int64_t ldb, const float* Gm, int64_t ldg,
+                                               const int32_t* rp, const int32_t* col, float* out, uint64_t* bar,
+                                               uint32_t phase) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (staged) sddmm_rows<CH, true>(n, chunks, Bs, k, Gm, ldg, rp, col, out, lane, warp, nw, bar, phase);
+  else sddmm_rows<CH, false>(n, chunks, Bg, ldb, Gm, ldg, rp, col, out, lane, warp, nw);
+}
+
+// Staged SDDMM with the CSR slice in shared memory (round 2, the default for
+// streaming batches).  Same CTA shape and B_i staging as sddmm_staged_kernel,
+// but no global load sits on a row's chain any more: matrix i + grid's row
+// pointers and column ids are cp.async'ed into the other half of a
+// double-buffered structure stage while matrix i computes, and so is the
+// metadata that addresses them (a 4-slot ring in shared memory: i + grid's
+// entry range, i + 3 grid's row range -- no metadata is held in registers
+// across the row loop); grad_C rows are prefetched PF rows ahead, and two
+// entries share one butterfly (the xor-16 step swaps halves, so lanes 0-15
+// reduce entry e and lanes 16-31 entry e + 1 -- every add pairs the same two
+// partials as the per-entry butterfly: the same bits).  A matrix whose B_i
+// or structure exceeds the stage takes the out-of-line global loop.
+struct SdMeta {
+  int64_t g;      // first global row
+  int64_t gnext;  // row_off[m + 1] (sizes == NULL)
+  int32_t n;      // rows (sizes != NULL)
+  int32_t ea, eb; // entry range [row_ptr[g], row_ptr[g + n])
+  int32_t pad;
+};
+template <int CH, int PF, bool FULL>
+__global__ void __launch_bounds__(kBwdThreads, 3) sddmm_struct_kernel(int32_t batch, int32_t k,
+                                                                     const int64_t* __restrict__ row_off,
+                                                                     const int32_t* __restrict__ sizes,
+                                                                     const int32_t* __restrict__ row_ptr,
+                                                                     const int32_t* __restrict__ col,
+                                                                     const float* __restrict__ B, int64_t ldb,
+                                                                     const float* __restrict__ G_, int64_t ldg,
+                                                                     float* __restrict__ out, int32_t cap_bytes,
+                                                                     int32_t rcap, int32_t ecap, int32_t dbg) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ SdMeta meta[4];
+  float* Bs = reinterpret_cast<float*>(smem);
+  int32_t* s_rp = reinterpret_cast<int32_t*>(smem + cap_bytes);  // [2][rcap]
+  int32_t* s_col = s_rp + 2 * rcap;                              // [2][ecap]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t G = gridDim.x;
+  auto rows_of = [&](const SdMeta& m) -> int32_t { return sizes ? m.n : (int32_t)(m.gnext - m.g); };
+  // slot of matrix m: its row range (thread 0) ...
+  auto fetch_rows = [&](int64_t m, SdMeta& d) {
+    if (m < batch) {
+      cp_async8(&d.g, row_off + m);
+      if (sizes) cp_async4(&d.n, sizes + m);
+      else cp_async8(&d.gnext, row_off + m + 1);
+    } else {
+      d.g = d.gnext = 0;
+      d.n = 0;
+    }
+  };
+  // ... and its entry range (thread 32, once the row range has landed)
+  auto fetch_entries = [&](SdMeta& d) {
+    const int32_t n = rows_of(d);
+    if (n > 0) {
+      cp_async4(&d.ea, row_ptr + d.g);
+      cp_async4(&d.eb, row_ptr + d.g + n);
+    } else {
+      d.ea = d.eb = 0;
+    }
+  };
+  auto fits = [&](int32_t n_, int32_t ea, int32_t eb) {
+    return n_ > 0 && (int64_t)n_ * k * 4 <= cap_bytes && n_ + 1 <= rcap && eb - ea <= ecap;
+  };
+  // cp.async a matrix's row pointers and column ids into stage `buf`
+  auto stage_struct = [&](int buf, const SdMeta& d) {
+    const int32_t n = rows_of(d);
+    if (fits(n, d.ea, d.eb)) {
+      for (int32_t t = threadIdx.x; t <= n; t += blockDim.x) cp_async4(s_rp + buf * rcap + t, row_ptr + d.g + t);
+      for (int32_t t = threadIdx.x; t < d.eb - d.ea; t += blockDim.x) cp_async4(s_col + buf * ecap + t, col + d.ea + t);
+    }
+  };
+  const int64_t i0 = blockIdx.x;
+  // prologue: rows of i0 .. i0 + 2G, entries of i0 and i0 + G, i0's structure
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    for (int q = 0; q < 3; ++q) fetch_rows(i0 + q * G, meta[q]);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (threadIdx.x == 32)
+    for (int q = 0; q < 2; ++q) fetch_entries(meta[q]);
+  cp_async_wait_all();
+  __syncthreads();
+  stage_struct(0, meta[0]);
+  cp_async_wait_all();
+  __syncthreads();
+  uint32_t phase = 0;
+  int j = 0;
+  for (int64_t i = i0; i < batch; i += G, ++j) {
+    const SdMeta& m0 = meta[j & 3];
+    const int32_t n0 = rows_of(m0);
+    const int64_t g0 = m0.g;
+    const int32_t e0a = m0.ea, e0b = m0.eb;
+    const bool staged = fits(n0, e0a, e0b);
+    if (threadIdx.x == 0) {
+      const SdMeta& m1 = meta[(j + 1) & 3];
+      const int32_t n1 = rows_of(m1);
+      if (n1 > 0 && !(dbg & 512))
+        bulk_prefetch_l2(B + m1.g * ldb, (uint32_t)(((int64_t)(n1 - 1) * ldb + k) * 4));
+      if (staged) {
+        const uint32_t bytes = (uint32_t)n0 * (uint32_t)k * 4u;
+        mbar_arrive_expect_tx(&bar, bytes);
+        if (ldb == k) {
+          bulk_g2s(Bs, B + g0 * ldb, bytes, &bar);
+        } else {
+          for (int32_t r = 0; r < n0; ++r) bulk_g2s(Bs + (int64_t)r * k, B + (g0 + r) * ldb, (uint32_t)k * 4u, &bar);
+        }
+      }
+      fetch_rows(i + 3 * G, meta[(j + 3) & 3]);
+    }
+    if (threadIdx.x == 32) fetch_entries(meta[(j + 2) & 3]);
+    stage_struct((j + 1) & 1, meta[(j + 1) & 3]);
+    if (staged) {
+      const int32_t* rp = s_rp + (j & 1) * rcap;
+      const int32_t* cs = s_col + (j & 1) * ecap;
+      const float* Gm = G_ + g0 * ldg;
+      float* o = out + e0a;
+      float4 gq[PF][CH];
+      auto gload = [&](int32_t r_, float4* dst) {
+        const float* grow = Gm + (int64_t)r_ * ldg + 4 * lane;
+#pragma unroll
+        for (int v = 0; v < CH; ++v)
+          dst[v] = (FULL || lane + 32 * v < (k >> 2)) ? ldg_nc_f4(grow + 128 * v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+#pragma unroll
+      for (int f = 0; f < PF; ++f)
+        if (warp + f * nw < n0) gload(warp + f * nw, gq[f]);
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      for (int32_t r = warp; r < n0; r += nw) {
+        float4 gv[CH];
+#pragma unroll
+        for (int v = 0; v < CH; ++v) gv[v] = gq[0][v];
+#pragma unroll
+        for (int f = 0; f + 1 < PF; ++f)
+#pragma unroll
+          for (int v = 0; v < CH; ++v) gq[f][v] = gq[f + 1][v];
+        if (r + PF * nw < n0) gload(r + PF * nw, gq[PF - 1]);
+        const int32_t ea = rp[r] - e0a, eb = rp[r + 1] - e0a;
+        // up to four entries per butterfly: the xor-16 step swaps pairs
+        // (lanes < 16 keep entries 0-1, the others 2-3), the xor-8 step
+        // swaps within the pair, xor 4, 2, 1 finish; lane 8q writes entry q
+        for (int32_t e = ea; e < eb; e += 4) {
+          const int32_t m = eb - e;  // warp-uniform
+          float p[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            p[q] = 0.f;
+            if (q < m) {
+              const float* bp = Bs + cs[e + q] * k + 4 * lane;
+#pragma unroll
+              for (int v = 0; v < CH; ++v) {
+                if (FULL || lane + 32 * v < (k >> 2)) {
+                  const float4 bb = *reinterpret_cast<const float4*>(bp + 128 * v);
+                  p[q] = fmaf(gv[v].x, bb.x, p[q]); p[q] = fmaf(gv[v].y, bb.y, p[q]);
+                  p[q] = fmaf(gv[v].z, bb.z, p[q]); p[q] = fmaf(gv[v].w, bb.w, p[q]);
+                }
+              }
+            }
+          }
+          const bool b4 = lane & 16, b3 = lane & 8;
+          const float x = __shfl_xor_sync(0xffffffffu, b4 ? p[0] : p[2], 16);
+          const float y = __shfl_xor_sync(0xffffffffu, b4 ? p[1] : p[3], 16);
+          const float q0 = (b4 ? p[2] : p[0]) + x, q1 = (b4 ? p[3] : p[1]) + y;
+          float t = (b3 ? q1 : q0) + __shfl_xor_sync(0xffffffffu, b3 ? q0 : q1, 8);
+#pragma unroll
+          for (int d = 4; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+          const int32_t q = (b4 ? 2 : 0) + (b3 ? 1 : 0);
+          if ((lane & 7) == 0 && q < m) o[e + q] = t;
+        }
+      }
+    } else if (n0 > 0) {  // B_i or the structure above the stage: the global loop
+      sddmm_rows_global<CH>(false, n0, k >> 2, Bs, k, B + g0 * ldb, ldb, G_ + g0 * ldg, ldg, row_ptr + g0, col,
+                            out, &bar, 0);
+    }
+    cp_async_wait_all();  // the next matrix's structure and the metadata ring
+    __syncthreads();      // ... visible to every warp; every warp is done with Bs
+  }
+}
 
 cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
-                         int64_t ldg, float* out, int32_t max_rows_hint, int32_t num_sms, int32_t dbg,
-                         cudaStream_t s) {
+                         int64_t ldg, float* out, int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms,
+                         int32_t dbg, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
   const bool vec = (k % 4 == 0) && (ldb % 4 == 0) && (ldg % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(G)) & 15u) == 0;
@@ -452,16 +648,45 @@ cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const
     cudaError_t e = cudaSuccess;
     const int chunks = k >> 2, ch = (chunks + 31) / 32;
     auto go = [&](auto kern) {
-      if (cap > 48 * 1024) {
+      if (cap > 47 * 1024) {  // dynamic + static above the 48 KB default
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
         if (e != cudaSuccess) return;
       }
       kern<<<grid, kBwdThreads, cap, s>>>(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, cap, dbg);
       e = cudaGetLastError();
     };
-    if (ch <= 1) go(sddmm_staged_kernel<1>);
-    else if (ch <= 2) go(sddmm_staged_kernel<2>);
-    else go(sddmm_staged_kernel<4>);
+    if ((dbg & kDbgSddmmGlobalStruct) || ch > 2) {  // structure read from global memory (k > 256: the
+                                                    // struct kernel would spill at 3 CTAs per SM)
+      if (ch <= 1) go(sddmm_staged_kernel<1>);
+      else if (ch <= 2) go(sddmm_staged_kernel<2>);
+      else go(sddmm_staged_kernel<4>);
+      return e;
+    }
+    // structure stage: two buffers of (hinted rows + 1) row pointers and
+    // (hinted entries) column ids; matrices above it take the global loop
+    const int32_t rcap = (max_rows_hint > 0 ? std::min<int32_t>(max_rows_hint, 1024) : 256) + 1;
+    const int32_t ecap = max_nnz_hint > 0 ? (int32_t)std::min<int64_t>(max_nnz_hint, 4096) : 2048;
+    const int32_t sbytes = cap + 2 * (rcap + ecap) * 4;
+    auto go2 = [&](auto kern) {
+      if (sbytes > 47 * 1024) {  // dynamic + static above the 48 KB default
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbytes);
+        if (e != cudaSuccess) return;
+      }
+      // persistent: exactly the resident CTAs (a partial last wave of a
+      // larger grid idles a third of the SMs at the end)
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwdThreads, sbytes);
+      if (e != cudaSuccess) return;
+      const int grid2 = (int)std::min<int64_t>(batch, (int64_t)num_sms * std::max(per_sm, 1));
+      kern<<<grid2, kBwdThreads, sbytes, s>>>(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, cap, rcap,
+                                              ecap, dbg);
+      e = cudaGetLastError();
+    };
+    const bool pf2 = (dbg & kDbgSddmmPf2) != 0;
+    if (chunks == 64) pf2 ? go2(sddmm_struct_kernel<2, 2, true>) : go2(sddmm_struct_kernel<2, 1, true>);
+    else if (chunks == 32) go2(sddmm_struct_kernel<1, 1, true>);
+    else if (ch <= 1) go2(sddmm_struct_kernel<1, 1, false>);
+    else go2(sddmm_struct_kernel<2, 1, false>);
     return e;
   }
   const int grid = batch < 65535 ? batch : 65535;

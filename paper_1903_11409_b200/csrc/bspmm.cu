@@ -859,8 +859,8 @@ BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k,
       return BSPMM_SUCCESS;
     }
   }
-  CK(h, launch_sddmm(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, h->hint_rows, h->num_sms,
-                     h->dbg,
+  CK(h, launch_sddmm(batch, k, row_off, sizes, row_ptr, col, B, ldb, G, ldg, out, h->hint_rows, h->hint_nnz,
+                     h->num_sms, h->dbg,
                      h->stream));
   h->launches++;
   return BSPMM_SUCCESS;

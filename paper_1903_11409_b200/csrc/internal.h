@@ -156,8 +156,8 @@ cudaError_t launch_transpose_csr(int32_t batch, const int64_t* row_off, const in
                                  int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms, cudaStream_t s);
 cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
-                         int64_t ldg, float* out, int32_t max_rows_hint, int32_t num_sms, int32_t dbg,
-                         cudaStream_t s);
+                         int64_t ldg, float* out, int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms,
+                         int32_t dbg, cudaStream_t s);
 cudaError_t launch_validate_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes,
                                 const int32_t* row_ptr, const int32_t* col, int* flag, cudaStream_t s);
 cudaError_t launch_validate_coo(int32_t batch, const int64_t* row_off, const int32_t* sizes,

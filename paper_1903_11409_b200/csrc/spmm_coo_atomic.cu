@@ -146,7 +146,7 @@ cudaError_t launch_spmm_coo_atomic(int32_t batch, int32_t k, const int64_t* row_
   p.C = C;
   p.ldc = ldc;
   const int smem = 2 * R * kt4 * 16;
-  if (smem > 48 * 1024) {
+  if (smem > 47 * 1024) {  // dynamic + static above the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(spmm_coo_atomic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
   }

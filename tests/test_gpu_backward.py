@@ -162,6 +162,35 @@ def test_sddmm_streaming_batch(h, dbg):
         h.set_hints(0, 0)
 
 
+@pytest.mark.parametrize("dbg", [0, 1 << 22, 1 << 23])
+@pytest.mark.parametrize("k,ld", [(256, 256), (128, 128), (64, 64), (200, 204), (256, 260), (384, 384)])
+def test_sddmm_standalone_kernels(h, k, ld, dbg):
+    """The standalone SDDMM for streaming batches (1500 matrices > 8 per SM):
+    the structure-staged kernel (k <= 256; all lanes active at k = 128 / 256,
+    guarded lanes otherwise), its grad_C prefetch-2 variant (bit 23), the
+    global-structure kernel (bit 22, and k > 256), with ld > k, rows of 0-9
+    entries (1-3 four-entry butterfly groups, duplicates, empty rows and
+    graphs); integer-valued inputs exactly, U[-1,1) within the bound.  Then
+    hints below the batch's largest matrix: those matrices take the
+    out-of-line global loop (B_i or the structure above the stage)."""
+    rng = np.random.default_rng(k * 7 + ld + dbg % 1000)
+    b = synth.random_batch(rng, 1500, k, nmax=48, dmax=9, duplicates=True, int_valued=True)
+    Gi = rng.integers(-4, 5, size=(b.n_rows, k)).astype(np.float32)
+    h.set_debug(256 | dbg)
+    try:
+        h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+        _sddmm_check(h, b, Gi, ld=ld, exact=True)
+        bf = synth.random_batch(rng, 1500, k, nmax=48, dmax=9, duplicates=True)
+        h.set_hints(int(bf.sizes.max()), int(bf.nnz.max()))
+        _sddmm_check(h, bf, grad(bf, k + 3), ld=ld)
+        for rows, nnz in ((24, int(bf.nnz.max())), (int(bf.sizes.max()), 40)):
+            h.set_hints(rows, nnz)
+            _sddmm_check(h, bf, grad(bf, k + 5), ld=ld)
+    finally:
+        h.set_debug(0)
+        h.set_hints(0, 0)
+
+
 def test_backward_c5_full_size_exhaustive(h):
     """The backward at BASELINE.json's full C5 size (65536 graphs, k = 256; the
     streaming paths: warp-per-matrix transpose, grad_B SpMM, standalone SDDMM),
