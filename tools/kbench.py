@@ -177,6 +177,7 @@ def main():
     ap.add_argument("--shard", type=int, default=1, help="time rank 0's shard of an N-way split (1 GPU)")
     ap.add_argument("--backward", action="store_true", help="also time csr_backward (grad_B and grad_vals)")
     ap.add_argument("--sddmm-dbg", default="", help="with --backward: debug bit sets for extra SDDMM timings")
+    ap.add_argument("--coo-dbg", default="", help="debug bit sets for extra fused-COO timings")
     ap.add_argument("--trace", action="store_true", help="phase trace of the last launch of the graph (per dbg)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -254,6 +255,10 @@ def main():
         if b.k % 4 == 0 and cid != 5:
             extra["coo_convert_csr_us"] = time_calls(h, reps, R, coo_convert_csr) * 1e3
             extra["coo_atomic_us"] = time_calls(h, reps, R, coo_atomic) * 1e3
+            for d in [int(x) for x in args.coo_dbg.split(",") if x]:
+                h.set_debug(d)
+                extra[f"coo_convert_csr_us_dbg{d}"] = time_calls(h, reps, R, coo_convert_csr) * 1e3
+            h.set_debug(0)
         print(json.dumps({"config": cid, "step_us": ms_step * 1e3, "fused_step_us": ms_fused * 1e3,
                           "offsets_us": ms_off * 1e3,
                           "spmm_us_no_graph": ms_ng * 1e3, "alg_bytes": per, "replicas": len(reps), **extra}),
