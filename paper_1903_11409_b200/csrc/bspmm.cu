@@ -182,6 +182,41 @@ bspmm_status_t plan_for(bspmm_handle_t h, int32_t batch, int32_t k, bool aligned
 
 }  // namespace
 
+// The device allocation containing p (cuMemGetAddressRange through the
+// runtime's driver entry point), cached per handle: the kernels' pre-wait L2
+// prefetch of B clips its (possibly stale) addresses to it.
+bool bspmm::alloc_range(bspmm_handle_t h, const void* p, uint64_t* lo, uint64_t* hi) {
+  const uint64_t a = reinterpret_cast<uint64_t>(p);
+  for (int q = 0; q < 16; ++q)
+    if (h->ar_lo[q] <= a && a < h->ar_hi[q]) {
+      *lo = h->ar_lo[q];
+      *hi = h->ar_hi[q];
+      return true;
+    }
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    else
+      cudaGetLastError();
+  }
+  if (!range) return false;
+  CUdeviceptr base = 0;
+  size_t bytes = 0;
+  if (range(&base, &bytes, (CUdeviceptr)a) != CUDA_SUCCESS || bytes == 0) return false;
+  const int q = h->ar_next;
+  h->ar_next = (q + 1) & 15;
+  h->ar_lo[q] = *lo = (uint64_t)base;
+  h->ar_hi[q] = *hi = (uint64_t)base + bytes;
+  return true;
+}
+
+
 extern "C" {
 
 BSPMM_API const char* bspmm_status_string(bspmm_status_t s) {
@@ -319,7 +354,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits >= (1 << 26)) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits >= (1 << 27)) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -416,6 +451,13 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
     const TmaMaps* maps = (L.cb >= 8 && (h->dbg & 32768)) ? tma_maps(h, B, k, ldb, 4 * L.cb) : nullptr;
     CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias,
               accumulate};
+    if (!(h->dbg & kDbgNoPrewaitPrefetch)) {
+      alloc_range(h, B, &a.b_lo, &a.b_hi);
+      if (!(h->dbg & kDbgNoStructPrefetch) && alloc_range(h, row_ptr, &a.s_lo[0], &a.s_hi[0])) {
+        alloc_range(h, col_idx, &a.s_lo[1], &a.s_hi[1]);
+        alloc_range(h, vals, &a.s_lo[2], &a.s_hi[2]);
+      }
+    }
     CK(h, launch_spmm_tile(a, L, h->stream));
     h->launches++;
     return BSPMM_SUCCESS;
@@ -427,6 +469,10 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
   CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias, accumulate,
             plan.sched ? h->dev_sched : nullptr};
   a.mc = mc;
+  if (!(h->dbg & kDbgNoPrewaitPrefetch)) {
+    alloc_range(h, B, &a.b_lo, &a.b_hi);
+    if (!(h->dbg & kDbgNoStructPrefetch)) alloc_range(h, row_ptr, &a.s_lo[0], &a.s_hi[0]);
+  }
   CK(h, launch_spmm_csr(a, plan, h->stream));
   if (plan.units > 0) h->launches++;
   return BSPMM_SUCCESS;
@@ -614,6 +660,11 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
       a.coo_nnz_off = nnz_off;
       a.coo_idx = idx;
       a.err = h->dev_flag;
+      if (!(h->dbg & kDbgNoPrewaitPrefetch)) {
+        alloc_range(h, B, &a.b_lo, &a.b_hi);
+        if (!(h->dbg & kDbgNoStructPrefetch) && alloc_range(h, idx, &a.s_lo[1], &a.s_hi[1]))
+          alloc_range(h, vals, &a.s_lo[2], &a.s_hi[2]);
+      }
       CK(h, launch_spmm_tile(a, TL, h->stream));
       h->launches++;
       h->coo_fused_pending = true;
@@ -635,6 +686,11 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
         plan.sched = 1;
         h->last_plan = plan;
         a.sched = h->dev_sched;
+      }
+      if (!(h->dbg & kDbgNoPrewaitPrefetch)) {
+        alloc_range(h, B, &a.b_lo, &a.b_hi);
+        if (!(h->dbg & kDbgNoStructPrefetch) && alloc_range(h, idx, &a.s_lo[1], &a.s_hi[1]))
+          alloc_range(h, vals, &a.s_lo[2], &a.s_hi[2]);
       }
       CK(h, launch_spmm_csr(a, plan, h->stream));
       if (plan.units > 0) h->launches++;

@@ -84,7 +84,19 @@ struct CsrArgs {
   const float* G = nullptr;             // SDDMM mode (NEXT-2): sd_out[e] = <G[row_e], B[col_e]>
   int64_t ldg = 0;
   float* sd_out = nullptr;
+  // the allocation holding B ([b_lo, b_hi), 0 = unknown): pre-wait L2
+  // prefetches of B are clipped to it
+  uint64_t b_lo = 0, b_hi = 0;
+  // the allocations of the structure arrays (CSR: row_ptr, col, vals; COO:
+  // -, idx, vals), for the same prefetch of the matrix's structure
+  uint64_t s_lo[3] = {}, s_hi[3] = {};
 };
+// debug bit 16777216: no pre-wait L2 prefetch of B (tile kernels)
+constexpr int32_t kDbgNoPrewaitPrefetch = 1 << 24;
+// debug bit 33554432: the pre-wait prefetch covers B only (not the matrix's structure)
+constexpr int32_t kDbgNoStructPrefetch = 1 << 25;
+// bspmm.cu: the device allocation containing p (cached per handle); false if unknown
+bool alloc_range(bspmm_handle_t h, const void* p, uint64_t* lo, uint64_t* hi);
 
 // kernels (.cu)
 cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStream_t s);
@@ -210,4 +222,7 @@ struct bspmm_handle_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_handoff = nullptr;  // bspmm_set_stream: new stream waits for the old one
   cudaEvent_t ev[64] = {};
+  // alloc_range cache: device allocations (base, end) seen as B
+  uint64_t ar_lo[16] = {}, ar_hi[16] = {};
+  int ar_next = 0;
 };

@@ -86,6 +86,30 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
   bytes &= ~15u;
   if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// L2 prefetch of [src, src + bytes) clipped to the allocation [lo, hi): a hint
+// only (never faults, never changes a result), so its address may come from a
+// read that races with the previous kernel (the pre-wait prologue below)
+__device__ __forceinline__ void prefetch_l2_clipped(uint64_t src, uint64_t bytes, uint64_t lo, uint64_t hi) {
+  uint64_t a = src < lo ? lo : src, e = src + bytes;
+  if (e > hi) e = hi;
+  a &= ~15ull;
+  while (a + 16 <= e) {
+    const uint64_t n = (e - a) < (1ull << 20) ? (e - a) : (1ull << 20);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)n & ~15u) : "memory");
+    a += n & ~15ull;
+  }
+}
+// relaxed (racy-by-design) loads for prefetch addresses read before griddepcontrol.wait
+__device__ __forceinline__ int64_t ld_relaxed_s64(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_relaxed_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 // ---- cp.async (LDGSTS), 4 bytes, + arrive-on when this thread's copies land
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");

@@ -66,6 +66,10 @@ struct SpmmParams {
   const float* __restrict__ G;
   int64_t ldg;
   float* __restrict__ sd_out;
+  // pre-wait L2 prefetch (few units per CTA): B's and the structure arrays'
+  // allocations (CSR row_ptr, col, vals; COO -, idx, vals); b_hi == 0: off
+  uint64_t b_lo, b_hi;
+  uint64_t s_lo[3], s_hi[3];
 };
 
 // GCN epilogue (NEXT-1, PAPER.md Fig. algo:graph_conv_batched): A (U + 1 b^T)
@@ -1201,6 +1205,39 @@ __device__ __forceinline__ void convert_units(const SpmmParams& p, unsigned char
   }
 }
 
+// Pre-wait prologue (programmatic dependent launch), batches with at most 8
+// units per CTA: consumer warp 0 (idle until the first unit lands) prefetches
+// into L2, BEFORE griddepcontrol.wait, the B rows and the structure slice of
+// this CTA's units -- a CTA becomes resident as soon as the previous launch's
+// CTA on its SM exits, so the prefetch fills the previous launch's tail (C3:
+// its CTAs finish over a ~5 us spread).  The row and entry ranges are read
+// with relaxed loads that may race with the previous kernel; the prefetches
+// are hints clipped to the arrays' allocations, and everything the kernel
+// uses is read again after the wait.
+template <bool COO>
+__device__ __forceinline__ void prefetch_units(const SpmmParams& p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = blockIdx.x + (int64_t)lane * gridDim.x;
+  if (lane >= 8 || u >= p.units) return;
+  const int64_t i = u / p.tiles;
+  if (u - i * p.tiles != 0 && u != blockIdx.x) return;  // a matrix's rows once per CTA
+  const int64_t g0 = ld_relaxed_s64(p.row_off + i);
+  const int64_t g1 = p.sizes ? g0 + ld_relaxed_s32(p.sizes + i) : ld_relaxed_s64(p.row_off + i + 1);
+  if (g1 <= g0 || g1 - g0 > (1 << 20)) return;
+  prefetch_l2_clipped(reinterpret_cast<uint64_t>(p.B + g0 * p.ldb), (uint64_t)(g1 - g0) * p.ldb * 4, p.b_lo,
+                      p.b_hi);
+  if (COO) {
+    if (!p.s_hi[1]) return;
+    const int64_t z0 = ld_relaxed_s64(p.nnz_off + i), z1 = ld_relaxed_s64(p.nnz_off + i + 1);
+    if (z1 <= z0 || z1 - z0 > (1 << 24)) return;
+    prefetch_l2_clipped(reinterpret_cast<uint64_t>(p.idx + 2 * z0), (uint64_t)(z1 - z0) * 8, p.s_lo[1], p.s_hi[1]);
+    prefetch_l2_clipped(reinterpret_cast<uint64_t>(p.vals + z0), (uint64_t)(z1 - z0) * 4, p.s_lo[2], p.s_hi[2]);
+  } else if (p.s_hi[0]) {
+    prefetch_l2_clipped(reinterpret_cast<uint64_t>(p.row_ptr + g0), (uint64_t)(g1 - g0 + 1) * 4, p.s_lo[0],
+                        p.s_hi[0]);
+  }
+}
+
 template <int CH, bool VEC, int EPI, bool COO, bool ONE = false>
 __global__ void __launch_bounds__(kMaxThreadsK(CH, COO), 1) __maxnreg__(kMaxRegsK(CH, COO)) spmm_csr_kernel(const SpmmParams p, const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1230,8 +1267,10 @@ __global__ void __launch_bounds__(kMaxThreadsK(CH, COO), 1) __maxnreg__(kMaxRegs
     }
   }
   __syncthreads();
+  if (p.b_hi && p.row_off && (threadIdx.x >> 5) == 1) prefetch_units<COO>(p);
   // programmatic dependent launch: everything above overlapped the previous
-  // kernel (e.g. the offsets builder); global memory is touched only after this
+  // kernel (e.g. the offsets builder); global memory is read only after this
+  // (the prefetch hints aside)
   pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) BSPMM_TRACE(p, 1);
@@ -1339,6 +1378,13 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.err = a.err;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
   sp.cvt_warps = a.cvt_warps;
   sp.coo_rows = plan.max_rows;
+  const bool pf = plan.units <= 8LL * plan.grid && epi != 3;
+  sp.b_lo = pf ? a.b_lo : 0;
+  sp.b_hi = pf ? a.b_hi : 0;
+  for (int q = 0; q < 3; ++q) {
+    sp.s_lo[q] = pf ? a.s_lo[q] : 0;
+    sp.s_hi[q] = pf ? a.s_hi[q] : 0;
+  }
   static const TmaMaps no_maps{};
   const TmaMaps& maps = a.maps ? *a.maps : no_maps;
   if (plan.vec) {

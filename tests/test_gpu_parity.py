@@ -709,3 +709,42 @@ def test_tile_fallbacks(h):
         assert_parity(b, out["auto"], "tile fallback")
         for kern in KERNELS:
             assert np.array_equal(out[kern].view(np.uint32), out["pipeline"].view(np.uint32)), kern
+
+
+# ------------------------------------------------ pre-wait L2 prefetch (PDL)
+PF_BITS = {"default": 0, "no_prefetch": 1 << 24, "b_only": 1 << 25, "with_col_val_run": 1 << 26}
+
+
+@pytest.mark.parametrize("bits", list(PF_BITS))
+@pytest.mark.parametrize("kern,cid", [("pipeline", 3), ("auto", 3), ("tile", 4), ("auto", 2)])
+def test_prewait_prefetch_reads_racing_offsets(h, kern, cid, bits):
+    """The kernels read row_off / nnz_off BEFORE griddepcontrol.wait for their
+    L2 prefetch hints.  Here the immediately preceding kernel (the offsets
+    builder, PDL-chained) writes row_off into a buffer pre-filled with huge
+    garbage offsets, so the racy read may see garbage: the prefetch must stay
+    inside the arrays' allocations (no fault) and the result must not depend
+    on it -- bitwise O3', for every prefetch variant (debug bits 24-26) and
+    both the CSR and the SparseTensor launch."""
+    b = synth.config(cid, coo=True)
+    dbg = PF_BITS[bits] | KERNELS[kern][0]
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    h.set_debug(dbg)
+    h.set_tile_cb(KERNELS[kern][1])
+    try:
+        B = T(b.B)
+        rp, col, vals, sz = T(b.row_ptr), T(b.col), T(b.vals), T(b.sizes)
+        for _ in range(3):
+            ro = torch.full((b.batch + 1,), (1 << 40) + 12345, dtype=torch.int64, device=DEV)
+            h.build_offsets(sz, out=ro)
+            C = h.csr(ro, None, rp, col, vals, B)
+            no = torch.full((b.batch + 1,), -(1 << 40), dtype=torch.int64, device=DEV)
+            no.copy_(T(b.nnz_off))  # a device copy, then the fused COO launch right behind it
+            Cc = h.coo(ro, None, no, T(b.coo_idx), T(b.coo_vals), B, checked=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(ro.cpu().numpy(), oracle.offsets(b.sizes))
+            assert_parity(b, C.cpu().numpy(), f"csr {kern} {bits}")
+            assert_parity(b, Cc.cpu().numpy(), f"coo {kern} {bits}")
+    finally:
+        h.set_debug(0)
+        h.set_tile_cb(0)
+        h.set_hints(0, 0)
