@@ -54,14 +54,16 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * leave Y undefined; timing only); 524288 = GCN layer with two groups of
  * Z-producer warps instead of three (3xTF32: three instead of two);
  * bits 20-21 = GCN feature-tile width (1: 64, 2: 128, 3: 256; 0: planner);
- * bit 22 (4194304) = standalone SDDMM reading the CSR structure from global
- * memory (the round-1 kernel) instead of the double-buffered shared stage;
- * bit 23 (8388608) = standalone SDDMM prefetching two grad_C rows ahead
- * instead of one (k = 256); bit 24 (16777216) = tile kernels without the
- * pre-wait L2 prefetch of B and the matrix's structure; bit 25 (33554432) =
+ * bit 22 (4194304) = GCN layer on CTA pairs (cta_group::2) regardless of the
+ * planner, bit 23 (8388608) = GCN layer on single CTAs; bit 24 (16777216)
+ * = SpMM kernels (tile and pipeline) without the pre-wait L2 prefetch of B
+ * and the matrices' structure; bit 25 (33554432) =
  * that prefetch without the structure; bit 26 (67108864) = with the CSR
  * (col, val) run as well (default: B and the row-pointer slice; SparseTensor
- * input: B and the (idx, val) slice).  0 (default) = normal. */
+ * input: B and the (idx, val) slice); bit 27 (134217728) = standalone SDDMM
+ * reading the CSR structure from global memory (the round-1 kernel) instead
+ * of the double-buffered shared stage; bit 28 (268435456) = standalone SDDMM
+ * prefetching two grad_C rows ahead instead of one (k = 256).  0 (default) = normal. */
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits);
 
 /* Small-batch tile kernel (spmm_tile.cu): float4 columns per tile (1, 2, 4,

@@ -27,8 +27,8 @@ constexpr int kBwdThreads = 256;
 // experiment bits (include/bspmm_debug.h): the standalone SDDMM with its
 // structure read from global memory (the round-1 kernel); two grad_C rows
 // prefetched instead of one
-constexpr int32_t kDbgSddmmGlobalStruct = 1 << 22;
-constexpr int32_t kDbgSddmmPf2 = 1 << 23;
+constexpr int32_t kDbgSddmmGlobalStruct = 1 << 27;
+constexpr int32_t kDbgSddmmPf2 = 1 << 28;
 
 // CSR -> per-matrix transposed CSR, one warp per matrix (see the header).
 // Entries of A_i are visited in storage order = (row, position) order, so a

@@ -354,7 +354,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits >= (1 << 27)) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits >= (1 << 29)) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }

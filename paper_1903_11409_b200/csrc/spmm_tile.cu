@@ -260,8 +260,10 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
   int64_t g0;
   int32_t n;
   if (p.row_off) {
-    g0 = p.row_off[i];
-    n = p.sizes ? __ldg(p.sizes + i) : (int32_t)(p.row_off[i + 1] - g0);
+    // read-only path: the 8-16 CTAs of an SM share the L1 line instead of
+    // each warp sending its own request to the same few L2 lines
+    g0 = __ldg(p.row_off + i);
+    n = p.sizes ? __ldg(p.sizes + i) : (int32_t)(__ldg(p.row_off + i + 1) - g0);
   } else {  // packed layout, offsets fused into the launch
     n = __ldg(p.sizes + i);
     g0 = tile_sizes_prefix(p.sizes, i);
@@ -399,10 +401,10 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileP
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tile_trace(p, 1);
   // ---- RT1: where the matrix and its entries live (independent loads)
-  const int64_t g0 = p.row_off[i];
-  const int32_t n = p.sizes ? __ldg(p.sizes + i) : (int32_t)(p.row_off[i + 1] - g0);
-  const int64_t z0 = p.nnz_off[i];
-  const int32_t nz = (int32_t)(p.nnz_off[i + 1] - z0);
+  const int64_t g0 = __ldg(p.row_off + i);
+  const int32_t n = p.sizes ? __ldg(p.sizes + i) : (int32_t)(__ldg(p.row_off + i + 1) - g0);
+  const int64_t z0 = __ldg(p.nnz_off + i);
+  const int32_t nz = (int32_t)(__ldg(p.nnz_off + i + 1) - z0);
   if (n <= 0) return;
   if (n > p.cap_rows || nz > p.cap_nnz) {  // beyond the hints: skipped, reported by bspmm_sync
     if (t == 0) atomicOr(p.err, 64);

@@ -162,13 +162,13 @@ def test_sddmm_streaming_batch(h, dbg):
         h.set_hints(0, 0)
 
 
-@pytest.mark.parametrize("dbg", [0, 1 << 22, 1 << 23])
+@pytest.mark.parametrize("dbg", [0, 1 << 27, 1 << 28])
 @pytest.mark.parametrize("k,ld", [(256, 256), (128, 128), (64, 64), (200, 204), (256, 260), (384, 384)])
 def test_sddmm_standalone_kernels(h, k, ld, dbg):
     """The standalone SDDMM for streaming batches (1500 matrices > 8 per SM):
     the structure-staged kernel (k <= 256; all lanes active at k = 128 / 256,
-    guarded lanes otherwise), its grad_C prefetch-2 variant (bit 23), the
-    global-structure kernel (bit 22, and k > 256), with ld > k, rows of 0-9
+    guarded lanes otherwise), its grad_C prefetch-2 variant (bit 28), the
+    global-structure kernel (bit 27, and k > 256), with ld > k, rows of 0-9
     entries (1-3 four-entry butterfly groups, duplicates, empty rows and
     graphs); integer-valued inputs exactly, U[-1,1) within the bound.  Then
     hints below the batch's largest matrix: those matrices take the

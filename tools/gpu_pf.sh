@@ -1,7 +1,7 @@
 # pre-wait prefetch A/B (kbench, default vs debug bit 24) + parity tests
 set -u
 O=gpurun_out/pf${1:-1}; mkdir -p $O
-timeout 300 python tools/kbench.py --configs 3,4,2 --dbg 0,16777216,0,16777216 --coo-dbg 16777216 > $O/kbench.jsonl 2> $O/kbench.err
+timeout 300 python tools/kbench.py --configs 4 --tile-cbs 8,16,32,8,16,32,8,16,32  > $O/kbench.jsonl 2> $O/kbench.err
 python - "$O" <<'PY'
 import json, sys
 for l in open(sys.argv[1] + "/kbench.jsonl"):

@@ -177,6 +177,7 @@ def main():
     ap.add_argument("--shard", type=int, default=1, help="time rank 0's shard of an N-way split (1 GPU)")
     ap.add_argument("--backward", action="store_true", help="also time csr_backward (grad_B and grad_vals)")
     ap.add_argument("--sddmm-dbg", default="", help="with --backward: debug bit sets for extra SDDMM timings")
+    ap.add_argument("--tile-cbs", default="0", help="tile-kernel column blocks to sweep (bspmm_set_tile_cb)")
     ap.add_argument("--coo-dbg", default="", help="debug bit sets for extra fused-COO timings")
     ap.add_argument("--trace", action="store_true", help="phase trace of the last launch of the graph (per dbg)")
     args = ap.parse_args()
@@ -205,8 +206,10 @@ def main():
                                             [int(x) for x in args.warps.split(",")],
                                             [int(x) for x in args.ctas.split(",")],
                                             [int(x) for x in args.chunks.split(",")]))
-        combos = [(kt, w, c, ch, d) for kt, w, c, ch in combos for d in [int(x) for x in args.dbg.split(",")]]
-        for kt, w, c, ch, dbg in combos:
+        combos = [(kt, w, c, ch, d, cb) for kt, w, c, ch in combos for d in [int(x) for x in args.dbg.split(",")]
+                  for cb in [int(x) for x in args.tile_cbs.split(",")]]
+        for kt, w, c, ch, dbg, cb in combos:
+            h.set_tile_cb(cb)
             if kt and kt > b.k:
                 continue
             h.set_tuning(kt, w, c, ch)
@@ -219,11 +222,13 @@ def main():
             plan = h.last_plan()
             gbs = per / (ms / 1e3) / 1e9
             tr = {"trace": trace_in_graph(h, reps, R)} if args.trace else {}
-            print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "chunks": ch, "dbg": dbg, "us": ms * 1e3, "GBs": gbs,
+            print(json.dumps({"config": cid, "kt": kt, "warps": w, "ctas": c, "chunks": ch, "dbg": dbg, "tile_cb": cb,
+                              "us": ms * 1e3, "GBs": gbs,
                               "frac": gbs / peak, "GFLOPs": 2 * b.n_nnz * b.k / (ms / 1e3) / 1e9,
                               "replicas": len(reps), "shard": args.shard, "plan": plan, **tr}), flush=True)
         h.set_tuning(0, 0, 0)
         h.set_debug(0)
+        h.set_tile_cb(0)
         ms_step = time_calls(h, reps, R, full_step)
         ms_fused = time_calls(h, reps, R, fused_step)
         ms_off = time_calls(h, reps, R, offsets_only)
