@@ -169,6 +169,22 @@ class Clocks:
                     self._warned = True
             time.sleep(self.period)
 
+    def sample_now(self):
+        """One synchronous sample from the calling thread (the timed region's own
+        poll loop: it does not depend on the sampler thread being scheduled)."""
+        if not self.ok or self.source != "nvml" or not self.active.is_set():
+            return
+        try:
+            nv = self.nv
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            mhz = nv.nvmlDeviceGetClockInfo(self.dev, nv.NVML_CLOCK_SM)
+            why = int(get_r(self.dev))
+            self.samples.append(mhz)
+            self.reasons |= why
+        except Exception:
+            pass
+
     def __enter__(self):
         if self.ok:
             self._t = threading.Thread(target=self._run, daemon=True)
@@ -478,6 +494,9 @@ def main():
     for s in range(K):
         step(kev[s])
     t1.record(stream)
+    while not t1.query():  # the GPU is still in the timed region: sample its clocks here too
+        clk.sample_now()
+        time.sleep(0.002)
     torch.cuda.synchronize(dev)
     clk.active.clear()
     clk.__exit__()
