@@ -1,0 +1,13 @@
+# quick A/B: kbench C4/C2 (twice) + a short bench line (clock sampling check)
+set -u
+O=gpurun_out/q${1:-1}; mkdir -p $O
+timeout 300 python tools/kbench.py --configs 4,2,3 --dbg 0,0 ${2:-} > $O/kbench.jsonl 2> $O/kbench.err
+python - "$O" <<'PY'
+import json, sys
+for l in open(sys.argv[1] + "/kbench.jsonl"):
+    d = json.loads(l)
+    if "us" in d: print(d["config"], d["dbg"], d.get("tile_cb"), round(d["us"], 3), round(d["frac"], 3))
+    else: print(d["config"], {k: round(v, 2) for k, v in d.items() if "coo_convert" in k})
+PY
+timeout 300 python bench.py --steps 100 --warmup 5 --no-e2e --no-cpu-baseline > $O/bench.json 2> $O/bench.err
+python -c "import json; d=json.loads(open('$O/bench.json').read().strip().splitlines()[-1]); print(d['value'], d['clocks'])"
