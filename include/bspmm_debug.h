@@ -47,8 +47,8 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * 8192 = GCN layer with one batched GEMM before the channel SpMMs instead
  * of channel GEMMs pipelined on the auxiliary stream; 16384 = never the
  * small-batch tile kernel (small batches run the pipeline kernel); 32768 =
- * tile kernel stages B by 2-D tensor TMA where that applies (default:
- * cp.async); 65536 = tile
+ * tile kernel stages B by 16-byte cp.async everywhere (default: 2-D tensor
+ * TMA for column blocks of >= 8 float4); 65536 = tile
  * kernel issues its row-pointer round trip after the B tile; 131072 = GCN
  * layer without the Z arithmetic, 262144 = GCN layer without the MMAs (both
  * leave Y undefined; timing only); 524288 = GCN layer with two groups of

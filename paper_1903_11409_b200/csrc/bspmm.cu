@@ -448,7 +448,7 @@ static bspmm_status_t csr_impl(bspmm_handle_t h, int32_t batch, int32_t k, const
     plan.threads = 128;
     plan.smem_bytes = L.smem;
     h->last_plan = plan;
-    const TmaMaps* maps = (L.cb >= 8 && (h->dbg & 32768)) ? tma_maps(h, B, k, ldb, 4 * L.cb) : nullptr;
+    const TmaMaps* maps = (L.cb >= 8 && !(h->dbg & 32768)) ? tma_maps(h, B, k, ldb, 4 * L.cb) : nullptr;
     CsrArgs a{batch, k, row_off, sizes, row_ptr, col_idx, vals, B, ldb, C, ldc, h->trace, h->dbg, maps, bias,
               accumulate};
     if (!(h->dbg & kDbgNoPrewaitPrefetch)) {

@@ -661,11 +661,13 @@ cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t
   tp.bias = reinterpret_cast<const float4*>(a.bias);
   tp.accumulate = a.accumulate;
   tp.trace = a.trace;
-  // B by 16-byte cp.async (config 4: 6.69-6.71 us per call against 6.87-6.88
-  // for 2-D tensor TMA, tools/probe/tile_balance.py); debug bit 32768 stages
-  // it by 2-D TMA where that applies (the handle's descriptors for box width
-  // 4 * cb, a 128-byte shared row pitch)
-  tp.tma = (a.maps != nullptr && L.cb >= 8 && (a.dbg & 32768)) ? 1 : 0;
+  // B by 2-D tensor TMA where that applies (the handle's descriptors for box
+  // width 4 * cb, a 128-byte shared row pitch; column blocks of >= 8 float4),
+  // else by 16-byte cp.async (debug bit 32768: always cp.async).  With the
+  // pre-wait prefetch the tile is an L2 hit and TMA's few bulk copies leave
+  // the LSU to the structure round trips: C4 5.62-5.65 vs 5.83-5.85 us (the
+  // order was the reverse before the prefetch: 6.87 vs 6.70 us)
+  tp.tma = (a.maps != nullptr && L.cb >= 8 && !(a.dbg & 32768)) ? 1 : 0;
   tp.rp_first = (a.dbg & 65536) ? 0 : 1;
   tp.dbg_bits = ((a.dbg & 16) ? 1 : 0) | ((a.dbg & (1 << 26)) ? 2 : 0);
   tp.nnz_off = a.coo_nnz_off;

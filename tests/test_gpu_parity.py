@@ -58,9 +58,9 @@ def assert_parity(b, C, what=""):
 
 # debug bit 16384 keeps small batches on the pipeline kernel (spmm_csr.cu);
 # 0 lets the planner choose; "tile" forces the small-batch tile kernel
-# (spmm_tile.cu) with 8-float4 column blocks (cp.async staging), "tile_tma"
-# the same kernel staging B by 2-D tensor TMA (debug bit 32768)
-KERNELS = {"auto": (0, 0), "pipeline": (16384, 0), "tile": (0, 8), "tile_tma": (32768, 8)}
+# (spmm_tile.cu) with 8-float4 column blocks (2-D tensor TMA staging of B),
+# "tile_cpasync" the same kernel staging B by cp.async (debug bit 32768)
+KERNELS = {"auto": (0, 0), "pipeline": (16384, 0), "tile": (0, 8), "tile_cpasync": (32768, 8)}
 
 
 def use_kernel(h, kern):
@@ -676,9 +676,9 @@ def test_tile_shapes(h, k, nlo, nhi, batch):
     h.csr(None, T(b.sizes), T(b.row_ptr), T(b.col), T(b.vals), T(b.B), Cd)   # fused offsets
     torch.cuda.synchronize()
     assert np.array_equal(Cd.cpu().numpy().view(np.uint32), out["pipeline"].view(np.uint32))
-    for kern in ("tile", "tile_tma"):
+    for kern in ("tile", "tile_cpasync"):
         assert np.array_equal(out[kern].view(np.uint32), out["pipeline"].view(np.uint32)), kern
-    for dbg in (0, 32768):                              # cp.async / 2-D TMA staging of B
+    for dbg in (0, 32768):                              # 2-D TMA / cp.async staging of B
         for cb in (1, 2, 4, 8, 16, 32):
             h.set_tile_cb(cb)
             h.set_debug(dbg)
