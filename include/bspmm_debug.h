@@ -58,9 +58,9 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf);
  * planner, bit 23 (8388608) = GCN layer on single CTAs; bit 24 (16777216)
  * = SpMM kernels (tile and pipeline) without the pre-wait L2 prefetch of B
  * and the matrices' structure; bit 25 (33554432) =
- * that prefetch without the structure; bit 26 (67108864) = with the CSR
- * (col, val) run as well (default: B and the row-pointer slice; SparseTensor
- * input: B and the (idx, val) slice); bit 27 (134217728) = standalone SDDMM
+ * that prefetch without the structure; bit 26 (67108864) = without the
+ * CSR (col, val) run (default: B, the row-pointer slice and the (col, val)
+ * run; SparseTensor input: B and the (idx, val) slice); bit 27 (134217728) = standalone SDDMM
  * reading the CSR structure from global memory (the round-1 kernel) instead
  * of the double-buffered shared stage; bit 28 (268435456) = standalone SDDMM
  * prefetching two grad_C rows ahead instead of one (k = 256).  0 (default) = normal. */

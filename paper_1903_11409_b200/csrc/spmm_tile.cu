@@ -109,10 +109,11 @@ __device__ __forceinline__ void tile_prefetch_b(const TileParams& p) {
                         p.s_hi[0]);
     const uint64_t rp = reinterpret_cast<uint64_t>(p.row_ptr);
     if (rp + 4 * (uint64_t)g0 < p.s_lo[0] || rp + 4 * (uint64_t)g1 + 4 > p.s_hi[0]) return;
-    // not the (col, val) run: its second dependent read measured slower on C4
-    // (6.1 vs 5.85 us; C2 2.9 vs 3.0) -- a CTA that becomes resident only at
-    // the release carries it into its critical path
-    if (!(p.dbg_bits & 2)) return;
+    // and the (col, val) run (a second dependent read): with cp.async staging
+    // it measured slower on C4 (6.1 vs 5.85 us), with TMA staging -- the
+    // default -- C4 5.52-5.60 vs 5.60-5.62 and C2 2.87 vs 3.04 us; debug bit
+    // 26 leaves it out
+    if (p.dbg_bits & 2) return;
     z0 = ld_relaxed_s32(p.row_ptr + g0);
     z1 = ld_relaxed_s32(p.row_ptr + g1);
     if (z1 <= z0 || z1 - z0 > (1 << 24) || !p.s_hi[1]) return;

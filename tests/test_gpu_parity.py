@@ -712,7 +712,7 @@ def test_tile_fallbacks(h):
 
 
 # ------------------------------------------------ pre-wait L2 prefetch (PDL)
-PF_BITS = {"default": 0, "no_prefetch": 1 << 24, "b_only": 1 << 25, "with_col_val_run": 1 << 26}
+PF_BITS = {"default": 0, "no_prefetch": 1 << 24, "b_only": 1 << 25, "no_col_val_run": 1 << 26}
 
 
 @pytest.mark.parametrize("bits", list(PF_BITS))
