@@ -1,6 +1,6 @@
 set -u
 O=gpurun_out/pft${1:-1}; mkdir -p $O
-timeout 300 python tools/kbench.py --configs 4 --dbg 0,16777216 --trace > $O/kbench.jsonl 2> $O/kbench.err
+timeout 300 python tools/kbench.py --configs ${2:-4} --dbg 0,16777216 --trace > $O/kbench.jsonl 2> $O/kbench.err
 python - "$O" <<'PY'
 import json, sys
 for l in open(sys.argv[1] + "/kbench.jsonl"):

@@ -1,7 +1,7 @@
 # quick A/B: kbench C4/C2 (twice) + a short bench line (clock sampling check)
 set -u
 O=gpurun_out/q${1:-1}; mkdir -p $O
-timeout 300 python tools/kbench.py --configs 4,2 --dbg ${2:-0,32768,0,32768,0,32768} > $O/kbench.jsonl 2> $O/kbench.err
+timeout 300 python tools/kbench.py --configs ${4:-4,2} --dbg ${2:-0,67108864} --tile-cbs ${3:-0,16} > $O/kbench.jsonl 2> $O/kbench.err
 python - "$O" <<'PY'
 import json, sys
 for l in open(sys.argv[1] + "/kbench.jsonl"):
