@@ -417,16 +417,23 @@ class Handle:
 
     def csr_backward(self, row_off: torch.Tensor, sizes: Optional[torch.Tensor], row_ptr: torch.Tensor,
                      col: torch.Tensor, vals: torch.Tensor, B: torch.Tensor, grad_C: torch.Tensor,
-                     want_B: bool = True, want_vals: bool = True):
-        """(grad_B, grad_vals) of C = A B for upstream grad_C (bspmm_csr_backward)."""
+                     want_B: bool = True, want_vals: bool = True, k: Optional[int] = None,
+                     grad_B: Optional[torch.Tensor] = None, grad_vals: Optional[torch.Tensor] = None):
+        """(grad_B, grad_vals) of C = A B for upstream grad_C (bspmm_csr_backward).
+        k defaults to grad_C's width (smaller: the leading k columns of row-strided
+        B / grad_C); grad_B / grad_vals: optional output tensors (else allocated)."""
         dev = self.device
         for name, t, dt in (("row_off", row_off, torch.int64), ("sizes", sizes, torch.int32),
                             ("row_ptr", row_ptr, torch.int32), ("col", col, torch.int32),
-                            ("vals", vals, torch.float32), ("B", B, torch.float32), ("grad_C", grad_C, torch.float32)):
+                            ("vals", vals, torch.float32), ("B", B, torch.float32), ("grad_C", grad_C, torch.float32),
+                            ("grad_B", grad_B, torch.float32), ("grad_vals", grad_vals, torch.float32)):
             _check(t, name, dt, dev)
-        k = grad_C.shape[1]
-        gB = torch.empty((grad_C.shape[0], k), dtype=torch.float32, device=dev) if want_B else None
-        gv = torch.empty(col.shape[0], dtype=torch.float32, device=dev) if want_vals else None
+        k = grad_C.shape[1] if k is None else int(k)
+        gB = grad_B if grad_B is not None else (
+            torch.empty((grad_C.shape[0], k), dtype=torch.float32, device=dev) if want_B else None)
+        gv = grad_vals if grad_vals is not None else (
+            torch.empty(col.shape[0], dtype=torch.float32, device=dev) if want_vals else None)
+        want_B = gB is not None
         self._stream()
         st = lib.bspmm_csr_backward(self._h, row_off.shape[0] - 1, k, _ptr(row_off), _ptr(sizes), _ptr(row_ptr),
                                     _ptr(col), _ptr(vals), _ptr(B), _ld(B, k, "B"), _ptr(grad_C),

@@ -631,6 +631,310 @@ __global__ void __launch_bounds__(kBwdThreads, 3) sddmm_struct_kernel(int32_t ba
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused backward for streaming batches (both adjoints, round 2): per matrix,
+// grad_C_i is staged in shared memory ONCE and feeds both
+//   grad_B_i = A_i^T grad_C_i      (bitwise the storage-order fp32 sum over
+//                                   the canonical A_i^T, as the transpose +
+//                                   forward-kernel path computes it)
+//   grad_vals_e = <grad_C[row_e], B[col_e]>   (the SDDMM's bits)
+// so grad_C is read once and no A^T is written to or read from HBM: C5 moves
+// B + grad_C in and grad_B out (8.1 GB) instead of the separate kernels'
+// 10.9 GB plus the transpose pass.  CTA flow per matrix (3 CTAs x 8 warps per
+// SM, persistent): the next matrix's CSR slice (row pointers, column ids,
+// values) is cp.async'ed into the other half of a double-buffered stage, its
+// metadata through the SDDMM kernel's 4-slot ring; grad_C_i lands by one
+// bulk copy while warp 0 transposes A_i in shared memory (column counts by
+// shared atomics, a warp scan, then a scatter 32 entries at a time in storage
+// order with equal columns ranked by __match_any_sync -- a stable counting
+// sort, so A^T comes out in canonical (row, col, original position) order);
+// then warp
+// w owns rows c = w, w + 8, ... of A^T (= rows of B and grad_B): B's row in
+// registers (loaded one row ahead), every entry (r, v, e) of the row reads
+// grad_C's row r from shared memory once for the FMA into grad_B and the dot
+// product with B's row (two entries per butterfly, the xor-16 step swapping
+// them).  A matrix above the stage capacities takes the out-of-line global
+// path (below).
+template <int CH>
+__device__ __noinline__ void bwd_fused_global(int32_t n, int32_t k, int64_t g0, const int32_t* __restrict__ row_ptr,
+                                              const int32_t* __restrict__ col, const float* __restrict__ vals,
+                                              const float* __restrict__ B, int64_t ldb,
+                                              const float* __restrict__ Gg, int64_t ldg, float* __restrict__ gB,
+                                              int64_t ldgb, float* __restrict__ gvals) {
+  // over-capacity matrix: grad_vals by the SDDMM's global loop; grad_B row c
+  // by scanning the matrix's entries in storage order for column c (the
+  // canonical A^T order), grad_C rows from global memory
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  sddmm_rows<CH, false>(n, k >> 2, B + g0 * ldb, ldb, Gg + g0 * ldg, ldg, row_ptr + g0, col, gvals, lane, warp, nw);
+  const int32_t z0 = __ldg(row_ptr + g0), z1 = __ldg(row_ptr + g0 + n);
+  for (int32_t c = warp; c < n; c += nw) {
+    for (int32_t j = lane; j < k; j += 32) {
+      float acc = 0.f;
+      int32_t r = 0;
+      for (int32_t e = z0; e < z1; ++e) {
+        while (e >= __ldg(row_ptr + g0 + r + 1)) ++r;
+        if (__ldg(col + e) == c) acc = fmaf(__ldg(vals + e), __ldg(Gg + (g0 + r) * ldg + j), acc);
+      }
+      gB[(g0 + c) * ldgb + j] = acc;
+    }
+  }
+}
+
+template <int CH, bool FULL>
+__global__ void __launch_bounds__(kBwdThreads, 3) backward_fused_kernel(
+    int32_t batch, int32_t k, const int64_t* __restrict__ row_off, const int32_t* __restrict__ sizes,
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const float* __restrict__ vals,
+    const float* __restrict__ B, int64_t ldb, const float* __restrict__ G_, int64_t ldg, float* __restrict__ gB,
+    int64_t ldgb, float* __restrict__ gvals, int32_t cap_bytes, int32_t rcap, int32_t ecap, int32_t dbg) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ SdMeta meta[4];
+  float* Gs = reinterpret_cast<float*>(smem);
+  int32_t* s_rp = reinterpret_cast<int32_t*>(smem + cap_bytes);  // [2][rcap]
+  int32_t* s_col = s_rp + 2 * rcap;                              // [2][ecap]
+  float* s_val = reinterpret_cast<float*>(s_col + 2 * ecap);     // [2][ecap]
+  int32_t* t_rp2 = reinterpret_cast<int32_t*>(s_val + 2 * ecap);  // [2][rcap]: A^T row pointers (column counts
+                                                                  // first), double-buffered: the next matrix's
+                                                                  // counters are zeroed while this one runs
+  int32_t* t_row = t_rp2 + 2 * rcap;                             // [ecap]: A^T entry -> source row
+  float* t_val = reinterpret_cast<float*>(t_row + ecap);         // [ecap]
+  int32_t* t_pos = reinterpret_cast<int32_t*>(t_val + ecap);     // [ecap]: A^T entry -> A's entry (local)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t G = gridDim.x;
+  auto rows_of = [&](const SdMeta& m) -> int32_t { return sizes ? m.n : (int32_t)(m.gnext - m.g); };
+  auto fetch_rows = [&](int64_t m, SdMeta& d) {
+    if (m < batch) {
+      cp_async8(&d.g, row_off + m);
+      if (sizes) cp_async4(&d.n, sizes + m);
+      else cp_async8(&d.gnext, row_off + m + 1);
+    } else {
+      d.g = d.gnext = 0;
+      d.n = 0;
+    }
+  };
+  auto fetch_entries = [&](SdMeta& d) {
+    const int32_t n = rows_of(d);
+    if (n > 0) {
+      cp_async4(&d.ea, row_ptr + d.g);
+      cp_async4(&d.eb, row_ptr + d.g + n);
+    } else {
+      d.ea = d.eb = 0;
+    }
+  };
+  auto fits = [&](int32_t n_, int32_t ea, int32_t eb) {
+    return n_ > 0 && (int64_t)n_ * k * 4 <= cap_bytes && n_ + 1 <= rcap && eb - ea <= ecap;
+  };
+  auto stage_struct = [&](int buf, const SdMeta& d) {
+    const int32_t n = rows_of(d);
+    if (fits(n, d.ea, d.eb)) {
+      for (int32_t t = threadIdx.x; t <= n; t += blockDim.x) cp_async4(s_rp + buf * rcap + t, row_ptr + d.g + t);
+      for (int32_t t = threadIdx.x; t < d.eb - d.ea; t += blockDim.x) {
+        cp_async4(s_col + buf * ecap + t, col + d.ea + t);
+        cp_async4(s_val + buf * ecap + t, vals + d.ea + t);
+      }
+    }
+  };
+  const int64_t i0 = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    for (int q = 0; q < 3; ++q) fetch_rows(i0 + q * G, meta[q]);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (threadIdx.x == 32)
+    for (int q = 0; q < 2; ++q) fetch_entries(meta[q]);
+  cp_async_wait_all();
+  __syncthreads();
+  stage_struct(0, meta[0]);
+  for (int32_t c = threadIdx.x; c < 2 * rcap; c += blockDim.x) t_rp2[c] = 0;  // column counters
+  cp_async_wait_all();
+  __syncthreads();
+  uint32_t phase = 0;
+  int j = 0;
+  for (int64_t i = i0; i < batch; i += G, ++j) {
+    const SdMeta& m0 = meta[j & 3];
+    const int32_t n0 = rows_of(m0);
+    const int64_t g0 = m0.g;
+    const int32_t e0a = m0.ea, nnz = m0.eb - m0.ea;
+    const bool staged = fits(n0, m0.ea, m0.eb);
+    int32_t* t_rp = t_rp2 + (j & 1) * rcap;
+    if (threadIdx.x == 0) {
+      const SdMeta& m1 = meta[(j + 1) & 3];
+      const int32_t n1 = rows_of(m1);
+      if (n1 > 0 && !(dbg & 512)) {  // the next matrix's grad_C and B rows into L2
+        bulk_prefetch_l2(G_ + m1.g * ldg, (uint32_t)(((int64_t)(n1 - 1) * ldg + k) * 4));
+        bulk_prefetch_l2(B + m1.g * ldb, (uint32_t)(((int64_t)(n1 - 1) * ldb + k) * 4));
+      }
+      if (staged) {
+        const uint32_t bytes = (uint32_t)n0 * (uint32_t)k * 4u;
+        mbar_arrive_expect_tx(&bar, bytes);
+        if (ldg == k) {
+          bulk_g2s(Gs, G_ + g0 * ldg, bytes, &bar);
+        } else {
+          for (int32_t r = 0; r < n0; ++r) bulk_g2s(Gs + (int64_t)r * k, G_ + (g0 + r) * ldg, (uint32_t)k * 4u, &bar);
+        }
+      }
+      fetch_rows(i + 3 * G, meta[(j + 3) & 3]);
+    }
+    if (threadIdx.x == 32) fetch_entries(meta[(j + 2) & 3]);
+    stage_struct((j + 1) & 1, meta[(j + 1) & 3]);
+    {  // the next matrix's column counters (that buffer was last read a matrix ago)
+      int32_t* t_nx = t_rp2 + ((j + 1) & 1) * rcap;
+      for (int32_t c = threadIdx.x; c < rcap; c += blockDim.x) t_nx[c] = 0;
+    }
+    if (staged) {
+      const int32_t* rp = s_rp + (j & 1) * rcap;
+      const int32_t* cs = s_col + (j & 1) * ecap;
+      const float* vs = s_val + (j & 1) * ecap;
+      // B's first row of this warp (registers), in flight during the transpose
+      float4 bq[CH];
+      auto bload = [&](int32_t c_, float4* dst) {
+        const float* brow = B + (g0 + c_) * ldb + 4 * lane;
+#pragma unroll
+        for (int v = 0; v < CH; ++v)
+          dst[v] = (FULL || lane + 32 * v < (k >> 2)) ? ldg_nc_f4(brow + 128 * v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      };
+      if (warp < n0) bload(warp, bq);
+      // ---- A_i^T in shared memory (while grad_C_i lands): column counts by
+      // shared atomics (the counters were zeroed at the end of the previous
+      // matrix), a warp scan, then every entry's slot = its column's start +
+      // the number of earlier entries of that column (stable)
+      for (int32_t e = threadIdx.x; e < nnz; e += blockDim.x) atomicAdd(&t_rp[cs[e] + 1], 1);
+      __syncthreads();
+      if (warp == 0) {  // inclusive scan of t_rp[1..n0] -> row pointers of A^T (t_rp[0] = 0)
+        int32_t carry = 0;
+        for (int32_t c0 = 1; c0 <= n0; c0 += 32) {
+          const int32_t c = c0 + lane;
+          int32_t x = c <= n0 ? t_rp[c] : 0;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+          }
+          if (c <= n0) t_rp[c] = carry + x;
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+      __syncthreads();
+      for (int32_t e = threadIdx.x; e < nnz; e += blockDim.x) {
+        const int32_t c = cs[e];
+        int32_t rank = 0, q = 0;
+        for (; q + 4 <= e; q += 4) {  // 4 column ids per shared load (the stage is 16-byte aligned)
+          const int4 c4 = *reinterpret_cast<const int4*>(cs + q);
+          rank += (c4.x == c) + (c4.y == c) + (c4.z == c) + (c4.w == c);
+        }
+        for (; q < e; ++q) rank += cs[q] == c ? 1 : 0;
+        int32_t lo = 0, hi = n0 - 1;  // source row: the last r with rp[r] - e0a <= e
+        while (lo < hi) {
+          const int32_t mid = (lo + hi + 1) >> 1;
+          if (rp[mid] - e0a <= e) lo = mid;
+          else hi = mid - 1;
+        }
+        const int32_t slot = t_rp[c] + rank;
+        t_row[slot] = lo;
+        t_val[slot] = vs[e];
+        t_pos[slot] = e;
+      }
+      __syncthreads();
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      float* ov = gvals + e0a;
+      for (int32_t c = warp; c < n0; c += nw) {
+        float4 b[CH];
+#pragma unroll
+        for (int v = 0; v < CH; ++v) b[v] = bq[v];
+        if (c + nw < n0) bload(c + nw, bq);
+        float4 acc[CH];
+#pragma unroll
+        for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int32_t sa = t_rp[c], sb = t_rp[c + 1];
+        for (int32_t s2 = sa; s2 < sb; s2 += 2) {
+          const bool two = s2 + 1 < sb;  // warp-uniform
+          const float* g0p = Gs + t_row[s2] * k + 4 * lane;
+          const float* g1p = Gs + t_row[two ? s2 + 1 : s2] * k + 4 * lane;
+          const float v0 = t_val[s2], v1 = two ? t_val[s2 + 1] : 0.f;
+          float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+          for (int v = 0; v < CH; ++v) {
+            if (FULL || lane + 32 * v < (k >> 2)) {
+              const float4 ga = *reinterpret_cast<const float4*>(g0p + 128 * v);
+              acc[v].x = fmaf(v0, ga.x, acc[v].x); acc[v].y = fmaf(v0, ga.y, acc[v].y);
+              acc[v].z = fmaf(v0, ga.z, acc[v].z); acc[v].w = fmaf(v0, ga.w, acc[v].w);
+              p0 = fmaf(ga.x, b[v].x, p0); p0 = fmaf(ga.y, b[v].y, p0);
+              p0 = fmaf(ga.z, b[v].z, p0); p0 = fmaf(ga.w, b[v].w, p0);
+              if (two) {
+                const float4 gb = *reinterpret_cast<const float4*>(g1p + 128 * v);
+                acc[v].x = fmaf(v1, gb.x, acc[v].x); acc[v].y = fmaf(v1, gb.y, acc[v].y);
+                acc[v].z = fmaf(v1, gb.z, acc[v].z); acc[v].w = fmaf(v1, gb.w, acc[v].w);
+                p1 = fmaf(gb.x, b[v].x, p1); p1 = fmaf(gb.y, b[v].y, p1);
+                p1 = fmaf(gb.z, b[v].z, p1); p1 = fmaf(gb.w, b[v].w, p1);
+              }
+            }
+          }
+          // xor-16 step with the pair swapped (lanes < 16: entry s2, others s2 + 1)
+          const bool hi16 = lane & 16;
+          float pp = (hi16 ? p1 : p0) + __shfl_xor_sync(0xffffffffu, hi16 ? p0 : p1, 16);
+#pragma unroll
+          for (int d = 8; d > 0; d >>= 1) pp += __shfl_xor_sync(0xffffffffu, pp, d);
+          if (lane == 0) ov[t_pos[s2]] = pp;
+          if (lane == 16 && two) ov[t_pos[s2 + 1]] = pp;
+        }
+        float* grow = gB + (g0 + c) * ldgb + 4 * lane;
+#pragma unroll
+        for (int v = 0; v < CH; ++v)
+          if (FULL || lane + 32 * v < (k >> 2)) stg_cs_f4(grow + 128 * v, acc[v]);
+      }
+    } else if (n0 > 0) {
+      bwd_fused_global<CH>(n0, k, g0, row_ptr, col, vals, B, ldb, G_, ldg, gB, ldgb, gvals);
+    }
+    cp_async_wait_all();  // the next matrix's structure and the metadata ring
+    __syncthreads();      // ... visible to every warp; every warp is done with Gs and the A^T stage
+  }
+}
+
+cudaError_t launch_backward_fused(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
+                                  const int32_t* row_ptr, const int32_t* col, const float* vals, const float* B,
+                                  int64_t ldb, const float* G, int64_t ldg, float* gB, int64_t ldgb, float* gvals,
+                                  int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms, int32_t dbg,
+                                  cudaStream_t s, bool* used) {
+  *used = false;
+  const int chunks = k >> 2;
+  const bool vec = (k % 4 == 0) && (ldb % 4 == 0) && (ldg % 4 == 0) && (ldgb % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(G) |
+                     reinterpret_cast<uintptr_t>(gB)) & 15u) == 0;
+  // streaming batches with hints that bound every matrix (the stage is sized
+  // from them); k <= 256 (two float4 per lane)
+  if (!vec || !vals || k > 256 || max_rows_hint <= 0 || max_nnz_hint <= 0 || max_nnz_hint > 1024 ||
+      batch <= 8LL * num_sms)
+    return cudaSuccess;
+  const int32_t cap = (int32_t)(((int64_t)max_rows_hint * k * 4 + 127) & ~127LL);
+  // multiples of 4 entries: the column-id stage is read 16 bytes at a time
+  const int32_t rcap = (max_rows_hint + 1 + 3) & ~3, ecap = (int32_t)((max_nnz_hint + 3) & ~3LL);
+  const int32_t sbytes = cap + 2 * (rcap + 2 * ecap) * 4 + (2 * rcap + 3 * ecap) * 4;
+  if (sbytes > 74 * 1024) return cudaSuccess;  // 3 CTAs per SM
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto kern) {
+    if (sbytes > 47 * 1024) {  // dynamic + static above the 48 KB default
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sbytes);
+      if (e != cudaSuccess) return;
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwdThreads, sbytes);
+    if (e != cudaSuccess) return;
+    const int grid = (int)std::min<int64_t>(batch, (int64_t)num_sms * std::max(per_sm, 1));
+    kern<<<grid, kBwdThreads, sbytes, s>>>(batch, k, row_off, sizes, row_ptr, col, vals, B, ldb, G, ldg, gB, ldgb,
+                                           gvals, cap, rcap, ecap, dbg);
+    e = cudaGetLastError();
+    *used = e == cudaSuccess;
+  };
+  if (chunks == 64) go(backward_fused_kernel<2, true>);
+  else if (chunks == 32) go(backward_fused_kernel<1, true>);
+  else if (chunks <= 32) go(backward_fused_kernel<1, false>);
+  else go(backward_fused_kernel<2, false>);
+  return e;
+}
+
 cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
                          int64_t ldg, float* out, int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms,

@@ -354,7 +354,7 @@ BSPMM_API bspmm_status_t bspmm_set_trace(bspmm_handle_t h, uint64_t* dev_buf) {
 }
 
 BSPMM_API bspmm_status_t bspmm_set_debug(bspmm_handle_t h, int32_t bits) {
-  if (!h || bits < 0 || bits >= (1 << 29)) return BSPMM_ERROR_INVALID_VALUE;
+  if (!h || bits < 0 || bits >= (1 << 30)) return BSPMM_ERROR_INVALID_VALUE;
   h->dbg = bits;
   return BSPMM_SUCCESS;
 }
@@ -934,6 +934,18 @@ BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int
   if (batch == 0 || (!grad_B && !grad_vals)) return BSPMM_SUCCESS;
   if (!row_off || !row_ptr) return fail(h, BSPMM_ERROR_INVALID_VALUE, "NULL pointer argument");
   DeviceGuard g(h->device);
+  if (grad_B && grad_vals && !(h->flags & BSPMM_VALIDATE) && !(h->dbg & (2048 | kDbgNoFusedBackward)) &&
+      grad_B != grad_C) {
+    // streaming batches: one fused kernel (grad_C staged once per matrix,
+    // A^T formed in shared memory); other shapes fall through
+    bool used = false;
+    CK(h, launch_backward_fused(batch, k, row_off, sizes, row_ptr, col, vals, B, ldb, grad_C, ldgc, grad_B, ldgb,
+                                grad_vals, h->hint_rows, h->hint_nnz, h->num_sms, h->dbg, h->stream, &used));
+    if (used) {
+      h->launches++;
+      return BSPMM_SUCCESS;
+    }
+  }
   if (grad_B && grad_vals && !(h->flags & BSPMM_VALIDATE) && !(h->dbg & 2048)) {
     // both adjoints: the transpose (latency-bound) runs on an auxiliary stream
     // concurrently with the SDDMM, then grad_B = A^T grad_C once it has joined

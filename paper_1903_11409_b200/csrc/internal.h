@@ -95,6 +95,9 @@ struct CsrArgs {
 constexpr int32_t kDbgNoPrewaitPrefetch = 1 << 24;
 // debug bit 33554432: the pre-wait prefetch covers B only (not the matrix's structure)
 constexpr int32_t kDbgNoStructPrefetch = 1 << 25;
+// debug bit 536870912: backward of streaming batches by the separate kernels
+// (transpose + forward kernel, SDDMM) instead of the fused kernel
+constexpr int32_t kDbgNoFusedBackward = 1 << 29;
 // bspmm.cu: the device allocation containing p (cached per handle); false if unknown
 bool alloc_range(bspmm_handle_t h, const void* p, uint64_t* lo, uint64_t* hi);
 
@@ -170,6 +173,13 @@ cudaError_t launch_sddmm(int32_t batch, int32_t k, const int64_t* row_off, const
                          const int32_t* row_ptr, const int32_t* col, const float* B, int64_t ldb, const float* G,
                          int64_t ldg, float* out, int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms,
                          int32_t dbg, cudaStream_t s);
+// fused backward (both adjoints) for streaming batches; *used = false when the
+// shape / hints do not qualify (the caller then runs the separate kernels)
+cudaError_t launch_backward_fused(int32_t batch, int32_t k, const int64_t* row_off, const int32_t* sizes,
+                                  const int32_t* row_ptr, const int32_t* col, const float* vals, const float* B,
+                                  int64_t ldb, const float* G, int64_t ldg, float* gB, int64_t ldgb, float* gvals,
+                                  int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms, int32_t dbg,
+                                  cudaStream_t s, bool* used);
 cudaError_t launch_validate_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes,
                                 const int32_t* row_ptr, const int32_t* col, int* flag, cudaStream_t s);
 cudaError_t launch_validate_coo(int32_t batch, const int64_t* row_off, const int32_t* sizes,

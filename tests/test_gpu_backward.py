@@ -227,3 +227,52 @@ def test_backward_c5_full_size_exhaustive(h):
         rv, bv = oracle.sddmm(b.k, ro, None, rp, col, Bw, Gw)
         ok, worst = oracle.check_bound(gv[z0:z1], rv, bv)
         assert ok, (i0, i1, worst)
+
+
+FUSED_OFF = 1 << 29  # debug bit: the separate kernels (transpose + forward kernel, SDDMM)
+
+
+@pytest.mark.parametrize("k,ld", [(256, 256), (128, 128), (64, 68), (200, 204), (256, 264)])
+def test_backward_fused_streaming(h, k, ld):
+    """The fused backward kernel (streaming batches: 1500 matrices > 8 per SM,
+    hints set): grad_B bitwise equal to O3' over the oracle's A^T and to the
+    separate kernels' result (debug bit 29), grad_vals bitwise equal to the
+    separate SDDMM and within the O6 bound; duplicates, empty rows and graphs,
+    rows of 0-9 entries, ld > k; then hints below the batch's largest matrix
+    (those matrices take the fused kernel's out-of-line global path).  grad_B
+    is pre-filled with NaN: every row of every matrix must be written."""
+    rng = np.random.default_rng(k * 3 + ld)
+    b = synth.random_batch(rng, 1500, k, nmax=48, dmax=9, duplicates=True)
+    G = grad(b, k + 7)
+    Gp = np.zeros((b.n_rows, ld), dtype=np.float32)
+    Gp[:, :k] = G
+    Bp = np.zeros((b.n_rows, ld), dtype=np.float32)
+    Bp[:, :k] = b.B
+    ort, oct_, ovt = oracle.csr_transpose(b.row_off, None, b.row_ptr, b.col, b.vals)
+    ref32 = oracle.spmm_f32(k, b.row_off, None, ort, oct_, ovt, G)
+    rv, bv = oracle.sddmm(k, b.row_off, None, b.row_ptr, b.col, b.B, G)
+
+    def run(dbg, rows, nnz):
+        h.set_hints(rows, nnz)
+        h.set_debug(dbg)
+        try:
+            gB = torch.full((b.n_rows, ld), float("nan"), device=DEV)
+            gv = torch.full((b.n_nnz,), float("nan"), device=DEV)
+            h.csr_backward(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(Bp), T(Gp), k=k,
+                           grad_B=gB, grad_vals=gv)
+            torch.cuda.synchronize()
+        finally:
+            h.set_debug(0)
+            h.set_hints(0, 0)
+        return gB.cpu().numpy()[:, :k], gv.cpu().numpy()
+
+    full = (int(b.sizes.max()), int(b.nnz.max()))
+    sep_B, sep_v = run(FUSED_OFF, *full)
+    for rows, nnz in (full, (24, full[1]), (full[0], 40)):
+        gB, gv = run(0, rows, nnz)
+        nd = np.count_nonzero(gB.view(np.uint32) != ref32.view(np.uint32))
+        assert nd == 0, f"hints {rows}/{nnz}: {nd} grad_B elements differ bitwise from O3'"
+        assert np.array_equal(gB.view(np.uint32), sep_B.view(np.uint32))
+        assert np.array_equal(gv.view(np.uint32), sep_v.view(np.uint32)), f"hints {rows}/{nnz}"
+        ok, worst = oracle.check_bound(gv, rv, bv)
+        assert ok, worst

@@ -176,6 +176,7 @@ def main():
     ap.add_argument("--copy-baseline", action="store_true", help="also time C.copy_(B) on the same replicas")
     ap.add_argument("--shard", type=int, default=1, help="time rank 0's shard of an N-way split (1 GPU)")
     ap.add_argument("--backward", action="store_true", help="also time csr_backward (grad_B and grad_vals)")
+    ap.add_argument("--bwd-dbg", default="", help="with --backward: debug bit sets for extra backward timings")
     ap.add_argument("--sddmm-dbg", default="", help="with --backward: debug bit sets for extra SDDMM timings")
     ap.add_argument("--tile-cbs", default="0", help="tile-kernel column blocks to sweep (bspmm_set_tile_cb)")
     ap.add_argument("--coo-dbg", default="", help="debug bit sets for extra fused-COO timings")
@@ -238,6 +239,9 @@ def main():
             extra["backward_us"] = time_calls(h, reps, max(3, R // 4), backward) * 1e3
             extra["transpose_us"] = time_calls(h, reps, max(3, R // 4), transpose_only) * 1e3
             extra["sddmm_us"] = time_calls(h, reps, max(3, R // 4), sddmm_only) * 1e3
+            for d in [int(x) for x in args.bwd_dbg.split(",") if x]:
+                h.set_debug(d)
+                extra[f"backward_us_dbg{d}"] = time_calls(h, reps, max(3, R // 4), backward) * 1e3
             for d in [int(x) for x in args.sddmm_dbg.split(",") if x]:
                 h.set_debug(d)
                 extra[f"sddmm_us_dbg{d}"] = time_calls(h, reps, max(3, R // 4), sddmm_only) * 1e3
