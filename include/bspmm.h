@@ -329,10 +329,14 @@ BSPMM_API bspmm_status_t bspmm_sddmm(bspmm_handle_t h, int32_t batch, int32_t k,
                                      const int32_t* sizes, const int32_t* row_ptr, const int32_t* col, const float* B,
                                      int64_t ldb, const float* G, int64_t ldg, float* out);
 
-/* Backward of bspmm_csr: grad_B (nullable) = A^T grad_C via an internal
- * transpose + the forward kernel (bitwise the fp32 storage-order sum over the
- * canonical A^T); grad_vals (nullable) = SDDMM(grad_C, B).  grad_B must not
- * alias grad_C.  total_rows / total_nnz: host sizes of the CSR. */
+/* Backward of bspmm_csr: grad_B (nullable) = A^T grad_C (bitwise the fp32
+ * storage-order sum over the canonical A^T); grad_vals (nullable) =
+ * SDDMM(grad_C, B).  With both requested on a streaming batch (more than 8
+ * matrices per SM, planner hints set, k <= 256, 16-byte aligned rows) one
+ * fused kernel computes both from grad_C staged once per matrix, forming
+ * A_i^T in shared memory; otherwise an internal transpose + the forward
+ * kernel, and the SDDMM.  Both give the same bits.  grad_B must not alias
+ * grad_C.  total_rows / total_nnz: host sizes of the CSR. */
 BSPMM_API bspmm_status_t bspmm_csr_backward(bspmm_handle_t h, int32_t batch, int32_t k, const int64_t* row_off,
                                             const int32_t* sizes, const int32_t* row_ptr, const int32_t* col,
                                             const float* vals, const float* B, int64_t ldb, const float* grad_C,
