@@ -25,6 +25,15 @@ $(LIB): $(CU_SRCS) $(HOST_SRCS) $(HDRS)
 	  2> build/ptxas.log || (cat build/ptxas.log; false)
 	@grep -E "registers|spill|smem" build/ptxas.log | sed 's/^ptxas info *: //' > build/ptxas_summary.txt || true
 
+# bounds-checked variant (device traps on violated index invariants; tests
+# load it with BSPMM_LIB=checked): the compute-sanitizer stand-in
+CHECKED   := $(PKG)/libbspmm_checked.so
+checked: $(CHECKED)
+$(CHECKED): $(CU_SRCS) $(HOST_SRCS) $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DBSPMM_CHECKED -shared -o $@ $(CU_SRCS) $(HOST_SRCS) -Xlinker -rpath=/usr/local/cuda/lib64 \
+	  2> build/ptxas_checked.log || (cat build/ptxas_checked.log; false)
+
 oracle: oracle/liboracle.so
 oracle/liboracle.so: oracle/oracle.c
 	$(CC) -O2 -std=c11 -fPIC -shared -fopenmp -ffp-contract=off -fno-fast-math -o $@ $< -lm
@@ -39,7 +48,7 @@ tools/probe/libfloor.so: tools/probe/floor.cu
 	$(NVCC) $(ARCH) -O3 -lineinfo -shared -Xcompiler -fPIC -o $@ $<
 
 clean:
-	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so
+	rm -f $(LIB) $(CHECKED) oracle/liboracle.so synth/libsynth.so
 	rm -rf build
 
-.PHONY: all lib oracle synth probes clean
+.PHONY: all lib checked oracle synth probes clean

@@ -7,7 +7,9 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbspmm.so")
+# BSPMM_LIB=checked selects the bounds-checked build (`make checked`): same ABI,
+# device-side index checks that trap (the compute-sanitizer stand-in)
+LIB_PATH = os.path.join(_HERE, "libbspmm_checked.so" if os.environ.get("BSPMM_LIB") == "checked" else "libbspmm.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bspmm.h")
 DEBUG_HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "bspmm_debug.h")
 

@@ -517,6 +517,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) sddmm_struct_kernel(int32_t ba
   auto stage_struct = [&](int buf, const SdMeta& d) {
     const int32_t n = rows_of(d);
     if (fits(n, d.ea, d.eb)) {
+      BSPMM_CHECK(n + 1 <= rcap && d.eb - d.ea <= ecap && d.ea >= 0);
       for (int32_t t = threadIdx.x; t <= n; t += blockDim.x) cp_async4(s_rp + buf * rcap + t, row_ptr + d.g + t);
       for (int32_t t = threadIdx.x; t < d.eb - d.ea; t += blockDim.x) cp_async4(s_col + buf * ecap + t, col + d.ea + t);
     }
@@ -590,6 +591,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) sddmm_struct_kernel(int32_t ba
           for (int v = 0; v < CH; ++v) gq[f][v] = gq[f + 1][v];
         if (r + PF * nw < n0) gload(r + PF * nw, gq[PF - 1]);
         const int32_t ea = rp[r] - e0a, eb = rp[r + 1] - e0a;
+        BSPMM_CHECK(0 <= ea && ea <= eb && eb <= e0b - e0a && eb <= ecap && r + 1 < rcap);
         // up to four entries per butterfly: the xor-16 step swaps pairs
         // (lanes < 16 keep entries 0-1, the others 2-3), the xor-8 step
         // swaps within the pair, xor 4, 2, 1 finish; lane 8q writes entry q
@@ -600,6 +602,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) sddmm_struct_kernel(int32_t ba
           for (int q = 0; q < 4; ++q) {
             p[q] = 0.f;
             if (q < m) {
+              BSPMM_CHECK(cs[e + q] >= 0 && cs[e + q] < n0 && (int64_t)n0 * k * 4 <= cap_bytes);
               const float* bp = Bs + cs[e + q] * k + 4 * lane;
 #pragma unroll
               for (int v = 0; v < CH; ++v) {
@@ -727,6 +730,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) backward_fused_kernel(
   auto stage_struct = [&](int buf, const SdMeta& d) {
     const int32_t n = rows_of(d);
     if (fits(n, d.ea, d.eb)) {
+      BSPMM_CHECK(n + 1 <= rcap && d.eb - d.ea <= ecap && d.ea >= 0);
       for (int32_t t = threadIdx.x; t <= n; t += blockDim.x) cp_async4(s_rp + buf * rcap + t, row_ptr + d.g + t);
       for (int32_t t = threadIdx.x; t < d.eb - d.ea; t += blockDim.x) {
         cp_async4(s_col + buf * ecap + t, col + d.ea + t);
@@ -798,7 +802,10 @@ __global__ void __launch_bounds__(kBwdThreads, 3) backward_fused_kernel(
       // shared atomics (the counters were zeroed at the end of the previous
       // matrix), a warp scan, then every entry's slot = its column's start +
       // the number of earlier entries of that column (stable)
-      for (int32_t e = threadIdx.x; e < nnz; e += blockDim.x) atomicAdd(&t_rp[cs[e] + 1], 1);
+      for (int32_t e = threadIdx.x; e < nnz; e += blockDim.x) {
+        BSPMM_CHECK(cs[e] >= 0 && cs[e] < n0 && n0 < rcap);
+        atomicAdd(&t_rp[cs[e] + 1], 1);
+      }
       __syncthreads();
       if (warp == 0) {  // inclusive scan of t_rp[1..n0] -> row pointers of A^T (t_rp[0] = 0)
         int32_t carry = 0;
@@ -830,6 +837,7 @@ __global__ void __launch_bounds__(kBwdThreads, 3) backward_fused_kernel(
           else hi = mid - 1;
         }
         const int32_t slot = t_rp[c] + rank;
+        BSPMM_CHECK(slot >= t_rp[c] && slot < t_rp[c + 1] && slot < nnz && lo >= 0 && lo < n0);
         t_row[slot] = lo;
         t_val[slot] = vs[e];
         t_pos[slot] = e;
@@ -847,8 +855,10 @@ __global__ void __launch_bounds__(kBwdThreads, 3) backward_fused_kernel(
 #pragma unroll
         for (int v = 0; v < CH; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
         const int32_t sa = t_rp[c], sb = t_rp[c + 1];
+        BSPMM_CHECK(0 <= sa && sa <= sb && sb <= nnz);
         for (int32_t s2 = sa; s2 < sb; s2 += 2) {
           const bool two = s2 + 1 < sb;  // warp-uniform
+          BSPMM_CHECK(t_row[s2] >= 0 && t_row[s2] < n0 && t_pos[s2] >= 0 && t_pos[s2] < nnz);
           const float* g0p = Gs + t_row[s2] * k + 4 * lane;
           const float* g1p = Gs + t_row[two ? s2 + 1 : s2] * k + 4 * lane;
           const float v0 = t_val[s2], v1 = two ? t_val[s2 + 1] : 0.f;

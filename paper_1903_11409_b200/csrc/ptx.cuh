@@ -4,6 +4,21 @@
 #pragma once
 #include <cstdint>
 
+// Bounds-checked build (make checked -> libbspmm_checked.so, loaded when
+// BSPMM_LIB=checked): BSPMM_CHECK traps on a violated index invariant, so a
+// bad shared- or global-memory index surfaces as a CUDA error in the tests
+// (compute-sanitizer stand-in).  Compiled out of the product library.
+#ifdef BSPMM_CHECKED
+#define BSPMM_CHECK(cond) \
+  do {                     \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define BSPMM_CHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace bspmm {
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {

@@ -89,6 +89,7 @@ __device__ __forceinline__ void tile_prefetch_b(const TileParams& p) {
   const int64_t g0 = ld_relaxed_s64(p.row_off + i);
   const int64_t g1 = p.sizes ? g0 + ld_relaxed_s32(p.sizes + i) : ld_relaxed_s64(p.row_off + i + 1);
   if (g1 <= g0 || g1 - g0 > (1 << 20)) return;
+  BSPMM_CHECK(p.b_lo < p.b_hi);
   if (threadIdx.x == 0) {
     prefetch_l2_clipped(reinterpret_cast<uint64_t>(p.B + g0 * p.ldb4), (uint64_t)(g1 - g0) * p.ldb4 * 16, p.b_lo,
                         p.b_hi);
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
   // cp.async.  Columns past k are zero-filled by TMA and never stored.
   const bool bst = n <= p.cap_rows;
   const bool tma = CB >= 8 && p.tma && bst;
+  BSPMM_CHECK(g0 >= 0 && n >= 0);
   // RT2 issued first (its loads are in flight while the B copies are issued;
   // they would otherwise queue behind the tile's bytes)
   int32_t z0 = 0, z1 = 0, rp0 = 0;
