@@ -1,3 +1,4 @@
+# ncu --set full of the fused backward at C5 (tools/probe/bwd_once.py): gpurun -- "bash tools/gpu_ncu_bwd.sh <tag>"
 set -u
 O=gpurun_out/nbw${1:-1}; mkdir -p $O
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:backward_fused -s 1 -c 1 \

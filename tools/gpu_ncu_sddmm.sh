@@ -1,3 +1,4 @@
+# ncu --set full of the standalone SDDMM at C5 (tools/probe/sddmm_once.py): gpurun -- "bash tools/gpu_ncu_sddmm.sh <tag> [dbg]"
 set -u
 O=gpurun_out/nsd${1:-1}; mkdir -p $O
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sddmm -s 2 -c 1 \

@@ -1,3 +1,5 @@
+# steady-state phase trace (kbench --trace) of one config with and without the pre-wait prefetch:
+#   gpurun -- "bash tools/gpu_pf_trace.sh <tag> <config>"
 set -u
 O=gpurun_out/pft${1:-1}; mkdir -p $O
 timeout 300 python tools/kbench.py --configs ${2:-4} --dbg 0,16777216 --trace > $O/kbench.jsonl 2> $O/kbench.err

@@ -1,4 +1,5 @@
-# quick A/B: kbench C4/C2 (twice) + a short bench line (clock sampling check)
+# quick A/B: kbench <configs> over debug-bit sets and tile column blocks + a short bench line:
+#   gpurun -- "bash tools/gpu_quick.sh <tag> <dbg list> <tile-cb list> <configs>"
 set -u
 O=gpurun_out/q${1:-1}; mkdir -p $O
 timeout 300 python tools/kbench.py --configs ${4:-4,2} --dbg ${2:-0,67108864} --tile-cbs ${3:-0,16} > $O/kbench.jsonl 2> $O/kbench.err
