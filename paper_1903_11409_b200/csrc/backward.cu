@@ -172,10 +172,167 @@ __global__ void __launch_bounds__(kTrWarps * 32) transpose_csr_kernel(int32_t ba
   }
 }
 
+// CTA-per-matrix transpose for small (latency-bound) batches: the warp
+// kernel above gives a whole matrix to one warp, so on C3 (200 matrices of
+// up to 300 rows / 1370 entries) 25 SMs work and the largest matrix's serial
+// passes set the time.  Here the 8 warps of a CTA split the matrix's entries
+// into 8 contiguous ranges: each warp counts its range per column (32 entries
+// at a time, equal columns grouped by __match_any_sync), a thread per column
+// turns the 8 counts into per-warp offsets and the column total, warp 0 scans
+// the totals into the A^T row pointers, and each warp scatters its range in
+// storage order (slot = column start + the earlier warps' count + the running
+// count within the warp) -- a stable counting sort: the same canonical order,
+// the same bits.  Matrices above the (hinted) shared-memory capacities run a
+// plain global-memory version of the same sort.
+constexpr int kTcWarps = kBwdThreads / 32;
+__global__ void __launch_bounds__(kBwdThreads) transpose_cta_kernel(int32_t batch, const int64_t* __restrict__ row_off,
+                                                                   const int32_t* __restrict__ sizes,
+                                                                   const int32_t* __restrict__ row_ptr,
+                                                                   const int32_t* __restrict__ col,
+                                                                   const float* __restrict__ vals,
+                                                                   int32_t* __restrict__ rowT, int32_t* __restrict__ colT,
+                                                                   float* __restrict__ valsT, int32_t rcap, int32_t ecap) {
+  extern __shared__ __align__(16) int32_t tc_smem[];
+  int32_t* cw_s = tc_smem;                   // [kTcWarps][rcap]: per-warp column counts -> cursors
+  int32_t* st_s = cw_s + kTcWarps * rcap;    // [rcap]: column totals -> absolute starts
+  int32_t* rp_s = st_s + rcap;               // [rcap]: row pointers relative to z0
+  int32_t* cs_s = rp_s + rcap;               // [ecap]: column ids
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int64_t i = blockIdx.x; i < batch; i += gridDim.x) {
+    const int64_t g0 = row_off[i], g1 = row_off[i + 1];
+    const int32_t n = sizes ? sizes[i] : (int32_t)(g1 - g0);
+    const int32_t z0 = row_ptr[g0], z1 = row_ptr[g0 + n], nnz = z1 - z0;
+    for (int64_t g = g0 + n + t; g < g1; g += blockDim.x) rowT[g] = z1;  // padding rows: empty
+    if (i == batch - 1 && t == 0) rowT[g1] = row_ptr[g1];
+    if (n + 1 <= rcap && nnz <= ecap) {
+      for (int32_t c = t; c < kTcWarps * rcap; c += blockDim.x) cw_s[c] = 0;
+      for (int32_t e = t; e < nnz; e += blockDim.x) cs_s[e] = __ldg(col + z0 + e);
+      for (int32_t r = t; r <= n; r += blockDim.x) rp_s[r] = __ldg(row_ptr + g0 + r) - z0;
+      __syncthreads();
+      const int32_t L = (nnz + kTcWarps - 1) / kTcWarps;
+      const int32_t w0 = min(nnz, warp * L), w1 = min(nnz, w0 + L);
+      int32_t* cw = cw_s + warp * rcap;
+      for (int32_t e0 = w0; e0 < w1; e0 += 32) {  // per-warp column counts
+        const int32_t e = e0 + lane;
+        const int32_t c = e < w1 ? cs_s[e] : -1 - lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, c);
+        if (e < w1 && (peers & lt) == 0) cw[c] += __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int32_t c = t; c < n; c += blockDim.x) {  // per-warp offsets within the column, column totals
+        int32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kTcWarps; ++w) {
+          const int32_t v = cw_s[w * rcap + c];
+          cw_s[w * rcap + c] = run;
+          run += v;
+        }
+        st_s[c] = run;
+      }
+      __syncthreads();
+      if (warp == 0) {  // exclusive scan of the totals -> absolute A^T row pointers
+        int32_t carry = z0;
+        for (int32_t c0 = 0; c0 < n; c0 += 32) {
+          const int32_t c = c0 + lane;
+          const int32_t v = c < n ? st_s[c] : 0;
+          int32_t x = v;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+          }
+          if (c < n) {
+            st_s[c] = carry + x - v;
+            rowT[g0 + c] = carry + x - v;
+          }
+          carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+      }
+      __syncthreads();
+      for (int32_t e0 = w0; e0 < w1; e0 += 32) {  // stable scatter of this warp's range
+        const int32_t e = e0 + lane;
+        const bool in = e < w1;
+        const int32_t c = in ? cs_s[e] : -1 - lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, c);
+        if (in) {
+          const int32_t slot = st_s[c] + cw[c] + __popc(peers & lt);
+          int32_t lo = 0, hi = n - 1;  // source row: the last r with rp[r] <= e (empty rows share rp)
+          while (lo < hi) {
+            const int32_t mid = (lo + hi + 1) >> 1;
+            if (rp_s[mid] <= e) lo = mid;
+            else hi = mid - 1;
+          }
+          BSPMM_CHECK(c >= 0 && c < n && slot >= z0 && slot < z1 && lo >= 0 && lo < n);
+          colT[slot] = lo;
+          valsT[slot] = __ldg(vals + z0 + e);  // bitwise move
+        }
+        __syncwarp();
+        if (in && (peers & lt) == 0) cw[c] += __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();  // shared memory reused by the next matrix
+      continue;
+    }
+    // above the capacities: the same counting sort on global memory (counters
+    // in rowT's own slots), ranks by a scan of the earlier entries
+    for (int32_t c = t; c < n; c += blockDim.x) rowT[g0 + c] = 0;
+    __syncthreads();
+    for (int32_t e = t; e < nnz; e += blockDim.x) atomicAdd(&rowT[g0 + __ldg(col + z0 + e)], 1);
+    __syncthreads();
+    if (warp == 0) {
+      int32_t carry = z0;
+      for (int32_t c0 = 0; c0 < n; c0 += 32) {
+        const int32_t c = c0 + lane;
+        const int32_t v = c < n ? rowT[g0 + c] : 0;
+        int32_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        if (c < n) rowT[g0 + c] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+    }
+    __syncthreads();
+    for (int32_t e = t; e < nnz; e += blockDim.x) {
+      const int32_t c = __ldg(col + z0 + e);
+      int32_t rank = 0;
+      for (int32_t q = 0; q < e; ++q) rank += __ldg(col + z0 + q) == c ? 1 : 0;
+      int32_t lo = 0, hi = n - 1;
+      while (lo < hi) {
+        const int32_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(row_ptr + g0 + mid) - z0 <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      const int32_t slot = rowT[g0 + c] + rank;
+      colT[slot] = lo;
+      valsT[slot] = __ldg(vals + z0 + e);
+    }
+    __syncthreads();
+  }
+}
+
 cudaError_t launch_transpose_csr(int32_t batch, const int64_t* row_off, const int32_t* sizes, const int32_t* row_ptr,
                                  const int32_t* col, const float* vals, int32_t* rowT, int32_t* colT, float* valsT,
                                  int32_t max_rows_hint, int64_t max_nnz_hint, int32_t num_sms, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
+  if (batch <= 8LL * num_sms && max_rows_hint > 0 && max_nnz_hint > 0) {
+    // small (latency-bound) batch: a CTA per matrix (C3 20 -> see DESIGN)
+    const int32_t rcap = (max_rows_hint + 1 + 3) & ~3;
+    const int32_t ecap = (int32_t)std::min<int64_t>((max_nnz_hint + 3) & ~3LL, 8192);
+    const int smem = ((kTcWarps + 2) * rcap + ecap) * 4;
+    if (smem <= 96 * 1024) {
+      cudaError_t e = cudaSuccess;
+      if (smem > 47 * 1024) e = cudaFuncSetAttribute(transpose_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      transpose_cta_kernel<<<batch, kBwdThreads, smem, s>>>(batch, row_off, sizes, row_ptr, col, vals, rowT, colT, valsT,
+                                                            rcap, ecap);
+      return cudaGetLastError();
+    }
+  }
   const int64_t need = ((int64_t)batch + kTrWarps - 1) / kTrWarps;
   const int grid = (int)std::min<int64_t>(need, (int64_t)num_sms * 8);
   // row-id capacity: the hinted largest matrix up to 1536 entries (no hint: search)

@@ -276,3 +276,38 @@ def test_backward_fused_streaming(h, k, ld):
         assert np.array_equal(gv.view(np.uint32), sep_v.view(np.uint32)), f"hints {rows}/{nnz}"
         ok, worst = oracle.check_bound(gv, rv, bv)
         assert ok, worst
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_transpose_cta_kernel_configs(h, cid):
+    """Small batches with planner hints take the CTA-per-matrix transpose:
+    bit-exact against the oracle's A^T, and the backward built on it bitwise
+    O3' (grad_B) / within the bound (grad_vals)."""
+    b = synth.config(cid)
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    try:
+        ort, oct_, ovt = check_transpose(h, b)
+        G = grad(b, cid + 20)
+        gB, gv = h.csr_backward(T(b.row_off), None, T(b.row_ptr), T(b.col), T(b.vals), T(b.B), T(G))
+        torch.cuda.synchronize()
+    finally:
+        h.set_hints(0, 0)
+    ref32 = oracle.spmm_f32(b.k, b.row_off, None, ort, oct_, ovt, G)
+    assert np.array_equal(gB.cpu().numpy().view(np.uint32), ref32.view(np.uint32))
+    rB, bB, rv, bv = oracle.backward(b.k, b.row_off, b.row_ptr, b.col, b.vals, b.B, G)
+    assert oracle.check_bound(gv.cpu().numpy(), rv, bv)[0]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_transpose_cta_kernel_adversarial(h, seed):
+    """Duplicates, empty rows and graphs, padded layouts (sizes < row_off
+    gaps via the sizes argument), matrices above the hinted capacities (the
+    kernel's global-memory path): bit-exact against the oracle."""
+    rng = np.random.default_rng(seed + 40)
+    b = synth.random_batch(rng, 300, 8, nmax=120, dmax=12, duplicates=True)
+    for rows, nnz in ((int(b.sizes.max()), int(b.nnz.max())), (32, 64), (int(b.sizes.max()), 100)):
+        h.set_hints(rows, nnz)
+        try:
+            check_transpose(h, b)
+        finally:
+            h.set_hints(0, 0)
