@@ -183,36 +183,27 @@ bspmm_status_t plan_for(bspmm_handle_t h, int32_t batch, int32_t k, bool aligned
 }  // namespace
 
 // The device allocation containing p (cuMemGetAddressRange through the
-// runtime's driver entry point), cached per handle: the kernels' pre-wait L2
-// prefetch of B clips its (possibly stale) addresses to it.
+// runtime's driver entry point): the kernels' pre-wait L2 prefetch clips its
+// (possibly stale) addresses to it.  Queried on every call -- a cached range
+// could outlive its allocation (freed, and a smaller one placed at the same
+// base) and let a prefetch reach unmapped memory.
 bool bspmm::alloc_range(bspmm_handle_t h, const void* p, uint64_t* lo, uint64_t* hi) {
-  const uint64_t a = reinterpret_cast<uint64_t>(p);
-  for (int q = 0; q < 16; ++q)
-    if (h->ar_lo[q] <= a && a < h->ar_hi[q]) {
-      *lo = h->ar_lo[q];
-      *hi = h->ar_hi[q];
-      return true;
-    }
-  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  (void)h;
+  static const PFN_cuMemGetAddressRange_v3020 range = []() -> PFN_cuMemGetAddressRange_v3020 {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess && fn)
-      range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
-    else
-      cudaGetLastError();
-  }
-  if (!range) return false;
+      return reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    cudaGetLastError();
+    return nullptr;
+  }();
+  if (!range || !p) return false;
   CUdeviceptr base = 0;
   size_t bytes = 0;
-  if (range(&base, &bytes, (CUdeviceptr)a) != CUDA_SUCCESS || bytes == 0) return false;
-  const int q = h->ar_next;
-  h->ar_next = (q + 1) & 15;
-  h->ar_lo[q] = *lo = (uint64_t)base;
-  h->ar_hi[q] = *hi = (uint64_t)base + bytes;
+  if (range(&base, &bytes, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS || bytes == 0) return false;
+  *lo = (uint64_t)base;
+  *hi = (uint64_t)base + bytes;
   return true;
 }
 

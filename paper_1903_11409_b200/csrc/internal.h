@@ -98,7 +98,7 @@ constexpr int32_t kDbgNoStructPrefetch = 1 << 25;
 // debug bit 536870912: backward of streaming batches by the separate kernels
 // (transpose + forward kernel, SDDMM) instead of the fused kernel
 constexpr int32_t kDbgNoFusedBackward = 1 << 29;
-// bspmm.cu: the device allocation containing p (cached per handle); false if unknown
+// bspmm.cu: the device allocation containing p (queried per call); false if unknown
 bool alloc_range(bspmm_handle_t h, const void* p, uint64_t* lo, uint64_t* hi);
 
 // kernels (.cu)
@@ -232,7 +232,4 @@ struct bspmm_handle_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_handoff = nullptr;  // bspmm_set_stream: new stream waits for the old one
   cudaEvent_t ev[64] = {};
-  // alloc_range cache: device allocations (base, end) seen as B
-  uint64_t ar_lo[16] = {}, ar_hi[16] = {};
-  int ar_next = 0;
 };
