@@ -90,6 +90,7 @@ struct CsrArgs {
   // the allocations of the structure arrays (CSR: row_ptr, col, vals; COO:
   // -, idx, vals), for the same prefetch of the matrix's structure
   uint64_t s_lo[3] = {}, s_hi[3] = {};
+  uint64_t g_lo = 0, g_hi = 0;  // SDDMM mode: grad_C's allocation
 };
 // debug bit 16777216: no pre-wait L2 prefetch of B (tile kernels)
 constexpr int32_t kDbgNoPrewaitPrefetch = 1 << 24;
@@ -232,4 +233,5 @@ struct bspmm_handle_s {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_handoff = nullptr;  // bspmm_set_stream: new stream waits for the old one
   cudaEvent_t ev[64] = {};
+  bool in_backward = false;  // csr_backward's grad_B SpMM is running (no pre-wait prefetch)
 };

@@ -70,6 +70,7 @@ struct SpmmParams {
   // allocations (CSR row_ptr, col, vals; COO -, idx, vals); b_hi == 0: off
   uint64_t b_lo, b_hi;
   uint64_t s_lo[3], s_hi[3];
+  uint64_t g_lo, g_hi;  // SDDMM mode: grad_C's allocation (its rows are prefetched too)
 };
 
 // GCN epilogue (NEXT-1, PAPER.md Fig. algo:graph_conv_batched): A (U + 1 b^T)
@@ -1226,6 +1227,9 @@ __device__ __forceinline__ void prefetch_units(const SpmmParams& p) {
   if (g1 <= g0 || g1 - g0 > (1 << 20)) return;
   prefetch_l2_clipped(reinterpret_cast<uint64_t>(p.B + g0 * p.ldb), (uint64_t)(g1 - g0) * p.ldb * 4, p.b_lo,
                       p.b_hi);
+  if (p.g_hi)  // SDDMM mode: the grad_C rows the consumers read from global memory
+    prefetch_l2_clipped(reinterpret_cast<uint64_t>(p.G + g0 * p.ldg), (uint64_t)(g1 - g0) * p.ldg * 4, p.g_lo,
+                        p.g_hi);
   if (COO) {
     if (!p.s_hi[1]) return;
     const int64_t z0 = ld_relaxed_s64(p.nnz_off + i), z1 = ld_relaxed_s64(p.nnz_off + i + 1);
@@ -1378,9 +1382,11 @@ cudaError_t launch_spmm_csr(const CsrArgs& a, const bspmm_plan_t& plan, cudaStre
   sp.err = a.err;  // C4: 8.4 vs 9.0 us; C5: 835 vs 849
   sp.cvt_warps = a.cvt_warps;
   sp.coo_rows = plan.max_rows;
-  const bool pf = plan.units <= 8LL * plan.grid && epi != 3;
+  const bool pf = plan.units <= 8LL * plan.grid && (epi != 3 || a.g_hi);
   sp.b_lo = pf ? a.b_lo : 0;
   sp.b_hi = pf ? a.b_hi : 0;
+  sp.g_lo = pf && epi == 3 ? a.g_lo : 0;
+  sp.g_hi = pf && epi == 3 ? a.g_hi : 0;
   for (int q = 0; q < 3; ++q) {
     sp.s_lo[q] = pf ? a.s_lo[q] : 0;
     sp.s_hi[q] = pf ? a.s_hi[q] : 0;
