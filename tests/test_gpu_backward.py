@@ -311,3 +311,49 @@ def test_transpose_cta_kernel_adversarial(h, seed):
             check_transpose(h, b)
         finally:
             h.set_hints(0, 0)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_backward_padded_layout(h, fused):
+    """row_off with gaps + sizes (padding rows between the matrices), a
+    streaming batch (1500 matrices) so that both adjoints take the fused
+    kernel (or, with debug bit 29, the separate kernels): grad_B's matrix rows
+    bitwise O3' over the oracle's A^T, padding rows never written (NaN stays),
+    grad_vals within the bound."""
+    rng = np.random.default_rng(77)
+    b = synth.random_batch(rng, 1500, 64, nmax=30, dmax=5, allow_empty_graphs=False, duplicates=True)
+    gap = 3
+    ro = np.array([int(b.row_off[i]) + gap * i for i in range(b.batch + 1)], dtype=np.int64)
+    Np = int(ro[-1])
+    rp = np.zeros(Np + 1, dtype=np.int32)
+    Bp = np.zeros((Np, 64), dtype=np.float32)
+    G = grad(b, 78)
+    Gp = np.zeros((Np, 64), dtype=np.float32)
+    for i in range(b.batch):
+        n = int(b.sizes[i])
+        rp[ro[i]:ro[i] + n + 1] = b.row_ptr[b.row_off[i]:b.row_off[i] + n + 1]
+        rp[ro[i] + n:ro[i + 1]] = b.row_ptr[b.row_off[i + 1]]
+        Bp[ro[i]:ro[i] + n] = b.B[b.row_off[i]:b.row_off[i + 1]]
+        Gp[ro[i]:ro[i] + n] = G[b.row_off[i]:b.row_off[i + 1]]
+    rp[Np] = b.row_ptr[-1]
+    h.set_hints(int(b.sizes.max()), int(b.nnz.max()))
+    h.set_debug(0 if fused else FUSED_OFF)
+    try:
+        gB = torch.full((Np, 64), float("nan"), device=DEV)
+        gv = torch.full((b.n_nnz,), float("nan"), device=DEV)
+        h.csr_backward(T(ro), T(b.sizes), T(rp), T(b.col), T(b.vals), T(Bp), T(Gp), grad_B=gB, grad_vals=gv)
+        torch.cuda.synchronize()
+    finally:
+        h.set_debug(0)
+        h.set_hints(0, 0)
+    gB, gv = gB.cpu().numpy(), gv.cpu().numpy()
+    ort, oct_, ovt = oracle.csr_transpose(b.row_off, None, b.row_ptr, b.col, b.vals)
+    ref32 = oracle.spmm_f32(64, b.row_off, None, ort, oct_, ovt, G)
+    for i in range(b.batch):
+        n = int(b.sizes[i])
+        assert np.array_equal(gB[ro[i]:ro[i] + n].view(np.uint32),
+                              ref32[b.row_off[i]:b.row_off[i + 1]].view(np.uint32)), i
+        assert np.all(np.isnan(gB[ro[i] + n:ro[i + 1]])), i
+    rv, bv = oracle.sddmm(64, b.row_off, None, b.row_ptr, b.col, b.B, G)
+    ok, worst = oracle.check_bound(gv, rv, bv)
+    assert ok, worst
