@@ -6,15 +6,22 @@
 //   dL/dval_e = <G[row_e], B[col_e]> (SDDMM at A's sparsity pattern)
 // (the standard adjoints).
 //
-// * transpose: one warp per matrix, a stable counting sort of its entries by
-//   column in shared memory (counts, warp scan, then a scatter in storage
-//   order in which equal columns rank by __match_any_sync), so A^T comes out
-//   in canonical (row, col, original position) order, bit-exact against the
-//   oracle.  Columns are counted in windows of WIN, so any n_i works.
-//   (Replaces an expand-to-COO + general device COO->CSR pair: C5 440 us.)
-// * SDDMM: one CTA per matrix, a warp per row; each lane holds 128-bit
-//   chunks of G's row, multiplies B's row chunks for every entry and the warp
-//   reduces with shuffles (fixed butterfly order: deterministic).
+// * transpose: a stable counting sort of each matrix's entries by column
+//   (counts, scan, then a scatter in storage order in which equal columns
+//   rank by __match_any_sync), so A^T comes out in canonical (row, col,
+//   original position) order, bit-exact against the oracle -- one warp per
+//   matrix (transpose_csr_kernel; columns counted in windows of WIN, so any
+//   n_i works), or, for small batches with hints, one CTA per matrix whose 8
+//   warps split the entries (transpose_cta_kernel).
+// * SDDMM: a warp per row; each lane holds 128-bit chunks of G's row,
+//   multiplies B's row chunks (B_i staged in shared memory) for every entry
+//   and the warp reduces with shuffles (fixed butterfly order: deterministic)
+//   -- sddmm_struct_kernel (streaming batches: the CSR slice double-buffered
+//   in shared memory by cp.async), sddmm_staged_kernel (the round-1 kernel,
+//   k > 256), sddmm_kernel (unaligned / scalar).
+// * backward_fused_kernel (streaming batches, both adjoints): grad_C_i staged
+//   once feeds grad_B = A^T grad_C (A_i^T formed in shared memory) and the
+//   SDDMM.
 #include <algorithm>
 #include <cstdint>
 
