@@ -654,7 +654,8 @@ BSPMM_API bspmm_status_t bspmm_coo(bspmm_handle_t h, int32_t batch, int32_t k, c
       plan.smem_bytes = TL.smem;
       plan.max_rows = h->hint_rows;
       h->last_plan = plan;
-      CsrArgs a{batch, k, ro, sizes, nullptr, nullptr, vals, B, ldb, C, ldc, h->trace, h->dbg, nullptr};
+      const TmaMaps* maps = (TL.cb >= 8 && !(h->dbg & 32768)) ? tma_maps(h, B, k, ldb, 4 * TL.cb) : nullptr;
+      CsrArgs a{batch, k, ro, sizes, nullptr, nullptr, vals, B, ldb, C, ldc, h->trace, h->dbg, maps};
       a.coo_nnz_off = nnz_off;
       a.coo_idx = idx;
       a.err = h->dev_flag;

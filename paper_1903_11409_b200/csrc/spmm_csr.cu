@@ -1294,7 +1294,7 @@ static cudaError_t launch_t(const SpmmParams& sp, const TmaMaps& maps, const bsp
   static thread_local int configured_bytes[64] = {};  // per device
   int dev = 0;
   cudaGetDevice(&dev);
-  if (plan.smem_bytes > 48 * 1024 && configured_bytes[dev & 63] < plan.smem_bytes) {
+  if (plan.smem_bytes > 47 * 1024 && configured_bytes[dev & 63] < plan.smem_bytes) {  // dynamic + static above 48 KB
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);
     if (e != cudaSuccess) return e;
     configured_bytes[dev & 63] = plan.smem_bytes;

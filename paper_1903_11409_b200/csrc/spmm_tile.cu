@@ -384,8 +384,10 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_kernel(const TileParam
 // then a thread per row orders its segment by the key (col << 16) | position
 // (a sorting network up to 8 entries, rank counting beyond).
 template <int CB>
-__global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileParams p) {
+__global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileParams p,
+                                                                     const __grid_constant__ TmaMaps maps) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
   float4* Bs = reinterpret_cast<float4*>(smem);
   int32_t* rp_s = reinterpret_cast<int32_t*>(smem + p.rp_off);
   int32_t* col_s = reinterpret_cast<int32_t*>(smem + p.col_off);
@@ -399,6 +401,15 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileP
   const int32_t c0 = (int32_t)(blockIdx.x - (uint32_t)i * (uint32_t)p.tiles) * CB;
   const int32_t cw = min(CB, p.k4 - c0);
   tile_trace(p, 0);
+  const bool tma = CB >= 8 && p.tma;  // B by 2-D tensor TMA (as the CSR tile kernel), else cp.async
+  if (tma) {  // before the wait: overlaps the previous kernel's tail
+    if (t == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+    if (t >= 32 && t < 32 + kTmaMaps && !(p.dbg_bits & 1)) prefetch_tensormap(&maps.m[t - 32]);
+    __syncthreads();
+  }
   tile_prefetch_b(p);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -420,7 +431,19 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileP
     cp_async4(rv + e, p.vals + z0 + e);
   }
   cp_async_commit();
-  {
+  if (tma) {
+    if (t < 32) {  // popcount(n) boxes of 2^b rows, the higher bits first
+      if (t == 0) mbar_arrive_expect_tx(&bar, (uint32_t)n * CB * 16u);
+      __syncwarp();
+      const int32_t big = n >> 8, rem = n & 255;
+      for (int32_t q = t - 8; q >= 0 && q < big; q += 24)
+        tma_load_2d(Bs + (size_t)q * 256 * CB, &maps.m[kTmaMaps - 1], c0 * 4, (int32_t)(g0 + q * 256), &bar);
+      if (t < 8 && (rem & (1 << t))) {
+        const int32_t r0 = big * 256 + (rem >> (t + 1) << (t + 1));
+        tma_load_2d(Bs + (size_t)r0 * CB, &maps.m[t], c0 * 4, (int32_t)(g0 + r0), &bar);
+      }
+    }
+  } else {
     const float4* src = p.B + g0 * p.ldb4 + c0;
     const int32_t cells = n * cw;
     if (cw == CB) {
@@ -433,7 +456,7 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileP
       }
     }
   }
-  cp_async_commit();
+  cp_async_commit();  // (an empty group with TMA staging)
   for (int32_t r = t; r < n; r += kTileThreads) cnt[r] = 0;
   tile_trace(p, 3);
   cp_async_wait_group<1>();  // this thread's slice copies
@@ -512,8 +535,13 @@ __global__ void __launch_bounds__(kTileThreads) spmm_tile_coo_kernel(const TileP
     }
   }
   tile_trace(p, 4);
-  cp_async_wait_all();  // the B tile
-  __syncthreads();
+  if (tma) {
+    __syncthreads();  // the converted structure
+    mbar_wait(&bar, 0);
+  } else {
+    cp_async_wait_all();  // the B tile
+    __syncthreads();
+  }
   tile_trace(p, 5);
   tile_rows<CB, 0, true, true>(p, Bs, rp_s, col_s, val_s, g0, n, c0, cw);
   tile_trace(p, 6);
@@ -586,7 +614,7 @@ static cudaError_t launch_tile_t(const TileParams& tp, const TmaMaps& maps, cons
   static thread_local int configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (L.smem > 48 * 1024 && configured[dev & 63] < L.smem) {
+  if (L.smem > 47 * 1024 && configured[dev & 63] < L.smem) {  // dynamic + static above the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
     configured[dev & 63] = L.smem;
@@ -617,12 +645,12 @@ static cudaError_t launch_tile_e(const TileParams& tp, const TmaMaps& m, const T
 }
 
 template <int CB>
-static cudaError_t launch_tile_coo_t(const TileParams& tp, const TileLayout& L, cudaStream_t s) {
+static cudaError_t launch_tile_coo_t(const TileParams& tp, const TmaMaps& m, const TileLayout& L, cudaStream_t s) {
   auto kern = spmm_tile_coo_kernel<CB>;
   static thread_local int configured[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (L.smem > 48 * 1024 && configured[dev & 63] < L.smem) {
+  if (L.smem > 47 * 1024 && configured[dev & 63] < L.smem) {  // dynamic + static above the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem);
     if (e != cudaSuccess) return e;
     configured[dev & 63] = L.smem;
@@ -637,7 +665,7 @@ static cudaError_t launch_tile_coo_t(const TileParams& tp, const TileLayout& L, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tp);
+  return cudaLaunchKernelEx(&cfg, kern, tp, m);
 }
 
 cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t s) {
@@ -686,19 +714,19 @@ cudaError_t launch_spmm_tile(const CsrArgs& a, const TileLayout& L, cudaStream_t
     tp.s_lo[q] = a.s_lo[q];
     tp.s_hi[q] = a.s_hi[q];
   }
+  static const TmaMaps no_maps{};
+  const TmaMaps& m = a.maps ? *a.maps : no_maps;
   if (a.coo_nnz_off) {  // SparseTensor input: the converting variant (row_off required)
     if (!a.row_off || !a.err || a.bias != nullptr || a.accumulate != 0) return cudaErrorInvalidValue;
     switch (L.cb) {
-      case 1: return launch_tile_coo_t<1>(tp, L, s);
-      case 2: return launch_tile_coo_t<2>(tp, L, s);
-      case 4: return launch_tile_coo_t<4>(tp, L, s);
-      case 8: return launch_tile_coo_t<8>(tp, L, s);
-      case 16: return launch_tile_coo_t<16>(tp, L, s);
-      default: return launch_tile_coo_t<32>(tp, L, s);
+      case 1: return launch_tile_coo_t<1>(tp, m, L, s);
+      case 2: return launch_tile_coo_t<2>(tp, m, L, s);
+      case 4: return launch_tile_coo_t<4>(tp, m, L, s);
+      case 8: return launch_tile_coo_t<8>(tp, m, L, s);
+      case 16: return launch_tile_coo_t<16>(tp, m, L, s);
+      default: return launch_tile_coo_t<32>(tp, m, L, s);
     }
   }
-  static const TmaMaps no_maps{};
-  const TmaMaps& m = a.maps ? *a.maps : no_maps;
   if (a.bias != nullptr || a.accumulate != 0) return cudaErrorInvalidValue;  // no GCN epilogue here (gcn_fused.cu)
   return launch_tile_e<0>(tp, m, L, s);
 }
